@@ -1,0 +1,121 @@
+/* sglgpu -- C ABI of the B200 (sm_100a) SGL Fourier transform library.
+ *
+ * This is the drop-in boundary for the reference's hot path, the fast SGL
+ * transform pair of /root/reference/proj/core:
+ *
+ *   SglCoefficients fsglft(const SampleGrid&, const TransformPlan&, unsigned threads)
+ *   SampleGrid      ifsglft(const SglCoefficients&, const TransformPlan&, unsigned threads)
+ *       (include/sgl/sgl_transform.hpp:71-76, bodies src/sgl_transform.cpp:274-348)
+ *
+ * The reference has no FFI; its interface is that C++ API.  The C++ mirror of it
+ * lives in include/sgl_b200/sgl_transform.hpp and is implemented on top of the
+ * entry points below, which is also what a ctypes / cgo / JNI binding would bind
+ * (see INTEGRATION.md).  Plain pointers and sizes only.
+ *
+ * Data layouts are the reference's (indexing.hpp:8-40):
+ *   samples       psi-order,   psi = 4B^2 i + 2B j + k,  8B^3 complex per function
+ *   coefficients  omega-order, omega = n(n-1)(2n-1)/6 + l(l+1) + m,
+ *                 B(B+1)(2B+1)/6 complex per function
+ * A complex value is two doubles (re, im), i.e. std::complex<double> /
+ * cuDoubleComplex.  A batch is `batch` functions stored back to back.
+ *
+ * Errors: every entry returns SGLGPU_OK (0) or a nonzero status; the message of
+ * the most recent failure on the calling thread is sglgpu_last_error().
+ * Shape errors are SGLGPU_EINVAL (the C++ wrapper maps them to
+ * std::invalid_argument, as the reference throws at sgl_transform.cpp:18-35).
+ */
+#ifndef SGLGPU_H
+#define SGLGPU_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    SGLGPU_OK = 0,
+    SGLGPU_EINVAL = 1,  /* bad argument / shape (reference: std::invalid_argument) */
+    SGLGPU_ECUDA = 2,   /* CUDA runtime error (reference: n/a; C++ wrapper: std::runtime_error) */
+    SGLGPU_ENOMEM = 3,  /* device allocation failed */
+    SGLGPU_ENODEV = 4   /* no usable CUDA device */
+};
+
+enum {
+    SGLGPU_MEM_HOST = 0,   /* pointers are host memory; the call copies in and out and
+                              returns after the result is in host memory */
+    SGLGPU_MEM_DEVICE = 1  /* pointers are device memory on the plan's device; the call is
+                              asynchronous on `stream` */
+};
+
+typedef struct sglgpu_plan sglgpu_plan;
+
+/* Everything TransformPlan::assemble consumes that is not generated in closed
+ * form (sgl_transform.cpp:52-88): the order-2B half-range Hermite rule
+ * (RadialRule r, a_mod; quadrature.hpp:27-32) and the calibrated polar weights
+ * (SphericalRule b_cal; quadrature.hpp:13-20).  The library derives cos(theta_j),
+ * the normalized Legendre table and the radial tables from these, in long
+ * double on the host, once per plan, and uploads them. */
+typedef struct {
+    int bandlimit;        /* B, 1 <= B <= 256 */
+    const double* r;      /* 2B radial nodes, increasing */
+    const double* a_mod;  /* 2B modified radial weights a * e^{r^2} * r^2 */
+    const double* b_cal;  /* 2B polar weights; NULL = closed form of quadrature.cpp:189-211 */
+    int device;           /* CUDA device ordinal; -1 = current device */
+} sglgpu_plan_desc;
+
+/* Creates a plan: generates and uploads the tables.  Cost O(B^3) host time. */
+int sglgpu_plan_create(const sglgpu_plan_desc* desc, sglgpu_plan** out);
+int sglgpu_plan_destroy(sglgpu_plan* plan);
+int sglgpu_plan_bandlimit(const sglgpu_plan* plan);
+/* Bytes of device memory held by the plan's tables. */
+size_t sglgpu_plan_table_bytes(const sglgpu_plan* plan);
+
+/* Forward transform (fsglft) of `batch` functions: samples -> coefficients. */
+int sglgpu_forward(sglgpu_plan* plan, const double* samples, double* coeffs, size_t batch,
+                   int mem_kind, void* stream);
+
+/* Inverse transform (ifsglft) of `batch` functions: coefficients -> samples. */
+int sglgpu_inverse(sglgpu_plan* plan, const double* coeffs, double* samples, size_t batch,
+                   int mem_kind, void* stream);
+
+/* Stage entry points (device memory only, asynchronous on `stream`), used by the
+ * multi-GPU shell / (l, m) decomposition.  `shells` is the nu-major intermediate
+ * S[nu][f][i] (nu = l(l+1)+m, f < batch, i < shell_count), i.e. the transpose of
+ * the reference's shells[i][nu] buffer (sgl_transform.cpp:281, 319).
+ *   spherical_forward: samples of shells [shell_begin, shell_begin+shell_count)
+ *                      (psi-order slice, per function 4B^2*shell_count complex,
+ *                      function stride `sample_stride` complex) -> shells
+ *   radial_forward:    shells (shell_count == 2B) for degrees l in [l_begin, l_end)
+ *                      -> coefficients (omega-order, function stride Omega)
+ *   radial_inverse / spherical_inverse: the mirror images. */
+int sglgpu_spherical_forward(sglgpu_plan* plan, const double* samples, size_t sample_stride,
+                             double* shells, int shell_begin, int shell_count, size_t batch,
+                             void* stream);
+int sglgpu_radial_forward(sglgpu_plan* plan, const double* shells, double* coeffs, int l_begin,
+                          int l_end, size_t batch, void* stream);
+int sglgpu_radial_inverse(sglgpu_plan* plan, const double* coeffs, double* shells, int l_begin,
+                          int l_end, size_t batch, void* stream);
+int sglgpu_spherical_inverse(sglgpu_plan* plan, const double* shells, double* samples,
+                             size_t sample_stride, int shell_begin, int shell_count,
+                             size_t batch, void* stream);
+
+/* Number of kernels the most recent forward/inverse call on this plan launched
+ * (for the bench's gpu_launches count). */
+int sglgpu_last_launch_count(const sglgpu_plan* plan);
+
+const char* sglgpu_last_error(void);
+
+/* Host-only (no CUDA) copy of the plan tables the kernels stream, for tests:
+ * with all output pointers NULL only sizes[0..2] (doubles in the Legendre,
+ * forward-radial and inverse-radial tables) are filled.  Offsets arrays have
+ * 2B+1 (Legendre, per (|m|, parity)) and B+1 (radial, per l) entries. */
+int sglgpu_host_tables(int B, const double* r, const double* a_mod, const double* bcal,
+                       long long* sizes, double* legendre, long long* legendre_off,
+                       double* radial_fwd, long long* radial_fwd_off, double* radial_inv,
+                       long long* radial_inv_off);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGLGPU_H */

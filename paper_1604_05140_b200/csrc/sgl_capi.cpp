@@ -1,0 +1,443 @@
+// C ABI of the B200 SGL transform (include/sglgpu.h): plans, device tables,
+// workspaces, tile schedules and the stage sequences of fsglft / ifsglft
+// (sgl_transform.cpp:274-348).  No CPU compute path: every transform runs the
+// sm_100a kernels of sgl_kernels.cu.
+#include "sglgpu.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "sgl_kernels.cuh"
+#include "sgl_tables.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Fail{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        fail(e == cudaErrorMemoryAllocation ? SGLGPU_ENOMEM : SGLGPU_ECUDA,
+             std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+void ck_launch(int n, const char* what) {
+    if (n < 0) ck(cudaGetLastError(), what);
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return SGLGPU_OK;
+    } catch (const Fail& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return SGLGPU_ENOMEM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return SGLGPU_ECUDA;
+    }
+}
+
+long long coefficient_count(int B) { return (long long)B * (B + 1) * (2 * B + 1) / 6; }
+long long sample_count(int B) { return 8LL * B * B * B; }
+
+template <class T>
+T* dev_upload(const std::vector<T>& h) {
+    T* d = nullptr;
+    const size_t bytes = std::max<size_t>(sizeof(T), h.size() * sizeof(T));
+    ck(cudaMalloc(&d, bytes), "cudaMalloc(table)");
+    if (!h.empty()) ck(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    return d;
+}
+
+struct DevBuf {
+    double* p = nullptr;
+    size_t cap = 0;  // doubles
+    void ensure(size_t n) {
+        if (n <= cap) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        ck(cudaMalloc(&p, n * sizeof(double)), "cudaMalloc(workspace)");
+        cap = n;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+enum Kind { kLegFwd = 0, kLegInv = 1, kRadFwd = 2, kRadInv = 3 };
+
+}  // namespace
+
+struct sglgpu_plan {
+    int B = 0;
+    int device = 0;
+    size_t table_bytes = 0;
+    double* d_tw = nullptr;
+    double* d_bcal = nullptr;
+    double* d_leg = nullptr;
+    long long* d_leg_off = nullptr;
+    double* d_W = nullptr;
+    long long* d_W_off = nullptr;
+    double* d_V = nullptr;
+    long long* d_V_off = nullptr;
+    DevBuf G, S, in, out;
+    std::map<std::tuple<int, int, int, int, int>, std::pair<sglk::Tile*, int>> tiles;
+    std::mutex mu;
+    int last_launches = 0;
+};
+
+namespace {
+
+// Host-side mirror of the per-problem shapes in sgl_kernels.cu.
+void problem_shape(Kind kind, int B, int batch, long long NB, int pid, int& M, int& N, int& K) {
+    switch (kind) {
+        case kLegFwd: {
+            const int am = pid >> 1, r = B - am - (pid & 1);
+            M = r > 0 ? (r + 1) / 2 : 0;
+            N = am == 0 ? (int)NB : 2 * (int)NB;
+            K = B;
+            break;
+        }
+        case kLegInv: {
+            const int am = pid >> 1, r = B - am - (pid & 1);
+            M = B;
+            N = am == 0 ? (int)NB : 2 * (int)NB;
+            K = r > 0 ? (r + 1) / 2 : 0;
+            break;
+        }
+        case kRadFwd:
+            M = B - pid;
+            N = (2 * pid + 1) * batch * 2;
+            K = 2 * B;
+            break;
+        case kRadInv:
+            M = 2 * B;
+            N = (2 * pid + 1) * batch * 2;
+            K = B - pid;
+            break;
+    }
+}
+
+// Tile list for one grouped contraction, heaviest K first, cached per shape.
+std::pair<sglk::Tile*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int SC, int lo, int hi) {
+    const auto key = std::make_tuple((int)kind, batch, SC, lo, hi);
+    auto it = p->tiles.find(key);
+    if (it != p->tiles.end()) return it->second;
+    const int B = p->B;
+    const long long NB = 2LL * batch * SC;
+    std::vector<sglk::Tile> v;
+    int plo = lo, phi = hi;
+    if (kind == kLegFwd || kind == kLegInv) {
+        plo = 0;
+        phi = 2 * B;
+    }
+    for (int pid = plo; pid < phi; ++pid) {
+        int M, N, K;
+        problem_shape(kind, B, batch, NB, pid, M, N, K);
+        if (M <= 0 || N <= 0) continue;
+        if (K <= 0 && kind != kLegInv) continue;  // LegInv with K = 0 must still write zeros
+        for (int m0 = 0; m0 < M; m0 += sglk::kBM)
+            for (int n0 = 0; n0 < N; n0 += sglk::kBN) v.push_back({pid, m0, n0, K});
+    }
+    std::stable_sort(v.begin(), v.end(), [](const sglk::Tile& a, const sglk::Tile& b) { return a.pad > b.pad; });
+    sglk::Tile* d = nullptr;
+    if (!v.empty()) d = dev_upload(v);
+    const auto res = std::make_pair(d, (int)v.size());
+    p->tiles[key] = res;
+    return res;
+}
+
+void set_device(sglgpu_plan* p) { ck(cudaSetDevice(p->device), "cudaSetDevice"); }
+
+// Largest batch chunk whose G + S workspaces stay under ~6 GiB.
+size_t batch_chunk(int B, size_t batch) {
+    const size_t per = (size_t)(16 + 4) * B * B * B * sizeof(double);  // G + S per function
+    const size_t budget = (size_t)6 << 30;
+    return std::max<size_t>(1, std::min(batch, budget / per));
+}
+
+// Stage sequences on device memory.  X: samples (function stride Psi complex),
+// C: coefficients (function stride Omega complex).
+int forward_device(sglgpu_plan* p, const double* X, double* C, int nb, cudaStream_t st) {
+    const int B = p->B;
+    sglk::Geo g{B, 2 * B, nb, 2LL * nb * 2 * B};
+    p->G.ensure((size_t)16 * B * B * B * nb);
+    p->S.ensure((size_t)4 * B * B * B * nb);
+    int n = 0, k;
+    k = sglk::launch_az_forward(g, X, 2 * (size_t)sample_count(B), p->G.p, p->d_bcal, p->d_tw, st);
+    ck_launch(k, "az_forward");
+    n += k;
+    auto lt = tiles_for(p, kLegFwd, nb, 2 * B, 0, 2 * B);
+    k = sglk::launch_legendre_forward(g, p->G.p, p->S.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+    ck_launch(k, "legendre_forward");
+    n += k;
+    auto rt = tiles_for(p, kRadFwd, nb, 2 * B, 0, B);
+    k = sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, p->S.p, C, p->d_W, p->d_W_off,
+                                    rt.first, rt.second, st);
+    ck_launch(k, "radial_forward");
+    n += k;
+    return n;
+}
+
+int inverse_device(sglgpu_plan* p, const double* C, double* X, int nb, cudaStream_t st) {
+    const int B = p->B;
+    sglk::Geo g{B, 2 * B, nb, 2LL * nb * 2 * B};
+    p->G.ensure((size_t)16 * B * B * B * nb);
+    p->S.ensure((size_t)4 * B * B * B * nb);
+    int n = 0, k;
+    auto rt = tiles_for(p, kRadInv, nb, 2 * B, 0, B);
+    k = sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, 0}, C, p->S.p, p->d_V, p->d_V_off,
+                                    rt.first, rt.second, st);
+    ck_launch(k, "radial_inverse");
+    n += k;
+    auto lt = tiles_for(p, kLegInv, nb, 2 * B, 0, 2 * B);
+    k = sglk::launch_legendre_inverse(g, p->S.p, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+    ck_launch(k, "legendre_inverse");
+    n += k;
+    k = sglk::launch_az_inverse(g, p->G.p, X, 2 * (size_t)sample_count(B), p->d_tw, st);
+    ck_launch(k, "az_inverse");
+    n += k;
+    return n;
+}
+
+void check_plan(const sglgpu_plan* p) {
+    if (!p) fail(SGLGPU_EINVAL, "sglgpu: null plan");
+}
+
+int run(sglgpu_plan* p, const double* in, double* out, size_t batch, int mem_kind, void* stream,
+        bool forward) {
+    return guarded([&] {
+        check_plan(p);
+        if (mem_kind != SGLGPU_MEM_HOST && mem_kind != SGLGPU_MEM_DEVICE)
+            fail(SGLGPU_EINVAL, "sglgpu: unknown mem_kind");
+        if (batch == 0) return;
+        if (!in || !out) fail(SGLGPU_EINVAL, "sglgpu: null data pointer");
+        std::lock_guard<std::mutex> lock(p->mu);
+        set_device(p);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int B = p->B;
+        const size_t psi = 2 * (size_t)sample_count(B), om = 2 * (size_t)coefficient_count(B);
+        const size_t in_len = forward ? psi : om, out_len = forward ? om : psi;
+        const size_t chunk = batch_chunk(B, batch);
+        int launches = 0;
+        if (mem_kind == SGLGPU_MEM_DEVICE) {
+            for (size_t b0 = 0; b0 < batch; b0 += chunk) {
+                const int nb = (int)std::min(chunk, batch - b0);
+                launches += forward ? forward_device(p, in + b0 * in_len, out + b0 * out_len, nb, st)
+                                    : inverse_device(p, in + b0 * in_len, out + b0 * out_len, nb, st);
+            }
+        } else {
+            p->in.ensure(in_len * chunk);
+            p->out.ensure(out_len * chunk);
+            for (size_t b0 = 0; b0 < batch; b0 += chunk) {
+                const int nb = (int)std::min(chunk, batch - b0);
+                ck(cudaMemcpyAsync(p->in.p, in + b0 * in_len, nb * in_len * sizeof(double),
+                                   cudaMemcpyHostToDevice, st),
+                   "H2D");
+                launches += forward ? forward_device(p, p->in.p, p->out.p, nb, st)
+                                    : inverse_device(p, p->in.p, p->out.p, nb, st);
+                ck(cudaMemcpyAsync(out + b0 * out_len, p->out.p, nb * out_len * sizeof(double),
+                                   cudaMemcpyDeviceToHost, st),
+                   "D2H");
+            }
+            ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        }
+        p->last_launches = launches;
+    });
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sglgpu_last_error(void) { return g_last_error.c_str(); }
+
+int sglgpu_plan_create(const sglgpu_plan_desc* desc, sglgpu_plan** out) {
+    return guarded([&] {
+        if (!desc || !out) fail(SGLGPU_EINVAL, "sglgpu_plan_create: null argument");
+        *out = nullptr;
+        const int B = desc->bandlimit;
+        if (B < 1 || B > 256) fail(SGLGPU_EINVAL, "sglgpu_plan_create: bandlimit must be in [1, 256]");
+        if (!desc->r || !desc->a_mod) fail(SGLGPU_EINVAL, "sglgpu_plan_create: radial rule required");
+        for (int i = 0; i < 2 * B; ++i) {
+            if (!(desc->r[i] > 0.0) || (i > 0 && !(desc->r[i] > desc->r[i - 1])))
+                fail(SGLGPU_EINVAL, "sglgpu_plan_create: radial nodes must be positive and increasing");
+        }
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+            cudaGetLastError();
+            fail(SGLGPU_ENODEV, "sglgpu_plan_create: no CUDA device");
+        }
+        int dev = desc->device;
+        if (dev < 0) ck(cudaGetDevice(&dev), "cudaGetDevice");
+        if (dev >= ndev) fail(SGLGPU_EINVAL, "sglgpu_plan_create: device ordinal out of range");
+        std::vector<double> bcal = desc->b_cal ? std::vector<double>(desc->b_cal, desc->b_cal + 2 * B)
+                                               : sglhost::sphere_bcal(B);
+        const sglhost::Tables t = sglhost::build_tables(B, desc->r, desc->a_mod, bcal.data());
+        auto* p = new sglgpu_plan;
+        p->B = B;
+        p->device = dev;
+        try {
+            set_device(p);
+            p->d_tw = dev_upload(t.twiddle);
+            p->d_bcal = dev_upload(t.bcal);
+            p->d_leg = dev_upload(t.legendre);
+            p->d_leg_off = dev_upload(t.legendre_off);
+            p->d_W = dev_upload(t.radial_fwd);
+            p->d_W_off = dev_upload(t.radial_fwd_off);
+            p->d_V = dev_upload(t.radial_inv);
+            p->d_V_off = dev_upload(t.radial_inv_off);
+        } catch (...) {
+            sglgpu_plan_destroy(p);
+            throw;
+        }
+        p->table_bytes = sizeof(double) * (t.twiddle.size() + t.bcal.size() + t.legendre.size() +
+                                           t.radial_fwd.size() + t.radial_inv.size()) +
+                         sizeof(long long) * (t.legendre_off.size() + t.radial_fwd_off.size() +
+                                              t.radial_inv_off.size());
+        *out = p;
+    });
+}
+
+int sglgpu_plan_destroy(sglgpu_plan* p) {
+    if (!p) return SGLGPU_OK;
+    cudaSetDevice(p->device);
+    cudaDeviceSynchronize();
+    for (void* q : {(void*)p->d_tw, (void*)p->d_bcal, (void*)p->d_leg, (void*)p->d_leg_off, (void*)p->d_W,
+                    (void*)p->d_W_off, (void*)p->d_V, (void*)p->d_V_off})
+        if (q) cudaFree(q);
+    for (auto& kv : p->tiles)
+        if (kv.second.first) cudaFree(kv.second.first);
+    p->G.release();
+    p->S.release();
+    p->in.release();
+    p->out.release();
+    delete p;
+    return SGLGPU_OK;
+}
+
+int sglgpu_plan_bandlimit(const sglgpu_plan* p) { return p ? p->B : 0; }
+
+size_t sglgpu_plan_table_bytes(const sglgpu_plan* p) { return p ? p->table_bytes : 0; }
+
+int sglgpu_last_launch_count(const sglgpu_plan* p) { return p ? p->last_launches : 0; }
+
+int sglgpu_forward(sglgpu_plan* plan, const double* samples, double* coeffs, size_t batch, int mem_kind,
+                   void* stream) {
+    return run(plan, samples, coeffs, batch, mem_kind, stream, true);
+}
+
+int sglgpu_inverse(sglgpu_plan* plan, const double* coeffs, double* samples, size_t batch, int mem_kind,
+                   void* stream) {
+    return run(plan, coeffs, samples, batch, mem_kind, stream, false);
+}
+
+int sglgpu_spherical_forward(sglgpu_plan* p, const double* samples, size_t sample_stride, double* shells,
+                             int shell_begin, int shell_count, size_t batch, void* stream) {
+    return guarded([&] {
+        check_plan(p);
+        const int B = p->B;
+        if (shell_begin < 0 || shell_count < 1 || shell_begin + shell_count > 2 * B)
+            fail(SGLGPU_EINVAL, "sglgpu_spherical_forward: shell range out of bounds");
+        if (batch == 0) return;
+        std::lock_guard<std::mutex> lock(p->mu);
+        set_device(p);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int nb = (int)batch;
+        sglk::Geo g{B, shell_count, nb, 2LL * nb * shell_count};
+        p->G.ensure((size_t)4 * B * B * g.NB);
+        int n = sglk::launch_az_forward(g, samples, 2 * sample_stride, p->G.p, p->d_bcal, p->d_tw, st);
+        ck_launch(n, "az_forward");
+        auto lt = tiles_for(p, kLegFwd, nb, shell_count, 0, 2 * B);
+        int k = sglk::launch_legendre_forward(g, p->G.p, shells, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+        ck_launch(k, "legendre_forward");
+        p->last_launches = n + k;
+    });
+}
+
+int sglgpu_spherical_inverse(sglgpu_plan* p, const double* shells, double* samples, size_t sample_stride,
+                             int shell_begin, int shell_count, size_t batch, void* stream) {
+    return guarded([&] {
+        check_plan(p);
+        const int B = p->B;
+        if (shell_begin < 0 || shell_count < 1 || shell_begin + shell_count > 2 * B)
+            fail(SGLGPU_EINVAL, "sglgpu_spherical_inverse: shell range out of bounds");
+        if (batch == 0) return;
+        std::lock_guard<std::mutex> lock(p->mu);
+        set_device(p);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int nb = (int)batch;
+        sglk::Geo g{B, shell_count, nb, 2LL * nb * shell_count};
+        p->G.ensure((size_t)4 * B * B * g.NB);
+        auto lt = tiles_for(p, kLegInv, nb, shell_count, 0, 2 * B);
+        int k = sglk::launch_legendre_inverse(g, shells, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+        ck_launch(k, "legendre_inverse");
+        int n = sglk::launch_az_inverse(g, p->G.p, samples, 2 * sample_stride, p->d_tw, st);
+        ck_launch(n, "az_inverse");
+        p->last_launches = n + k;
+    });
+}
+
+int sglgpu_radial_forward(sglgpu_plan* p, const double* shells, double* coeffs, int l_begin, int l_end,
+                          size_t batch, void* stream) {
+    return guarded([&] {
+        check_plan(p);
+        const int B = p->B;
+        if (l_begin < 0 || l_end > B || l_begin > l_end) fail(SGLGPU_EINVAL, "sglgpu_radial_forward: bad l range");
+        if (batch == 0 || l_begin == l_end) return;
+        std::lock_guard<std::mutex> lock(p->mu);
+        set_device(p);
+        const int nb = (int)batch;
+        sglk::Geo g{B, 2 * B, nb, 2LL * nb * 2 * B};
+        auto rt = tiles_for(p, kRadFwd, nb, 2 * B, l_begin, l_end);
+        int k = sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, (long long)l_begin * l_begin}, shells,
+                                            coeffs, p->d_W, p->d_W_off, rt.first, rt.second,
+                                            static_cast<cudaStream_t>(stream));
+        ck_launch(k, "radial_forward");
+        p->last_launches = k;
+    });
+}
+
+int sglgpu_radial_inverse(sglgpu_plan* p, const double* coeffs, double* shells, int l_begin, int l_end,
+                          size_t batch, void* stream) {
+    return guarded([&] {
+        check_plan(p);
+        const int B = p->B;
+        if (l_begin < 0 || l_end > B || l_begin > l_end) fail(SGLGPU_EINVAL, "sglgpu_radial_inverse: bad l range");
+        if (batch == 0 || l_begin == l_end) return;
+        std::lock_guard<std::mutex> lock(p->mu);
+        set_device(p);
+        const int nb = (int)batch;
+        sglk::Geo g{B, 2 * B, nb, 2LL * nb * 2 * B};
+        auto rt = tiles_for(p, kRadInv, nb, 2 * B, l_begin, l_end);
+        int k = sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, (long long)l_begin * l_begin}, coeffs,
+                                            shells, p->d_V, p->d_V_off, rt.first, rt.second,
+                                            static_cast<cudaStream_t>(stream));
+        ck_launch(k, "radial_inverse");
+        p->last_launches = k;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,733 @@
+// sm_100a kernels of the SGL transform pair (fsglft / ifsglft of
+// /root/reference/proj/core/src/sgl_transform.cpp:274-348), re-designed for B200:
+//
+//  * az_forward / az_inverse  -- the per-ring azimuthal DFT of length 2B
+//    (reference: DftPlan::forward_rows / synthesize_rows, kernels.cpp:478-502,
+//    FftCore radix-2, kernels.cpp:85-195) as a shared-memory Stockham FFT with
+//    in-register radix-16 butterflies.  The forward epilogue applies b_cal
+//    (spherical_transform.cpp:214-220), folds each ring with its equatorial mirror
+//    (theta_{2B-1-j} = pi - theta_j) into even/odd parts and scatters to the
+//    m-major intermediate G; the inverse prologue undoes the fold and drops the
+//    Nyquist bin (spherical_transform.cpp:295-303).
+//  * legendre_forward / legendre_inverse -- the polar Legendre contraction,
+//    mathematically sum_j Pbar_lm(cos theta_j) b_j G_m[j] (the reference does it
+//    seminaively: DCT/DST + truncated rows, spherical_transform.cpp:222-243 and
+//    273-294).  Here it is a direct contraction over the folded K = B polar nodes
+//    as grouped fp64 DMMA (mma.sync m8n8k4 .f64) GEMMs, one problem per
+//    (|m|, parity); +m and -m share the table and are batched along N.
+//  * radial_forward / radial_inverse -- the discrete R transform per (l, m)
+//    (drt_forward / drt_inverse, radial_transform.cpp:75-133) as one grouped DMMA
+//    GEMM per l, shared by all 2l+1 orders m and all functions of the batch.
+//
+// All arithmetic is fp64.
+#include "sgl_kernels.cuh"
+
+namespace sglk {
+
+// ------------------------------------------------------------------ complex helpers
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+
+// e^{SIGN * 2 pi i k / 16} times a, k compile-time after unrolling.
+template <int SIGN>
+__device__ __forceinline__ double2 rot16(double2 a, int k) {
+    constexpr double c1 = 0.92387953251128675613;  // cos(pi/8)
+    constexpr double s1 = 0.38268343236508977173;  // sin(pi/8)
+    constexpr double h = 0.70710678118654752440;   // cos(pi/4)
+    k &= 15;
+    if (k == 0) return a;
+    if (k == 4) return SIGN > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+    if (k == 8) return make_double2(-a.x, -a.y);
+    if (k == 12) return SIGN > 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+    double c, s;
+    switch (k) {
+        case 1: c = c1; s = s1; break;
+        case 2: c = h; s = h; break;
+        case 3: c = s1; s = c1; break;
+        case 5: c = -s1; s = c1; break;
+        case 6: c = -h; s = h; break;
+        case 7: c = -c1; s = s1; break;
+        case 9: c = -c1; s = -s1; break;
+        case 10: c = -h; s = -h; break;
+        case 11: c = -s1; s = -c1; break;
+        case 13: c = s1; s = -c1; break;
+        case 14: c = h; s = -h; break;
+        default: c = c1; s = -s1; break;  // 15
+    }
+    if (SIGN < 0) s = -s;
+    return cmul(a, make_double2(c, s));
+}
+
+__host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
+__host__ __device__ constexpr int brevc(int x, int bits) {
+    int r = 0;
+    for (int i = 0; i < bits; ++i) r |= ((x >> i) & 1) << (bits - 1 - i);
+    return r;
+}
+
+// In-register DFT of size R <= 16, natural order in and out:
+// y_p = sum_q x_q e^{SIGN 2 pi i p q / R}.
+template <int R, int SIGN>
+__device__ __forceinline__ void dft_reg(double2 (&v)[R]) {
+    constexpr int bits = ilog2c(R);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int j = brevc(i, bits);
+        if (i < j) {
+            const double2 t = v[i];
+            v[i] = v[j];
+            v[j] = t;
+        }
+    }
+#pragma unroll
+    for (int len = 2; len <= R; len <<= 1) {
+#pragma unroll
+        for (int i = 0; i < R; i += len) {
+#pragma unroll
+            for (int j = 0; j < len / 2; ++j) {
+                const double2 t = rot16<SIGN>(v[i + j + len / 2], j * (16 / len));
+                v[i + j + len / 2] = csub(v[i + j], t);
+                v[i + j] = cadd(v[i + j], t);
+            }
+        }
+    }
+}
+
+// Padded position of element x inside a ring in shared memory (one pad slot per
+// 16 elements keeps the radix-16 scatters bank-conflict free).
+__device__ __forceinline__ int phys(int x) { return x + (x >> 4); }
+
+template <int N>
+struct FFTShape {
+    static constexpr int RMAX = N < 16 ? N : 16;
+    static constexpr int T = N / RMAX;              // threads per ring
+    static constexpr int STRIDE = N + N / 16 + 1;   // padded ring stride (complex)
+    static constexpr int LOGN = ilog2c(N);
+    static constexpr int R0 = 1 << (LOGN % 4 == 0 ? (N < 16 ? LOGN : 4) : LOGN % 4);  // first radix
+    static constexpr int IG = (T * 2 <= 256) ? 128 / T : 1;  // shell pairs per CTA
+    static constexpr int THREADS = 2 * IG * T;
+};
+
+// One Stockham pass of radix R on a ring of length N held by T threads.
+// Ns = product of the radices already applied.  tw[x] = e^{-2 pi i x / N}.
+template <int N, int R, int SIGN>
+__device__ __forceinline__ void stockham_pass(double2* ring, int Ns, int t, const double2* tw) {
+    constexpr int T = FFTShape<N>::T;
+    constexpr int NBF = N / R;          // butterflies in this pass
+    constexpr int PER = NBF / T;        // butterflies per thread
+    double2 v[PER][R];
+#pragma unroll
+    for (int b = 0; b < PER; ++b) {
+        const int j = t + b * T;
+        const int k = j & (Ns - 1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[b][r] = ring[phys(j + r * NBF)];
+        if (Ns > 1) {
+            const int step = k * (N / (Ns * R));
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                double2 w = tw[(r * step) & (N - 1)];
+                if (SIGN > 0) w.y = -w.y;
+                v[b][r] = cmul(v[b][r], w);
+            }
+        }
+        dft_reg<R, SIGN>(v[b]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < PER; ++b) {
+        const int j = t + b * T;
+        const int k = j & (Ns - 1);
+        const int base = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) ring[phys(base + r * Ns)] = v[b][r];
+    }
+    __syncwarp();
+}
+
+template <int N, int SIGN>
+__device__ __forceinline__ void ring_fft(double2* ring, int t, const double2* tw) {
+    using S = FFTShape<N>;
+    if constexpr (N == 1) {
+        return;
+    } else {
+        int Ns = 1;
+        if constexpr (S::R0 != S::RMAX || N < 16) {
+            stockham_pass<N, S::R0, SIGN>(ring, Ns, t, tw);
+            Ns *= S::R0;
+        }
+        if constexpr (N >= 16) {
+#pragma unroll 1
+            while (Ns < N) {
+                stockham_pass<N, 16, SIGN>(ring, Ns, t, tw);
+                Ns *= 16;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ azimuthal forward
+// grid.x = ceil(nshell / IG), grid.y = B (j' = polar node in the northern half).
+// CTA holds rings (s, j') and (s, 2B-1-j') for IG consecutive flat shells s.
+template <int N>
+__global__ void __launch_bounds__(FFTShape<N>::THREADS)
+az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2* __restrict__ G,
+                  const double* __restrict__ bcal, const double2* __restrict__ twg) {
+    using S = FFTShape<N>;
+    constexpr int B = N / 2;
+    extern __shared__ double2 smem[];
+    double2* tw = smem;
+    double2* rings = smem + N;
+    const int tid = threadIdx.x;
+    const int jp = blockIdx.y;
+    const int s0 = blockIdx.x * S::IG;
+    const int nshell = g.batch * g.SC;
+    for (int x = tid; x < N; x += S::THREADS) tw[x] = twg[x];
+    // load 2*IG rings, coalesced along each ring
+    for (int idx = tid; idx < 2 * S::IG * N; idx += S::THREADS) {
+        const int q = idx / N, e = idx - q * N;
+        const int s = s0 + (q >> 1);
+        const int j = (q & 1) ? (N - 1 - jp) : jp;
+        double2 v = make_double2(0.0, 0.0);
+        if (s < nshell) {
+            const int f = s / g.SC, i = s - f * g.SC;
+            v = X[(size_t)f * fstride + ((size_t)i * N + j) * N + e];
+        }
+        rings[q * S::STRIDE + phys(e)] = v;
+    }
+    __syncthreads();
+    {
+        const int q = tid / S::T, t = tid - q * S::T;
+        ring_fft<N, -1>(rings + q * S::STRIDE, t, tw);
+    }
+    __syncthreads();
+    // epilogue: E/O fold, b_cal, scatter rows G[p][|m|][j'][sgn][s]
+    const double b = bcal[jp];
+    const long long row_len = g.NB / 2;  // complex per row
+    for (int idx = tid; idx < 2 * N * S::IG; idx += S::THREADS) {
+        const int sl = idx % S::IG;
+        const int rowi = idx / S::IG;  // p * N + bin
+        const int p = rowi / N, bin = rowi - p * N;
+        const int s = s0 + sl;
+        if (bin == B || s >= nshell) continue;
+        const int m = bin < B ? bin : bin - N;
+        const int am = m < 0 ? -m : m;
+        const int sgn = m < 0 ? 1 : 0;
+        const double2 f1 = rings[(2 * sl) * S::STRIDE + phys(bin)];
+        const double2 f2 = rings[(2 * sl + 1) * S::STRIDE + phys(bin)];
+        const double2 v = p ? csub(f1, f2) : cadd(f1, f2);
+        G[((((long long)p * B + am) * B + jp) * 2 + sgn) * row_len + s] = cscale(b, v);
+    }
+}
+
+// ------------------------------------------------------------------ azimuthal inverse
+template <int N>
+__global__ void __launch_bounds__(FFTShape<N>::THREADS)
+az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X, size_t fstride,
+                  const double2* __restrict__ twg) {
+    using S = FFTShape<N>;
+    constexpr int B = N / 2;
+    extern __shared__ double2 smem[];
+    double2* tw = smem;
+    double2* rings = smem + N;
+    const int tid = threadIdx.x;
+    const int jp = blockIdx.y;
+    const int s0 = blockIdx.x * S::IG;
+    const int nshell = g.batch * g.SC;
+    const long long row_len = g.NB / 2;
+    for (int x = tid; x < N; x += S::THREADS) tw[x] = twg[x];
+    for (int idx = tid; idx < N * S::IG; idx += S::THREADS) {
+        const int sl = idx % S::IG;
+        const int bin = idx / S::IG;
+        const int s = s0 + sl;
+        double2 e = make_double2(0.0, 0.0), o = make_double2(0.0, 0.0);
+        if (bin != B && s < nshell) {
+            const int m = bin < B ? bin : bin - N;
+            const int am = m < 0 ? -m : m;
+            const int sgn = m < 0 ? 1 : 0;
+            e = G[((((long long)0 * B + am) * B + jp) * 2 + sgn) * row_len + s];
+            o = G[((((long long)1 * B + am) * B + jp) * 2 + sgn) * row_len + s];
+        }
+        rings[(2 * sl) * S::STRIDE + phys(bin)] = cadd(e, o);
+        rings[(2 * sl + 1) * S::STRIDE + phys(bin)] = csub(e, o);
+    }
+    __syncthreads();
+    {
+        const int q = tid / S::T, t = tid - q * S::T;
+        ring_fft<N, +1>(rings + q * S::STRIDE, t, tw);
+    }
+    __syncthreads();
+    for (int idx = tid; idx < 2 * S::IG * N; idx += S::THREADS) {
+        const int q = idx / N, e = idx - q * N;
+        const int s = s0 + (q >> 1);
+        if (s >= nshell) continue;
+        const int j = (q & 1) ? (N - 1 - jp) : jp;
+        const int f = s / g.SC, i = s - f * g.SC;
+        X[(size_t)f * fstride + ((size_t)i * N + j) * N + e] = rings[q * S::STRIDE + phys(e)];
+    }
+}
+
+// ------------------------------------------------------------------ naive azimuthal (non-pow2 2B)
+// Direct DFT per ring for bandlimits whose 2B is not a power of two (the
+// reference's naive fallback, kernels.cpp:35-45).  One CTA per (shell, j').
+__global__ void az_forward_naive_kernel(Geo g, const double2* __restrict__ X, size_t fstride,
+                                        double2* __restrict__ G, const double* __restrict__ bcal,
+                                        const double2* __restrict__ twg) {
+    extern __shared__ double2 smem[];
+    const int B = g.B, N = 2 * B;
+    const int jp = blockIdx.y, s = blockIdx.x;
+    const int f = s / g.SC, i = s - f * g.SC;
+    double2* r1 = smem;
+    double2* r2 = smem + N;
+    for (int e = threadIdx.x; e < N; e += blockDim.x) {
+        r1[e] = X[(size_t)f * fstride + ((size_t)i * N + jp) * N + e];
+        r2[e] = X[(size_t)f * fstride + ((size_t)i * N + (N - 1 - jp)) * N + e];
+    }
+    __syncthreads();
+    const long long row_len = g.NB / 2;
+    for (int bin = threadIdx.x; bin < N; bin += blockDim.x) {
+        if (bin == B) continue;
+        double2 a1 = make_double2(0, 0), a2 = make_double2(0, 0);
+        for (int k = 0; k < N; ++k) {
+            const double2 w = twg[(int)(((long long)bin * k) % N)];
+            a1 = cadd(a1, cmul(r1[k], w));
+            a2 = cadd(a2, cmul(r2[k], w));
+        }
+        const int m = bin < B ? bin : bin - N;
+        const int am = m < 0 ? -m : m, sgn = m < 0;
+        for (int p = 0; p < 2; ++p) {
+            const double2 v = p ? csub(a1, a2) : cadd(a1, a2);
+            G[((((long long)p * B + am) * B + jp) * 2 + sgn) * row_len + s] = cscale(bcal[jp], v);
+        }
+    }
+}
+
+__global__ void az_inverse_naive_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
+                                        size_t fstride, const double2* __restrict__ twg) {
+    extern __shared__ double2 smem[];
+    const int B = g.B, N = 2 * B;
+    const int jp = blockIdx.y, s = blockIdx.x;
+    const int f = s / g.SC, i = s - f * g.SC;
+    double2* r1 = smem;
+    double2* r2 = smem + N;
+    const long long row_len = g.NB / 2;
+    for (int bin = threadIdx.x; bin < N; bin += blockDim.x) {
+        double2 e = make_double2(0, 0), o = make_double2(0, 0);
+        if (bin != B) {
+            const int m = bin < B ? bin : bin - N;
+            const int am = m < 0 ? -m : m, sgn = m < 0;
+            e = G[((((long long)0 * B + am) * B + jp) * 2 + sgn) * row_len + s];
+            o = G[((((long long)1 * B + am) * B + jp) * 2 + sgn) * row_len + s];
+        }
+        r1[bin] = cadd(e, o);
+        r2[bin] = csub(e, o);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < N; k += blockDim.x) {
+        double2 a1 = make_double2(0, 0), a2 = make_double2(0, 0);
+        for (int bin = 0; bin < N; ++bin) {
+            double2 w = twg[(int)(((long long)bin * k) % N)];
+            w.y = -w.y;
+            a1 = cadd(a1, cmul(r1[bin], w));
+            a2 = cadd(a2, cmul(r2[bin], w));
+        }
+        X[(size_t)f * fstride + ((size_t)i * N + jp) * N + k] = a1;
+        X[(size_t)f * fstride + ((size_t)i * N + (N - 1 - jp)) * N + k] = a2;
+    }
+}
+
+// ------------------------------------------------------------------ grouped DMMA GEMM
+// C[row][col] = sum_k A[row][k] * Bm[k][col], addresses separable:
+//   A:  A + rowA(row) + colA(k)        Bm: Bm + rowB(k) + colB(col)
+//   C:  C + rowC(row) + colC(col), value scaled by scaleC(col)
+// cols come in (re, im) pairs that are adjacent in memory for Bm and C.
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+// --- problem kinds
+// Legendre forward: prob = 2|m| + p.  rows l = |m|+p+2r, K = B (j'), cols n' = sgn*NB + n.
+struct LegFwd {
+    Geo g;
+    const double* A;        // table
+    const long long* aoff;  // per prob
+    const double* Bm;       // G
+    double* C;              // S
+    static constexpr bool A_KCONTIG = true;
+    static constexpr bool B_KCONTIG = false;
+    __device__ int am(int pid) const { return pid >> 1; }
+    __device__ int M(int pid) const { const int r = g.B - am(pid) - (pid & 1); return r > 0 ? (r + 1) / 2 : 0; }
+    __device__ int N(int pid) const { return am(pid) == 0 ? (int)g.NB : 2 * (int)g.NB; }
+    __device__ int K(int) const { return g.B; }
+    __device__ long long rowA(int pid, int r) const { return aoff[pid] + (long long)r * g.B; }
+    __device__ long long colA(int, int k) const { return k; }
+    __device__ long long rowB(int pid, int k) const {
+        return ((((long long)(pid & 1) * g.B + am(pid)) * g.B + k) * 2) * g.NB;
+    }
+    __device__ long long colB(int, int n) const { return n; }
+    __device__ long long rowC(int pid, int r) const {
+        const long long l = am(pid) + (pid & 1) + 2 * r;
+        return l * (l + 1) * g.NB;
+    }
+    __device__ long long colC(int pid, int n) const {
+        const int sgn = n >= g.NB;
+        const long long nn = n - (sgn ? g.NB : 0);
+        return (sgn ? -am(pid) : am(pid)) * g.NB + nn;
+    }
+    __device__ double scaleC(int pid, int n) const { return (n >= g.NB && (am(pid) & 1)) ? -1.0 : 1.0; }
+};
+
+// Legendre inverse: prob = 2|m| + p.  rows j' (M = B), K = #l of parity p, cols n'.
+struct LegInv {
+    Geo g;
+    const double* A;
+    const long long* aoff;
+    const double* Bm;  // S
+    double* C;         // G
+    static constexpr bool A_KCONTIG = false;
+    static constexpr bool B_KCONTIG = false;
+    __device__ int am(int pid) const { return pid >> 1; }
+    __device__ int M(int) const { return g.B; }
+    __device__ int N(int pid) const { return am(pid) == 0 ? (int)g.NB : 2 * (int)g.NB; }
+    __device__ int K(int pid) const { const int r = g.B - am(pid) - (pid & 1); return r > 0 ? (r + 1) / 2 : 0; }
+    __device__ long long rowA(int pid, int j) const { return aoff[pid] + j; }
+    __device__ long long colA(int, int k) const { return (long long)k * g.B; }
+    __device__ long long rowB(int pid, int k) const {
+        const long long l = am(pid) + (pid & 1) + 2 * k;
+        return l * (l + 1) * g.NB;
+    }
+    __device__ long long colB(int pid, int n) const {
+        const int sgn = n >= g.NB;
+        const long long nn = n - (sgn ? g.NB : 0);
+        return (sgn ? -am(pid) : am(pid)) * g.NB + nn;
+    }
+    __device__ long long rowC(int pid, int j) const {
+        return ((((long long)(pid & 1) * g.B + am(pid)) * g.B + j) * 2) * g.NB;
+    }
+    __device__ long long colC(int, int n) const { return n; }
+    __device__ double scaleC(int pid, int n) const { return (n >= g.NB && (am(pid) & 1)) ? -1.0 : 1.0; }
+};
+
+__host__ __device__ inline long long degree_offset(long long n) { return (n - 1) * n * (2 * n - 1) / 6; }
+
+// Shell-block view of the nu-major intermediate S for the radial stage.  On one
+// GPU S is a single block S[nu][f][i] (i < 2B).  Under the multi-GPU shell / (l, m)
+// split every rank receives one block per source rank, S_r[nu - nu0][f][i_local]
+// (i_local < sc_blk), placed blk_stride reals apart; the radial GEMM reads them
+// in place, so the exchange needs no re-interleaving pass.
+struct ShellBlocks {
+    int sc_blk;            // shells per block
+    long long blk_stride;  // reals between blocks
+    long long nu0;         // first nu held
+    __device__ long long row(int i) const {
+        const int b = i / sc_blk;
+        return b * blk_stride + 2LL * (i - b * sc_blk);
+    }
+};
+
+// Radial forward: prob = l.  rows n = l+1+r (M = B-l), K = 2B (i), cols (mf, c),
+// mf = f * (2l+1) + (m + l).  g.SC = sc_blk, g.NB = batch * sc_blk * 2.
+struct RadFwd {
+    Geo g;
+    const double* A;        // W
+    const long long* aoff;
+    const double* Bm;       // S blocks
+    double* C;              // coefficients
+    long long omega;        // coefficients per function
+    ShellBlocks sb;
+    static constexpr bool A_KCONTIG = true;
+    static constexpr bool B_KCONTIG = true;
+    __device__ int M(int l) const { return g.B - l; }
+    __device__ int N(int l) const { return (2 * l + 1) * g.batch * 2; }
+    __device__ int K(int) const { return 2 * g.B; }
+    __device__ long long rowA(int l, int r) const { return aoff[l] + (long long)r * 2 * g.B; }
+    __device__ long long colA(int, int k) const { return k; }
+    __device__ long long rowB(int, int k) const { return sb.row(k); }
+    __device__ long long colB(int l, int n) const {
+        const int mf = n >> 1, w = 2 * l + 1;
+        const int f = mf / w, mm = mf - f * w;  // mm = m + l
+        return ((long long)l * l + mm - sb.nu0) * g.NB + (long long)f * 2 * g.SC + (n & 1);
+    }
+    __device__ long long rowC(int l, int r) const { return 2 * degree_offset(l + 1 + r); }
+    __device__ long long colC(int l, int n) const {
+        const int mf = n >> 1, w = 2 * l + 1;
+        const int f = mf / w, mm = mf - f * w;
+        return (long long)f * 2 * omega + 2LL * ((long long)l * l + mm) + (n & 1);
+    }
+    __device__ double scaleC(int, int) const { return 1.0; }
+};
+
+// Radial inverse: prob = l.  rows i (M = 2B), K = B-l (n), cols (mf, c).
+struct RadInv {
+    Geo g;
+    const double* A;        // V
+    const long long* aoff;
+    const double* Bm;       // coefficients
+    double* C;              // S blocks
+    long long omega;
+    ShellBlocks sb;
+    static constexpr bool A_KCONTIG = true;
+    static constexpr bool B_KCONTIG = false;
+    __device__ int M(int) const { return 2 * g.B; }
+    __device__ int N(int l) const { return (2 * l + 1) * g.batch * 2; }
+    __device__ int K(int l) const { return g.B - l; }
+    __device__ long long rowA(int l, int i) const { return aoff[l] + (long long)i * (g.B - l); }
+    __device__ long long colA(int, int k) const { return k; }
+    __device__ long long rowB(int l, int k) const { return 2 * degree_offset(l + 1 + k); }
+    __device__ long long colB(int l, int n) const {
+        const int mf = n >> 1, w = 2 * l + 1;
+        const int f = mf / w, mm = mf - f * w;
+        return (long long)f * 2 * omega + 2LL * ((long long)l * l + mm) + (n & 1);
+    }
+    __device__ long long rowC(int, int i) const { return sb.row(i); }
+    __device__ long long colC(int l, int n) const {
+        const int mf = n >> 1, w = 2 * l + 1;
+        const int f = mf / w, mm = mf - f * w;
+        return ((long long)l * l + mm - sb.nu0) * g.NB + (long long)f * 2 * g.SC + (n & 1);
+    }
+    __device__ double scaleC(int, int) const { return 1.0; }
+};
+
+template <class P>
+__global__ void __launch_bounds__(128) gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles) {
+    constexpr int BM = kBM, BN = kBN, BK = kBK;
+    constexpr int LDA = BK + 4;  // conflict-free A fragment loads
+    constexpr int LDB = BN + 4;  // conflict-free B fragment loads
+    __shared__ __align__(16) double As[2][BM][LDA];
+    __shared__ __align__(16) double Bs[2][BK][LDB];
+
+    const Tile t = tiles[blockIdx.x];
+    const int pid = t.prob, m0 = t.m0, n0 = t.n0;
+    const int M = pr.M(pid), N = pr.N(pid), K = pr.K(pid);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    // ---- per-thread fixed load coordinates
+    // A: 512 elements per chunk, 4 per thread
+    int a_row[4], a_k[4];
+    long long a_rowoff[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (P::A_KCONTIG) {
+            a_row[q] = tid >> 2;
+            a_k[q] = (tid & 3) * 4 + q;
+        } else {
+            a_k[q] = tid >> 3;
+            a_row[q] = (tid & 7) * 4 + q;
+        }
+        const int row = m0 + a_row[q];
+        a_rowoff[q] = row < M ? pr.rowA(pid, row) : -1;
+    }
+    // B: 1024 double2 per chunk, 8 per thread
+    int b_k[8], b_c[8];
+    long long b_coloff[8];  // may be negative (LegInv: -|m| rows); validity in b_ok
+    bool b_ok[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        if (P::B_KCONTIG) {
+            b_k[q] = tid & 15;
+            b_c[q] = ((tid >> 4) + 8 * q) * 2;
+        } else {
+            b_k[q] = (tid >> 6) + 2 * q;
+            b_c[q] = (tid & 63) * 2;
+        }
+        const int col = n0 + b_c[q];
+        b_ok[q] = col < N;
+        b_coloff[q] = b_ok[q] ? pr.colB(pid, col) : 0;
+    }
+
+    double2 rb[8];
+    double ra[4];
+    auto load_chunk = [&](int k0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int k = k0 + a_k[q];
+            ra[q] = (a_rowoff[q] >= 0 && k < K) ? __ldg(pr.A + a_rowoff[q] + pr.colA(pid, k)) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int k = k0 + b_k[q];
+            if (b_ok[q] && k < K) {
+                rb[q] = __ldg(reinterpret_cast<const double2*>(pr.Bm + pr.rowB(pid, k) + b_coloff[q]));
+            } else {
+                rb[q] = make_double2(0.0, 0.0);
+            }
+        }
+    };
+    auto store_chunk = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) As[buf][a_row[q]][a_k[q]] = ra[q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) *reinterpret_cast<double2*>(&Bs[buf][b_k[q]][b_c[q]]) = rb[q];
+    };
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    const int fm_active = min(4, (M - m0 + 7) >> 3);
+    const int nchunks = (K + BK - 1) / BK;
+    load_chunk(0);
+    store_chunk(0);
+    __syncthreads();
+    for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        if (c + 1 < nchunks) load_chunk((c + 1) * BK);
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int fm = 0; fm < 4; ++fm) a[fm] = As[buf][fm * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+            for (int fn = 0; fn < 4; ++fn) b[fn] = Bs[buf][kk + (lane & 3)][warp * 32 + fn * 8 + (lane >> 2)];
+#pragma unroll
+            for (int fm = 0; fm < 4; ++fm) {
+                if (fm < fm_active) {
+#pragma unroll
+                    for (int fn = 0; fn < 4; ++fn) dmma884(acc[fm][fn], a[fm], b[fn]);
+                }
+            }
+        }
+        if (c + 1 < nchunks) store_chunk(buf ^ 1);
+        __syncthreads();
+    }
+    // ---- epilogue
+#pragma unroll
+    for (int fm = 0; fm < 4; ++fm) {
+        const int row = m0 + fm * 8 + (lane >> 2);
+        if (row >= M) continue;
+        const long long ro = pr.rowC(pid, row);
+#pragma unroll
+        for (int fn = 0; fn < 4; ++fn) {
+            const int col = n0 + warp * 32 + fn * 8 + 2 * (lane & 3);
+            if (col >= N) continue;
+            const double s = pr.scaleC(pid, col);
+            *reinterpret_cast<double2*>(pr.C + ro + pr.colC(pid, col)) =
+                make_double2(s * acc[fm][fn][0], s * acc[fm][fn][1]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ launchers
+template <int N>
+static int az_fwd_launch(const Geo& g, const double* X, size_t fstride, double* G, const double* bcal,
+                         const double* tw, cudaStream_t s) {
+    using S = FFTShape<N>;
+    const size_t smem = sizeof(double2) * (N + 2 * S::IG * S::STRIDE);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(az_forward_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const int nshell = g.batch * g.SC;
+    dim3 grid((nshell + S::IG - 1) / S::IG, g.B);
+    az_forward_kernel<N><<<grid, S::THREADS, smem, s>>>(g, reinterpret_cast<const double2*>(X), fstride / 2,
+                                                         reinterpret_cast<double2*>(G), bcal,
+                                                         reinterpret_cast<const double2*>(tw));
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+template <int N>
+static int az_inv_launch(const Geo& g, const double* G, double* X, size_t fstride, const double* tw,
+                         cudaStream_t s) {
+    using S = FFTShape<N>;
+    const size_t smem = sizeof(double2) * (N + 2 * S::IG * S::STRIDE);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(az_inverse_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const int nshell = g.batch * g.SC;
+    dim3 grid((nshell + S::IG - 1) / S::IG, g.B);
+    az_inverse_kernel<N><<<grid, S::THREADS, smem, s>>>(g, reinterpret_cast<const double2*>(G),
+                                                         reinterpret_cast<double2*>(X), fstride / 2,
+                                                         reinterpret_cast<const double2*>(tw));
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// sample_stride is in doubles here (2 per complex); kernels take complex strides.
+int launch_az_forward(const Geo& g, const double* samples, size_t sample_stride, double* G,
+                      const double* bcal, const double* twiddle, cudaStream_t s) {
+    switch (2 * g.B) {
+        case 2: return az_fwd_launch<2>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 4: return az_fwd_launch<4>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 8: return az_fwd_launch<8>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 16: return az_fwd_launch<16>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 32: return az_fwd_launch<32>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 64: return az_fwd_launch<64>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 128: return az_fwd_launch<128>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 256: return az_fwd_launch<256>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 512: return az_fwd_launch<512>(g, samples, sample_stride, G, bcal, twiddle, s);
+        default: break;
+    }
+    const int N = 2 * g.B;
+    dim3 grid(g.batch * g.SC, g.B);
+    az_forward_naive_kernel<<<grid, 128, 2 * N * sizeof(double2), s>>>(
+        g, reinterpret_cast<const double2*>(samples), sample_stride / 2, reinterpret_cast<double2*>(G), bcal,
+        reinterpret_cast<const double2*>(twiddle));
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_az_inverse(const Geo& g, const double* G, double* samples, size_t sample_stride,
+                      const double* twiddle, cudaStream_t s) {
+    switch (2 * g.B) {
+        case 2: return az_inv_launch<2>(g, G, samples, sample_stride, twiddle, s);
+        case 4: return az_inv_launch<4>(g, G, samples, sample_stride, twiddle, s);
+        case 8: return az_inv_launch<8>(g, G, samples, sample_stride, twiddle, s);
+        case 16: return az_inv_launch<16>(g, G, samples, sample_stride, twiddle, s);
+        case 32: return az_inv_launch<32>(g, G, samples, sample_stride, twiddle, s);
+        case 64: return az_inv_launch<64>(g, G, samples, sample_stride, twiddle, s);
+        case 128: return az_inv_launch<128>(g, G, samples, sample_stride, twiddle, s);
+        case 256: return az_inv_launch<256>(g, G, samples, sample_stride, twiddle, s);
+        case 512: return az_inv_launch<512>(g, G, samples, sample_stride, twiddle, s);
+        default: break;
+    }
+    const int N = 2 * g.B;
+    dim3 grid(g.batch * g.SC, g.B);
+    az_inverse_naive_kernel<<<grid, 128, 2 * N * sizeof(double2), s>>>(
+        g, reinterpret_cast<const double2*>(G), reinterpret_cast<double2*>(samples), sample_stride / 2,
+        reinterpret_cast<const double2*>(twiddle));
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+template <class P>
+static int gemm_launch(const P& p, const Tile* tiles, int ntiles, cudaStream_t s) {
+    if (ntiles <= 0) return 0;
+    gemm_dmma_kernel<P><<<ntiles, 128, 0, s>>>(p, tiles);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_legendre_forward(const Geo& g, const double* G, double* S, const double* tab,
+                            const long long* tab_off, const Tile* tiles, int ntiles, cudaStream_t s) {
+    LegFwd p{g, tab, tab_off, G, S};
+    return gemm_launch(p, tiles, ntiles, s);
+}
+
+int launch_legendre_inverse(const Geo& g, const double* S, double* G, const double* tab,
+                            const long long* tab_off, const Tile* tiles, int ntiles, cudaStream_t s) {
+    LegInv p{g, tab, tab_off, S, G};
+    return gemm_launch(p, tiles, ntiles, s);
+}
+
+int launch_radial_forward(const Geo& g, const RadialBlocks& rb, const double* S, double* C,
+                          const double* W, const long long* w_off, const Tile* tiles, int ntiles,
+                          cudaStream_t s) {
+    RadFwd p{g, W, w_off, S, C, degree_offset(g.B + 1), ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
+    return gemm_launch(p, tiles, ntiles, s);
+}
+
+int launch_radial_inverse(const Geo& g, const RadialBlocks& rb, const double* C, double* S,
+                          const double* V, const long long* v_off, const Tile* tiles, int ntiles,
+                          cudaStream_t s) {
+    RadInv p{g, V, v_off, C, S, degree_offset(g.B + 1), ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
+    return gemm_launch(p, tiles, ntiles, s);
+}
+
+}  // namespace sglk

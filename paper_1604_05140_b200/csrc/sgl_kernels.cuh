@@ -1,0 +1,65 @@
+// Launch interface of the sm_100a kernels (sgl_kernels.cu).  Host-side callers:
+// sgl_capi.cpp.  All pointers are device pointers; every launcher enqueues on
+// `stream` and returns the number of kernels it launched (or -1 on a launch error).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace sglk {
+
+// Tile descriptor for the grouped DMMA contraction: {problem, m0, n0, unused}.
+struct Tile {
+    int prob, m0, n0, pad;
+};
+
+constexpr int kBM = 32;   // CTA tile rows
+constexpr int kBN = 128;  // CTA tile cols (reals)
+constexpr int kBK = 16;   // k chunk
+
+// Geometry shared by the stages.  "shell" is a flat index s = f * SC + i over
+// the functions of the batch and the SC radial shells handled by the call.
+struct Geo {
+    int B;          // bandlimit
+    int SC;         // shells per function in this call (2B for the whole transform)
+    int batch;      // functions
+    long long NB;   // reals per nu-row of S and per G row half: batch * SC * 2
+};
+
+// Azimuthal stage (forward): FFT of length 2B per ring (sign -1, kernels.cpp:478),
+// b_cal weighting, equatorial fold E/O and scatter to the m-major intermediate
+//   G[p][|m|][j'][sgn][f][i]  (complex), p = parity, j' < B, sgn = (m < 0).
+int launch_az_forward(const Geo& g, const double* samples, size_t sample_stride,
+                      double* G, const double* bcal, const double* twiddle, cudaStream_t s);
+// Azimuthal stage (inverse): unfold E/O, zero Nyquist bin, FFT sign +1 without
+// 1/N (kernels.cpp:491), write psi-order rings.
+int launch_az_inverse(const Geo& g, const double* G, double* samples, size_t sample_stride,
+                      const double* twiddle, cudaStream_t s);
+
+// Polar stage: per (|m|, parity) DMMA contraction against the normalized
+// Legendre table.  tab: rows Pbar_{l,|m|}(cos theta_j'), j' < B.
+int launch_legendre_forward(const Geo& g, const double* G, double* S, const double* tab,
+                            const long long* tab_off, const Tile* tiles, int ntiles,
+                            cudaStream_t s);
+int launch_legendre_inverse(const Geo& g, const double* S, double* G, const double* tab,
+                            const long long* tab_off, const Tile* tiles, int ntiles,
+                            cudaStream_t s);
+
+// Radial stage: per l DMMA contraction against W_l (forward) / V_l (inverse).
+// S is read/written as shell blocks (see ShellBlocks in sgl_kernels.cu); for the
+// single-GPU transform rb = {2B, 0, 0} and g.SC = 2B.
+struct RadialBlocks {
+    int sc_blk;
+    long long blk_stride;
+    long long nu0;
+};
+int launch_radial_forward(const Geo& g, const RadialBlocks& rb, const double* S, double* C,
+                          const double* W, const long long* w_off, const Tile* tiles, int ntiles,
+                          cudaStream_t s);
+int launch_radial_inverse(const Geo& g, const RadialBlocks& rb, const double* C, double* S,
+                          const double* V, const long long* v_off, const Tile* tiles, int ntiles,
+                          cudaStream_t s);
+
+}  // namespace sglk
