@@ -104,6 +104,15 @@ int sglgpu_spherical_inverse(sglgpu_plan* plan, const double* shells, double* sa
  * (for the bench's gpu_launches count). */
 int sglgpu_last_launch_count(const sglgpu_plan* plan);
 
+/* Live per-stage timing for benchmarks: between begin and end every stage launch
+ * of sglgpu_forward / sglgpu_inverse is bracketed by CUDA events on the call's
+ * stream; end synchronizes and returns, per stage, the summed milliseconds and
+ * the number of launches.  Stages: 0 az_forward, 1 legendre_forward,
+ * 2 radial_forward, 3 radial_inverse, 4 legendre_inverse, 5 az_inverse. */
+#define SGLGPU_NUM_STAGES 6
+int sglgpu_profile_begin(sglgpu_plan* plan);
+int sglgpu_profile_end(sglgpu_plan* plan, double* stage_ms, int* stage_launches);
+
 const char* sglgpu_last_error(void);
 
 /* Host-only (no CUDA) copy of the plan tables the kernels stream, for tests:

@@ -106,6 +106,10 @@ struct sglgpu_plan {
     std::map<std::tuple<int, int, int, int, int>, std::pair<sglk::Tile*, int>> tiles;
     std::mutex mu;
     int last_launches = 0;
+    // live per-stage timing (sglgpu_profile_begin/end)
+    bool profiling = false;
+    std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> prof;
+    std::vector<cudaEvent_t> ev_pool;
 };
 
 namespace {
@@ -171,6 +175,34 @@ std::pair<sglk::Tile*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int 
 
 void set_device(sglgpu_plan* p) { ck(cudaSetDevice(p->device), "cudaSetDevice"); }
 
+cudaEvent_t pool_event(sglgpu_plan* p) {
+    if (!p->ev_pool.empty()) {
+        cudaEvent_t e = p->ev_pool.back();
+        p->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+}
+
+// Brackets one stage launch with events when profiling is on.
+template <class F>
+int staged(sglgpu_plan* p, int stage, cudaStream_t st, F&& launch) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (p->profiling) {
+        a = pool_event(p);
+        b = pool_event(p);
+        ck(cudaEventRecord(a, st), "cudaEventRecord");
+    }
+    const int k = launch();
+    if (p->profiling) {
+        ck(cudaEventRecord(b, st), "cudaEventRecord");
+        p->prof.emplace_back(stage, a, b);
+    }
+    return k;
+}
+
 // Largest batch chunk whose G + S workspaces stay under ~6 GiB.
 size_t batch_chunk(int B, size_t batch) {
     const size_t per = (size_t)(16 + 4) * B * B * B * sizeof(double);  // G + S per function
@@ -186,16 +218,22 @@ int forward_device(sglgpu_plan* p, const double* X, double* C, int nb, cudaStrea
     p->G.ensure((size_t)16 * B * B * B * nb);
     p->S.ensure((size_t)4 * B * B * B * nb);
     int n = 0, k;
-    k = sglk::launch_az_forward(g, X, 2 * (size_t)sample_count(B), p->G.p, p->d_bcal, p->d_tw, st);
+    k = staged(p, 0, st, [&] {
+        return sglk::launch_az_forward(g, X, 2 * (size_t)sample_count(B), p->G.p, p->d_bcal, p->d_tw, st);
+    });
     ck_launch(k, "az_forward");
     n += k;
     auto lt = tiles_for(p, kLegFwd, nb, 2 * B, 0, 2 * B);
-    k = sglk::launch_legendre_forward(g, p->G.p, p->S.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+    k = staged(p, 1, st, [&] {
+        return sglk::launch_legendre_forward(g, p->G.p, p->S.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+    });
     ck_launch(k, "legendre_forward");
     n += k;
     auto rt = tiles_for(p, kRadFwd, nb, 2 * B, 0, B);
-    k = sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, p->S.p, C, p->d_W, p->d_W_off,
-                                    rt.first, rt.second, st);
+    k = staged(p, 2, st, [&] {
+        return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, p->S.p, C, p->d_W, p->d_W_off,
+                                           rt.first, rt.second, st);
+    });
     ck_launch(k, "radial_forward");
     n += k;
     return n;
@@ -208,15 +246,21 @@ int inverse_device(sglgpu_plan* p, const double* C, double* X, int nb, cudaStrea
     p->S.ensure((size_t)4 * B * B * B * nb);
     int n = 0, k;
     auto rt = tiles_for(p, kRadInv, nb, 2 * B, 0, B);
-    k = sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, 0}, C, p->S.p, p->d_V, p->d_V_off,
-                                    rt.first, rt.second, st);
+    k = staged(p, 3, st, [&] {
+        return sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, 0}, C, p->S.p, p->d_V, p->d_V_off,
+                                           rt.first, rt.second, st);
+    });
     ck_launch(k, "radial_inverse");
     n += k;
     auto lt = tiles_for(p, kLegInv, nb, 2 * B, 0, 2 * B);
-    k = sglk::launch_legendre_inverse(g, p->S.p, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+    k = staged(p, 4, st, [&] {
+        return sglk::launch_legendre_inverse(g, p->S.p, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+    });
     ck_launch(k, "legendre_inverse");
     n += k;
-    k = sglk::launch_az_inverse(g, p->G.p, X, 2 * (size_t)sample_count(B), p->d_tw, st);
+    k = staged(p, 5, st, [&] {
+        return sglk::launch_az_inverse(g, p->G.p, X, 2 * (size_t)sample_count(B), p->d_tw, st);
+    });
     ck_launch(k, "az_inverse");
     n += k;
     return n;
@@ -330,6 +374,11 @@ int sglgpu_plan_destroy(sglgpu_plan* p) {
         if (q) cudaFree(q);
     for (auto& kv : p->tiles)
         if (kv.second.first) cudaFree(kv.second.first);
+    for (auto& [stage, a, b] : p->prof) {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+    for (auto e : p->ev_pool) cudaEventDestroy(e);
     p->G.release();
     p->S.release();
     p->in.release();
@@ -343,6 +392,37 @@ int sglgpu_plan_bandlimit(const sglgpu_plan* p) { return p ? p->B : 0; }
 size_t sglgpu_plan_table_bytes(const sglgpu_plan* p) { return p ? p->table_bytes : 0; }
 
 int sglgpu_last_launch_count(const sglgpu_plan* p) { return p ? p->last_launches : 0; }
+
+int sglgpu_profile_begin(sglgpu_plan* p) {
+    return guarded([&] {
+        check_plan(p);
+        std::lock_guard<std::mutex> lock(p->mu);
+        p->profiling = true;
+    });
+}
+
+int sglgpu_profile_end(sglgpu_plan* p, double* stage_ms, int* stage_launches) {
+    return guarded([&] {
+        check_plan(p);
+        std::lock_guard<std::mutex> lock(p->mu);
+        set_device(p);
+        p->profiling = false;
+        for (int s = 0; s < SGLGPU_NUM_STAGES; ++s) {
+            if (stage_ms) stage_ms[s] = 0.0;
+            if (stage_launches) stage_launches[s] = 0;
+        }
+        for (auto& [stage, a, b] : p->prof) {
+            ck(cudaEventSynchronize(b), "cudaEventSynchronize");
+            float ms = 0.f;
+            ck(cudaEventElapsedTime(&ms, a, b), "cudaEventElapsedTime");
+            if (stage_ms) stage_ms[stage] += ms;
+            if (stage_launches) stage_launches[stage] += 1;
+            p->ev_pool.push_back(a);
+            p->ev_pool.push_back(b);
+        }
+        p->prof.clear();
+    });
+}
 
 int sglgpu_forward(sglgpu_plan* plan, const double* samples, double* coeffs, size_t batch, int mem_kind,
                    void* stream) {
