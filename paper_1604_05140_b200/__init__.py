@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libsglb200.so")
+LIB_PATH = os.environ.get("SGL_B200_LIB", os.path.join(_PKG, "libsglb200.so"))
 TABLES_DIR = os.environ.get("SGL_TABLES", os.path.join(_PKG, "tables"))
 
 SGLGPU_OK, SGLGPU_EINVAL, SGLGPU_ECUDA, SGLGPU_ENOMEM, SGLGPU_ENODEV = range(5)

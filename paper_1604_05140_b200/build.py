@@ -41,15 +41,16 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
     deps = _sources() + _headers() + [os.path.abspath(__file__)]
-    if not force and not _stale(LIB, deps):
-        return LIB
+    target = out or LIB
+    if not force and not _stale(target, deps):
+        return target
     objdir = os.path.join(PKG, "_obj")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     common = ["-O3", "-std=c++20", "-Xcompiler", "-fPIC,-pthread", "-I", os.path.join(REPO, "include"),
-              "-I", CSRC]
+              "-I", CSRC] + [f for f in os.environ.get("SGL_NVCC_FLAGS", "").split() if f]
     procs = []
     for src in _sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
@@ -65,12 +66,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if p.returncode != 0:
             sys.stderr.write(out.decode())
             raise RuntimeError("build failed: " + " ".join(cmd))
-    tmp = LIB + ".tmp"
+    tmp = target + ".tmp"
     link = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart", "-Xcompiler", "-pthread"]
     subprocess.run(link, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose=True, out=outs[0] if outs else None))

@@ -22,6 +22,8 @@
 // All arithmetic is fp64.
 #include "sgl_kernels.cuh"
 
+#include <algorithm>
+
 namespace sglk {
 
 // ------------------------------------------------------------------ complex helpers
@@ -101,6 +103,13 @@ __device__ __forceinline__ void dft_reg(double2 (&v)[R]) {
 // 16 elements keeps the radix-16 scatters bank-conflict free).
 __device__ __forceinline__ int phys(int x) { return x + (x >> 4); }
 
+#ifndef SGL_AZ_ELEMS
+#define SGL_AZ_ELEMS 1024  // ring elements per shell-pair group and CTA (sets IG = SGL_AZ_ELEMS / N)
+#endif
+#ifndef SGL_AZ_MINB
+#define SGL_AZ_MINB 4
+#endif
+
 template <int N>
 struct FFTShape {
     static constexpr int RMAX = N < 16 ? N : 16;
@@ -108,14 +117,29 @@ struct FFTShape {
     static constexpr int STRIDE = N + N / 16 + 1;   // padded ring stride (complex)
     static constexpr int LOGN = ilog2c(N);
     static constexpr int R0 = 1 << (LOGN % 4 == 0 ? (N < 16 ? LOGN : 4) : LOGN % 4);  // first radix
-    static constexpr int IG = (T * 2 <= 256) ? 128 / T : 1;  // shell pairs per CTA
+    static constexpr int IG = (T * 2 <= 256) ? (SGL_AZ_ELEMS / 16) / T : 1;  // shell pairs per CTA
     static constexpr int THREADS = 2 * IG * T;
 };
 
+// Synchronizes the threads that share a ring pair (j', 2B-1-j'): one warp when
+// the pair fits in a warp, else the CTA (uniform control flow in both kernels).
+template <int N>
+__device__ __forceinline__ void pair_sync() {
+    if constexpr (2 * FFTShape<N>::T <= 32) {
+        __syncwarp();
+    } else {
+        __syncthreads();
+    }
+}
+
 // One Stockham pass of radix R on a ring of length N held by T threads.
 // Ns = product of the radices already applied.  tw[x] = e^{-2 pi i x / N}.
-template <int N, int R, int SIGN>
-__device__ __forceinline__ void stockham_pass(double2* ring, int Ns, int t, const double2* tw) {
+// Inputs come from ld(x), outputs go to st(x, v): the first pass of the forward
+// FFT reads global memory directly into registers and the last pass of the
+// inverse writes global memory directly, so only the middle exchanges touch
+// shared memory.  When IN_PLACE, all reads complete (pair_sync) before any write.
+template <int N, int R, int SIGN, bool IN_PLACE, class Ld, class St>
+__device__ __forceinline__ void stockham_pass(int Ns, int t, const double2* tw, Ld&& ld, St&& st) {
     constexpr int T = FFTShape<N>::T;
     constexpr int NBF = N / R;          // butterflies in this pass
     constexpr int PER = NBF / T;        // butterflies per thread
@@ -123,9 +147,13 @@ __device__ __forceinline__ void stockham_pass(double2* ring, int Ns, int t, cons
 #pragma unroll
     for (int b = 0; b < PER; ++b) {
         const int j = t + b * T;
-        const int k = j & (Ns - 1);
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[b][r] = ring[phys(j + r * NBF)];
+        for (int r = 0; r < R; ++r) v[b][r] = ld(j + r * NBF);
+    }
+#pragma unroll
+    for (int b = 0; b < PER; ++b) {
+        const int j = t + b * T;
+        const int k = j & (Ns - 1);
         if (Ns > 1) {
             const int step = k * (N / (Ns * R));
 #pragma unroll
@@ -137,44 +165,67 @@ __device__ __forceinline__ void stockham_pass(double2* ring, int Ns, int t, cons
         }
         dft_reg<R, SIGN>(v[b]);
     }
-    __syncwarp();
+    if (IN_PLACE) pair_sync<N>();
 #pragma unroll
     for (int b = 0; b < PER; ++b) {
         const int j = t + b * T;
         const int k = j & (Ns - 1);
         const int base = (j - k) * R + k;
 #pragma unroll
-        for (int r = 0; r < R; ++r) ring[phys(base + r * Ns)] = v[b][r];
+        for (int r = 0; r < R; ++r) st(base + r * Ns, v[b][r]);
     }
-    __syncwarp();
 }
 
-template <int N, int SIGN>
-__device__ __forceinline__ void ring_fft(double2* ring, int t, const double2* tw) {
+// Full FFT of one ring: first pass reads ld, last pass writes st, middle
+// passes run in place on `ring` (padded).  Ends without a trailing sync.
+template <int N, int SIGN, bool FIRST_IN_PLACE, class Ld, class St>
+__device__ __forceinline__ void ring_fft_io(double2* ring, int t, const double2* tw, Ld&& ld, St&& st) {
     using S = FFTShape<N>;
-    if constexpr (N == 1) {
-        return;
+    auto rd = [&](int x) { return ring[phys(x)]; };
+    auto wr = [&](int x, double2 v) { ring[phys(x)] = v; };
+    constexpr bool head = (S::R0 != S::RMAX || N < 16);        // a leading small-radix pass
+    constexpr int P16 = (N >= 16) ? (S::LOGN - (head ? ilog2c(S::R0) : 0)) / 4 : 0;
+    constexpr int NPASS = (head ? 1 : 0) + P16;
+    if constexpr (NPASS == 1) {
+        if constexpr (head) stockham_pass<N, S::R0, SIGN, FIRST_IN_PLACE>(1, t, tw, ld, st);
+        else stockham_pass<N, 16, SIGN, FIRST_IN_PLACE>(1, t, tw, ld, st);
     } else {
         int Ns = 1;
-        if constexpr (S::R0 != S::RMAX || N < 16) {
-            stockham_pass<N, S::R0, SIGN>(ring, Ns, t, tw);
+        if constexpr (head) {
+            stockham_pass<N, S::R0, SIGN, FIRST_IN_PLACE>(Ns, t, tw, ld, wr);
             Ns *= S::R0;
+        } else {
+            stockham_pass<N, 16, SIGN, FIRST_IN_PLACE>(Ns, t, tw, ld, wr);
+            Ns *= 16;
         }
-        if constexpr (N >= 16) {
+        pair_sync<N>();
 #pragma unroll 1
-            while (Ns < N) {
-                stockham_pass<N, 16, SIGN>(ring, Ns, t, tw);
-                Ns *= 16;
-            }
+        for (int p = 1; p < NPASS - 1; ++p) {
+            stockham_pass<N, 16, SIGN, true>(Ns, t, tw, rd, wr);
+            Ns *= 16;
+            pair_sync<N>();
         }
+        stockham_pass<N, 16, SIGN, true>(Ns, t, tw, rd, st);
     }
 }
+
+// ------------------------------------------------------------------ async copy helpers
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 // ------------------------------------------------------------------ azimuthal forward
 // grid.x = ceil(nshell / IG), grid.y = B (j' = polar node in the northern half).
 // CTA holds rings (s, j') and (s, 2B-1-j') for IG consecutive flat shells s.
+// The first FFT pass loads each ring straight from HBM into registers
+// (coalesced: the T threads of a ring read consecutive elements); the result
+// lands in shared memory, where the epilogue folds the ring pair into even/odd
+// parts, applies b_cal and writes rows of G[p][|m|][j'][sgn][s] (IG shells
+// contiguous per row).
 template <int N>
-__global__ void __launch_bounds__(FFTShape<N>::THREADS)
+__global__ void __launch_bounds__(FFTShape<N>::THREADS, SGL_AZ_MINB)
 az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2* __restrict__ G,
                   const double* __restrict__ bcal, const double2* __restrict__ twg) {
     using S = FFTShape<N>;
@@ -186,28 +237,28 @@ az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2*
     const int jp = blockIdx.y;
     const int s0 = blockIdx.x * S::IG;
     const int nshell = g.batch * g.SC;
-    for (int x = tid; x < N; x += S::THREADS) tw[x] = twg[x];
-    // load 2*IG rings, coalesced along each ring
-    for (int idx = tid; idx < 2 * S::IG * N; idx += S::THREADS) {
-        const int q = idx / N, e = idx - q * N;
-        const int s = s0 + (q >> 1);
-        const int j = (q & 1) ? (N - 1 - jp) : jp;
-        double2 v = make_double2(0.0, 0.0);
-        if (s < nshell) {
-            const int f = s / g.SC, i = s - f * g.SC;
-            v = X[(size_t)f * fstride + ((size_t)i * N + j) * N + e];
-        }
-        rings[q * S::STRIDE + phys(e)] = v;
-    }
+    for (int x = tid; x < N; x += S::THREADS) tw[x] = __ldg(twg + x);
     __syncthreads();
     {
-        const int q = tid / S::T, t = tid - q * S::T;
-        ring_fft<N, -1>(rings + q * S::STRIDE, t, tw);
+        const int q = tid / S::T, tt = tid - q * S::T;
+        const int s = s0 + (q >> 1);
+        const int j = (q & 1) ? (N - 1 - jp) : jp;
+        const double2* src = X;
+        const bool ok = s < nshell;
+        if (ok) {
+            const int f = s / g.SC, i = s - f * g.SC;
+            src = X + (size_t)f * fstride + ((size_t)i * N + j) * N;
+        }
+        double2* ring = rings + q * S::STRIDE;
+        ring_fft_io<N, -1, false>(
+            ring, tt, tw, [&](int x) { return ok ? __ldcs(src + x) : make_double2(0.0, 0.0); },
+            [&](int x, double2 v) { ring[phys(x)] = v; });
     }
     __syncthreads();
     // epilogue: E/O fold, b_cal, scatter rows G[p][|m|][j'][sgn][s]
-    const double b = bcal[jp];
+    const double b = __ldg(bcal + jp);
     const long long row_len = g.NB / 2;  // complex per row
+#pragma unroll 4
     for (int idx = tid; idx < 2 * N * S::IG; idx += S::THREADS) {
         const int sl = idx % S::IG;
         const int rowi = idx / S::IG;  // p * N + bin
@@ -225,8 +276,12 @@ az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2*
 }
 
 // ------------------------------------------------------------------ azimuthal inverse
+// Prologue: cp.async E (p = 0) rows into the ring-j' buffer and O (p = 1) rows
+// into the ring-(2B-1-j') buffer.  The first FFT pass reads E +- O straight
+// from both buffers (Nyquist bin B zero); the last pass writes the psi-order
+// samples straight to HBM (coalesced).
 template <int N>
-__global__ void __launch_bounds__(FFTShape<N>::THREADS)
+__global__ void __launch_bounds__(FFTShape<N>::THREADS, SGL_AZ_MINB)
 az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X, size_t fstride,
                   const double2* __restrict__ twg) {
     using S = FFTShape<N>;
@@ -239,35 +294,49 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
     const int s0 = blockIdx.x * S::IG;
     const int nshell = g.batch * g.SC;
     const long long row_len = g.NB / 2;
-    for (int x = tid; x < N; x += S::THREADS) tw[x] = twg[x];
-    for (int idx = tid; idx < N * S::IG; idx += S::THREADS) {
+#pragma unroll 4
+    for (int idx = tid; idx < 2 * N * S::IG; idx += S::THREADS) {
         const int sl = idx % S::IG;
-        const int bin = idx / S::IG;
+        const int rowi = idx / S::IG;  // p * N + bin
+        const int p = rowi / N, bin = rowi - p * N;
         const int s = s0 + sl;
-        double2 e = make_double2(0.0, 0.0), o = make_double2(0.0, 0.0);
+        double2* dst = rings + (2 * sl + p) * S::STRIDE + phys(bin);
         if (bin != B && s < nshell) {
             const int m = bin < B ? bin : bin - N;
             const int am = m < 0 ? -m : m;
             const int sgn = m < 0 ? 1 : 0;
-            e = G[((((long long)0 * B + am) * B + jp) * 2 + sgn) * row_len + s];
-            o = G[((((long long)1 * B + am) * B + jp) * 2 + sgn) * row_len + s];
+            cp_async16(dst, G + ((((long long)p * B + am) * B + jp) * 2 + sgn) * row_len + s);
+        } else {
+            *dst = make_double2(0.0, 0.0);
         }
-        rings[(2 * sl) * S::STRIDE + phys(bin)] = cadd(e, o);
-        rings[(2 * sl + 1) * S::STRIDE + phys(bin)] = csub(e, o);
     }
+    for (int x = tid; x < N; x += S::THREADS) tw[x] = __ldg(twg + x);
+    cp_async_wait_all();
     __syncthreads();
     {
-        const int q = tid / S::T, t = tid - q * S::T;
-        ring_fft<N, +1>(rings + q * S::STRIDE, t, tw);
-    }
-    __syncthreads();
-    for (int idx = tid; idx < 2 * S::IG * N; idx += S::THREADS) {
-        const int q = idx / N, e = idx - q * N;
-        const int s = s0 + (q >> 1);
-        if (s >= nshell) continue;
-        const int j = (q & 1) ? (N - 1 - jp) : jp;
-        const int f = s / g.SC, i = s - f * g.SC;
-        X[(size_t)f * fstride + ((size_t)i * N + j) * N + e] = rings[q * S::STRIDE + phys(e)];
+        const int q = tid / S::T, tt = tid - q * S::T;
+        const int sl = q >> 1;
+        const int s = s0 + sl;
+        const bool mirror = q & 1;
+        const int j = mirror ? (N - 1 - jp) : jp;
+        double2* ring = rings + q * S::STRIDE;
+        const double2* e_buf = rings + (2 * sl) * S::STRIDE;
+        const double2* o_buf = rings + (2 * sl + 1) * S::STRIDE;
+        double2* dst = X;
+        const bool ok = s < nshell;
+        if (ok) {
+            const int f = s / g.SC, i = s - f * g.SC;
+            dst = X + (size_t)f * fstride + ((size_t)i * N + j) * N;
+        }
+        ring_fft_io<N, +1, true>(
+            ring, tt, tw,
+            [&](int x) {
+                const double2 e = e_buf[phys(x)], o = o_buf[phys(x)];
+                return mirror ? csub(e, o) : cadd(e, o);
+            },
+            [&](int x, double2 v) {
+                if (ok) __stcs(dst + x, v);
+            });
     }
 }
 
