@@ -295,14 +295,16 @@ def main():
     dom = int(np.argmax(stage_ms))
     per_launch_ms = stage_ms[dom] / max(1, stage_n[dom])
     flops, nbytes = work[dom]
-    flops *= nb
-    nbytes *= nb
+    # algorithmic work of one launch = per-step work / launches per step
+    lps = max(1, int(stage_n[dom]) // args.steps)
+    flops *= nb / lps
+    nbytes *= nb / lps
     stage_info = {}
     for s in range(6):
         if stage_n[s]:
-            t_ms = stage_ms[s] / stage_n[s]
+            t_ms = stage_ms[s] / args.steps  # per step (a stage may be split into several launches)
             stage_info[wl.STAGE_NAMES[s]] = {
-                "ms": round(t_ms, 5),
+                "ms": round(t_ms, 5), "launches_per_step": int(stage_n[s]) // args.steps,
                 "tflops": round(work[s][0] * nb / (t_ms * 1e-3) / 1e12, 3),
                 "gbs": round(work[s][1] * nb / (t_ms * 1e-3) / 1e9, 1),
                 "share": round(stage_ms[s] / stage_ms.sum(), 4),

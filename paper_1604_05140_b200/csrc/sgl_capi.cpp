@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -162,8 +163,10 @@ std::pair<sglk::Tile*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int 
         problem_shape(kind, B, batch, NB, pid, M, N, K);
         if (M <= 0 || N <= 0) continue;
         if (K <= 0 && kind != kLegInv) continue;  // LegInv with K = 0 must still write zeros
-        for (int m0 = 0; m0 < M; m0 += sglk::kBM)
-            for (int n0 = 0; n0 < N; n0 += sglk::kBN) v.push_back({pid, m0, n0, K});
+        const int wm = (kind == kLegFwd || kind == kLegInv) ? sglk::kWM_LEG : sglk::kWM_RAD;
+        const int bm = sglk::tile_rows(wm), bn = sglk::tile_cols(wm);
+        for (int m0 = 0; m0 < M; m0 += bm)
+            for (int n0 = 0; n0 < N; n0 += bn) v.push_back({pid, m0, n0, K});
     }
     std::stable_sort(v.begin(), v.end(), [](const sglk::Tile& a, const sglk::Tile& b) { return a.pad > b.pad; });
     sglk::Tile* d = nullptr;
@@ -210,59 +213,167 @@ size_t batch_chunk(int B, size_t batch) {
     return std::max<size_t>(1, std::min(batch, budget / per));
 }
 
+// L2 residency of the azimuthal -> polar intermediate G: the spherical stage
+// runs in slices whose G slice (64 B^2 bytes per shell and function) stays
+// below ~SGL_G_CHUNK_MB, so the Legendre kernel reads (forward) / the inverse FFT
+// reads (inverse) it from L2 right after it was written, instead of from HBM.
+// For batch == 1 the slice is a shell range; for batches it is a function range.
+struct Slices {
+    int count;       // number of slices
+    int shells;      // shells per slice (batch == 1) or 2B
+    int functions;   // functions per slice (batch > 1) or 1
+};
+
+Slices plan_slices(int B, int nb) {
+    // Measured on B200 (B = 128, one function): shell slices of 16-64 MiB cost more
+    // in per-launch tails than the L2 reuse saves, so a single function runs
+    // unsliced; batches are sliced to bound the workspace.
+    double mb = nb == 1 ? 0.0 : 1024.0;
+    if (const char* e = std::getenv("SGL_G_CHUNK_MB")) mb = std::atof(e);
+    const double per_shell = 64.0 * B * B;  // bytes of G per (shell, function)
+    const long long cap = std::max(1LL, (long long)(mb * 1048576.0 / per_shell));
+    Slices sl{1, 2 * B, nb};
+    if (mb <= 0) return sl;
+    if (nb == 1) {
+        int sh = 2 * B;
+        while (sh > cap && sh % 2 == 0) sh /= 2;  // 2B is a power of two for the FFT path
+        sl.shells = sh;
+        sl.count = (2 * B) / sh;
+    } else {
+        const long long per_fn = cap / (2 * B);
+        const int fpc = (int)std::max(1LL, std::min<long long>(nb, per_fn));
+        sl.functions = fpc;
+        sl.count = (nb + fpc - 1) / fpc;
+    }
+    return sl;
+}
+
 // Stage sequences on device memory.  X: samples (function stride Psi complex),
 // C: coefficients (function stride Omega complex).
 int forward_device(sglgpu_plan* p, const double* X, double* C, int nb, cudaStream_t st) {
     const int B = p->B;
-    sglk::Geo g{B, 2 * B, nb, 2LL * nb * 2 * B};
-    p->G.ensure((size_t)16 * B * B * B * nb);
+    const size_t psi2 = 2 * (size_t)sample_count(B), om2 = 2 * (size_t)coefficient_count(B);
+    const Slices sl = plan_slices(B, nb);
     p->S.ensure((size_t)4 * B * B * B * nb);
     int n = 0, k;
-    k = staged(p, 0, st, [&] {
-        return sglk::launch_az_forward(g, X, 2 * (size_t)sample_count(B), p->G.p, p->d_bcal, p->d_tw, st);
-    });
-    ck_launch(k, "az_forward");
-    n += k;
-    auto lt = tiles_for(p, kLegFwd, nb, 2 * B, 0, 2 * B);
-    k = staged(p, 1, st, [&] {
-        return sglk::launch_legendre_forward(g, p->G.p, p->S.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
-    });
-    ck_launch(k, "legendre_forward");
-    n += k;
-    auto rt = tiles_for(p, kRadFwd, nb, 2 * B, 0, B);
-    k = staged(p, 2, st, [&] {
-        return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, p->S.p, C, p->d_W, p->d_W_off,
-                                           rt.first, rt.second, st);
-    });
-    ck_launch(k, "radial_forward");
-    n += k;
+    if (nb == 1) {
+        // shell slices: az + Legendre per slice into the full S, then radial once
+        const int SC = sl.shells;
+        sglk::Geo gc{B, SC, 1, 2LL * SC};
+        p->G.ensure((size_t)4 * B * B * gc.NB);
+        const sglk::SView sv{2LL * 2 * B, 2 * B, 0};
+        auto lt = tiles_for(p, kLegFwd, 1, SC, 0, 2 * B);
+        for (int c = 0; c < sl.count; ++c) {
+            const int i0 = c * SC;
+            k = staged(p, 0, st, [&] {
+                return sglk::launch_az_forward(gc, X + (size_t)i0 * 2 * 4 * B * B, psi2, p->G.p, p->d_bcal, p->d_tw, st);
+            });
+            ck_launch(k, "az_forward");
+            n += k;
+            sglk::SView v = sv;
+            v.i0 = i0;
+            k = staged(p, 1, st, [&] {
+                return sglk::launch_legendre_forward(gc, v, p->G.p, p->S.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+            });
+            ck_launch(k, "legendre_forward");
+            n += k;
+        }
+        sglk::Geo g{B, 2 * B, 1, 2LL * 2 * B};
+        auto rt = tiles_for(p, kRadFwd, 1, 2 * B, 0, B);
+        k = staged(p, 2, st, [&] {
+            return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, p->S.p, C, p->d_W, p->d_W_off,
+                                               rt.first, rt.second, st);
+        });
+        ck_launch(k, "radial_forward");
+        return n + k;
+    }
+    // function slices: the whole forward per slice (G and S slices stay in L2)
+    for (int f0 = 0; f0 < nb; f0 += sl.functions) {
+        const int fb = std::min(sl.functions, nb - f0);
+        sglk::Geo g{B, 2 * B, fb, 2LL * fb * 2 * B};
+        p->G.ensure((size_t)4 * B * B * g.NB);
+        const sglk::SView sv{g.NB, 2 * B, 0};
+        auto lt = tiles_for(p, kLegFwd, fb, 2 * B, 0, 2 * B);
+        auto rt = tiles_for(p, kRadFwd, fb, 2 * B, 0, B);
+        k = staged(p, 0, st, [&] {
+            return sglk::launch_az_forward(g, X + (size_t)f0 * psi2, psi2, p->G.p, p->d_bcal, p->d_tw, st);
+        });
+        ck_launch(k, "az_forward");
+        n += k;
+        k = staged(p, 1, st, [&] {
+            return sglk::launch_legendre_forward(g, sv, p->G.p, p->S.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+        });
+        ck_launch(k, "legendre_forward");
+        n += k;
+        k = staged(p, 2, st, [&] {
+            return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, p->S.p, C + (size_t)f0 * om2,
+                                               p->d_W, p->d_W_off, rt.first, rt.second, st);
+        });
+        ck_launch(k, "radial_forward");
+        n += k;
+    }
     return n;
 }
 
 int inverse_device(sglgpu_plan* p, const double* C, double* X, int nb, cudaStream_t st) {
     const int B = p->B;
-    sglk::Geo g{B, 2 * B, nb, 2LL * nb * 2 * B};
-    p->G.ensure((size_t)16 * B * B * B * nb);
+    const size_t psi2 = 2 * (size_t)sample_count(B), om2 = 2 * (size_t)coefficient_count(B);
+    const Slices sl = plan_slices(B, nb);
     p->S.ensure((size_t)4 * B * B * B * nb);
     int n = 0, k;
-    auto rt = tiles_for(p, kRadInv, nb, 2 * B, 0, B);
-    k = staged(p, 3, st, [&] {
-        return sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, 0}, C, p->S.p, p->d_V, p->d_V_off,
-                                           rt.first, rt.second, st);
-    });
-    ck_launch(k, "radial_inverse");
-    n += k;
-    auto lt = tiles_for(p, kLegInv, nb, 2 * B, 0, 2 * B);
-    k = staged(p, 4, st, [&] {
-        return sglk::launch_legendre_inverse(g, p->S.p, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
-    });
-    ck_launch(k, "legendre_inverse");
-    n += k;
-    k = staged(p, 5, st, [&] {
-        return sglk::launch_az_inverse(g, p->G.p, X, 2 * (size_t)sample_count(B), p->d_tw, st);
-    });
-    ck_launch(k, "az_inverse");
-    n += k;
+    if (nb == 1) {
+        sglk::Geo g{B, 2 * B, 1, 2LL * 2 * B};
+        auto rt = tiles_for(p, kRadInv, 1, 2 * B, 0, B);
+        k = staged(p, 3, st, [&] {
+            return sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, 0}, C, p->S.p, p->d_V, p->d_V_off,
+                                               rt.first, rt.second, st);
+        });
+        ck_launch(k, "radial_inverse");
+        n += k;
+        const int SC = sl.shells;
+        sglk::Geo gc{B, SC, 1, 2LL * SC};
+        p->G.ensure((size_t)4 * B * B * gc.NB);
+        auto lt = tiles_for(p, kLegInv, 1, SC, 0, 2 * B);
+        for (int c = 0; c < sl.count; ++c) {
+            const int i0 = c * SC;
+            const sglk::SView v{2LL * 2 * B, 2 * B, i0};
+            k = staged(p, 4, st, [&] {
+                return sglk::launch_legendre_inverse(gc, v, p->S.p, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+            });
+            ck_launch(k, "legendre_inverse");
+            n += k;
+            k = staged(p, 5, st, [&] {
+                return sglk::launch_az_inverse(gc, p->G.p, X + (size_t)i0 * 2 * 4 * B * B, psi2, p->d_tw, st);
+            });
+            ck_launch(k, "az_inverse");
+            n += k;
+        }
+        return n;
+    }
+    for (int f0 = 0; f0 < nb; f0 += sl.functions) {
+        const int fb = std::min(sl.functions, nb - f0);
+        sglk::Geo g{B, 2 * B, fb, 2LL * fb * 2 * B};
+        p->G.ensure((size_t)4 * B * B * g.NB);
+        const sglk::SView sv{g.NB, 2 * B, 0};
+        auto rt = tiles_for(p, kRadInv, fb, 2 * B, 0, B);
+        auto lt = tiles_for(p, kLegInv, fb, 2 * B, 0, 2 * B);
+        k = staged(p, 3, st, [&] {
+            return sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, 0}, C + (size_t)f0 * om2, p->S.p,
+                                               p->d_V, p->d_V_off, rt.first, rt.second, st);
+        });
+        ck_launch(k, "radial_inverse");
+        n += k;
+        k = staged(p, 4, st, [&] {
+            return sglk::launch_legendre_inverse(g, sv, p->S.p, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+        });
+        ck_launch(k, "legendre_inverse");
+        n += k;
+        k = staged(p, 5, st, [&] {
+            return sglk::launch_az_inverse(g, p->G.p, X + (size_t)f0 * psi2, psi2, p->d_tw, st);
+        });
+        ck_launch(k, "az_inverse");
+        n += k;
+    }
     return n;
 }
 
@@ -451,7 +562,8 @@ int sglgpu_spherical_forward(sglgpu_plan* p, const double* samples, size_t sampl
         int n = sglk::launch_az_forward(g, samples, 2 * sample_stride, p->G.p, p->d_bcal, p->d_tw, st);
         ck_launch(n, "az_forward");
         auto lt = tiles_for(p, kLegFwd, nb, shell_count, 0, 2 * B);
-        int k = sglk::launch_legendre_forward(g, p->G.p, shells, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+        const sglk::SView sv{g.NB, shell_count, 0};
+        int k = sglk::launch_legendre_forward(g, sv, p->G.p, shells, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
         ck_launch(k, "legendre_forward");
         p->last_launches = n + k;
     });
@@ -472,7 +584,8 @@ int sglgpu_spherical_inverse(sglgpu_plan* p, const double* shells, double* sampl
         sglk::Geo g{B, shell_count, nb, 2LL * nb * shell_count};
         p->G.ensure((size_t)4 * B * B * g.NB);
         auto lt = tiles_for(p, kLegInv, nb, shell_count, 0, 2 * B);
-        int k = sglk::launch_legendre_inverse(g, shells, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+        const sglk::SView sv{g.NB, shell_count, 0};
+        int k = sglk::launch_legendre_inverse(g, sv, shells, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
         ck_launch(k, "legendre_inverse");
         int n = sglk::launch_az_inverse(g, p->G.p, samples, 2 * sample_stride, p->d_tw, st);
         ck_launch(n, "az_inverse");

@@ -215,6 +215,9 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NLEFT>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NLEFT)); }
 
 // ------------------------------------------------------------------ azimuthal forward
 // grid.x = ceil(nshell / IG), grid.y = B (j' = polar node in the northern half).
@@ -422,12 +425,23 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
 
 // --- problem kinds
 // Legendre forward: prob = 2|m| + p.  rows l = |m|+p+2r, K = B (j'), cols n' = sgn*NB + n.
+// Column n of a Legendre problem is (sgn, f, i_local, c) over the G chunk
+// (g.SC shells per function); it lands in S at (nu, f, sv.i0 + i_local, c)
+// of an S with sv.sc shells per function and sv.NB reals per nu row.
+__device__ __forceinline__ long long s_col(const Geo& g, const SView& sv, int am, int n) {
+    const int sgn = n >= g.NB;
+    const int nn = n - (sgn ? (int)g.NB : 0);
+    const int f = nn / (2 * g.SC), rem = nn - f * 2 * g.SC;
+    return (sgn ? -am : am) * sv.NB + (long long)f * 2 * sv.sc + 2LL * sv.i0 + rem;
+}
+
 struct LegFwd {
     Geo g;
     const double* A;        // table
     const long long* aoff;  // per prob
     const double* Bm;       // G
     double* C;              // S
+    SView sv;
     static constexpr bool A_KCONTIG = true;
     static constexpr bool B_KCONTIG = false;
     __device__ int am(int pid) const { return pid >> 1; }
@@ -442,13 +456,9 @@ struct LegFwd {
     __device__ long long colB(int, int n) const { return n; }
     __device__ long long rowC(int pid, int r) const {
         const long long l = am(pid) + (pid & 1) + 2 * r;
-        return l * (l + 1) * g.NB;
+        return l * (l + 1) * sv.NB;
     }
-    __device__ long long colC(int pid, int n) const {
-        const int sgn = n >= g.NB;
-        const long long nn = n - (sgn ? g.NB : 0);
-        return (sgn ? -am(pid) : am(pid)) * g.NB + nn;
-    }
+    __device__ long long colC(int pid, int n) const { return s_col(g, sv, am(pid), n); }
     __device__ double scaleC(int pid, int n) const { return (n >= g.NB && (am(pid) & 1)) ? -1.0 : 1.0; }
 };
 
@@ -459,6 +469,7 @@ struct LegInv {
     const long long* aoff;
     const double* Bm;  // S
     double* C;         // G
+    SView sv;
     static constexpr bool A_KCONTIG = false;
     static constexpr bool B_KCONTIG = false;
     __device__ int am(int pid) const { return pid >> 1; }
@@ -469,13 +480,9 @@ struct LegInv {
     __device__ long long colA(int, int k) const { return (long long)k * g.B; }
     __device__ long long rowB(int pid, int k) const {
         const long long l = am(pid) + (pid & 1) + 2 * k;
-        return l * (l + 1) * g.NB;
+        return l * (l + 1) * sv.NB;
     }
-    __device__ long long colB(int pid, int n) const {
-        const int sgn = n >= g.NB;
-        const long long nn = n - (sgn ? g.NB : 0);
-        return (sgn ? -am(pid) : am(pid)) * g.NB + nn;
-    }
+    __device__ long long colB(int pid, int n) const { return s_col(g, sv, am(pid), n); }
     __device__ long long rowC(int pid, int j) const {
         return ((((long long)(pid & 1) * g.B + am(pid)) * g.B + j) * 2) * g.NB;
     }
@@ -563,125 +570,210 @@ struct RadInv {
     __device__ double scaleC(int, int) const { return 1.0; }
 };
 
-template <class P>
-__global__ void __launch_bounds__(128) gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles) {
-    constexpr int BM = kBM, BN = kBN, BK = kBK;
-    constexpr int LDA = BK + 4;  // conflict-free A fragment loads
-    constexpr int LDB = BN + 4;  // conflict-free B fragment loads
-    __shared__ __align__(16) double As[2][BM][LDA];
-    __shared__ __align__(16) double Bs[2][BK][LDB];
+#ifndef SGL_GEMM_STAGES
+#define SGL_GEMM_STAGES 2
+#endif
+#ifndef SGL_GEMM_MINB
+#define SGL_GEMM_MINB 4
+#endif
+#ifndef SGL_GEMM_PERSISTENT
+#define SGL_GEMM_PERSISTENT 0
+#endif
 
-    const Tile t = tiles[blockIdx.x];
-    const int pid = t.prob, m0 = t.m0, n0 = t.n0;
-    const int M = pr.M(pid), N = pr.N(pid), K = pr.K(pid);
+__device__ __forceinline__ void cp_async8_zfill(void* smem_dst, const void* gmem_src, bool ok) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gmem_src), "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async16_zfill(void* smem_dst, const void* gmem_src, bool ok) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem_src), "r"(ok ? 16 : 0));
+}
+
+// Persistent grouped DMMA GEMM.  Each CTA walks its tiles (blockIdx.x,
+// + gridDim.x, ...) as one flat sequence of (tile, k-chunk) steps through a
+// STAGES-deep cp.async pipeline, so global loads stay in flight across tile
+// boundaries and the short-K tiles of the triangular problems pay no prologue.
+// 4 warps of 32 x 32 (4 x 4 m8n8k4 fragments), arranged WM x (4/WM): the CTA
+// tile is (32 WM) x (128 / WM).  WM = 1 for the wide Legendre problems, WM = 4
+// for the radial problems whose N = 2(2l+1) is narrow.  Shared-memory tiles are
+// stored with the operand's contiguous dimension innermost (row- or k-major)
+// so both the cp.async fills and the fragment loads are bank-conflict free.
+template <class P, int WM>
+struct GemmCfg {
+    static constexpr int BM = 32 * WM, BN = 128 / WM, BK = kBK, ST = SGL_GEMM_STAGES;
+    static constexpr int A_ELEMS = BM * BK;  // per stage
+    static constexpr int B_ELEMS = BK * BN;
+    // padded smem strides (B is always [k][n]; its (re, im) pairs move as 16 B)
+    static constexpr int LDA = P::A_KCONTIG ? BK + 4 : BM + 4;
+    static constexpr int LDB = BN + 4;
+    static constexpr int A_STAGE = P::A_KCONTIG ? BM * LDA : BK * LDA;
+    static constexpr int B_STAGE = BK * LDB;
+    static constexpr size_t SMEM = sizeof(double) * ST * (A_STAGE + B_STAGE);
+    static constexpr int AQ = A_ELEMS / 128;  // A elements per thread
+    static constexpr int BQ = B_ELEMS / 256;  // B (re, im) pairs per thread
+};
+
+template <class P, int WM>
+__global__ void __launch_bounds__(128, SGL_GEMM_MINB)
+gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles, int ntiles) {
+    using C = GemmCfg<P, WM>;
+    constexpr int BM = C::BM, BN = C::BN, BK = C::BK, ST = C::ST;
+    extern __shared__ __align__(16) double gsm[];
+    double* As = gsm;
+    double* Bs = gsm + ST * C::A_STAGE;
+
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wr = (warp % WM) * 32, wc = (warp / WM) * 32;
+    const int nmine = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
-    // ---- per-thread fixed load coordinates
-    // A: 512 elements per chunk, 4 per thread
-    int a_row[4], a_k[4];
-    long long a_rowoff[4];
+    // fixed per-thread load coordinates (tile-relative) and smem offsets
+    int a_row[C::AQ], a_k[C::AQ], a_so[C::AQ];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < C::AQ; ++q) {
         if (P::A_KCONTIG) {
-            a_row[q] = tid >> 2;
-            a_k[q] = (tid & 3) * 4 + q;
+            a_row[q] = (tid >> 2) + 32 * (q >> 2);
+            a_k[q] = (tid & 3) * 4 + (q & 3);
+            a_so[q] = a_row[q] * C::LDA + a_k[q];
         } else {
-            a_k[q] = tid >> 3;
-            a_row[q] = (tid & 7) * 4 + q;
+            const int e = tid + 128 * q;
+            a_row[q] = e % BM;
+            a_k[q] = e / BM;
+            a_so[q] = a_k[q] * C::LDA + a_row[q];
         }
-        const int row = m0 + a_row[q];
-        a_rowoff[q] = row < M ? pr.rowA(pid, row) : -1;
     }
-    // B: 1024 double2 per chunk, 8 per thread
-    int b_k[8], b_c[8];
-    long long b_coloff[8];  // may be negative (LegInv: -|m| rows); validity in b_ok
-    bool b_ok[8];
+    int b_k[C::BQ], b_c[C::BQ], b_so[C::BQ];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        if (P::B_KCONTIG) {
-            b_k[q] = tid & 15;
-            b_c[q] = ((tid >> 4) + 8 * q) * 2;
-        } else {
-            b_k[q] = (tid >> 6) + 2 * q;
-            b_c[q] = (tid & 63) * 2;
+    for (int q = 0; q < C::BQ; ++q) {
+        const int e = tid + 128 * q;
+        if (P::B_KCONTIG) {  // 8 consecutive k per column pair: 128 B global runs
+            const int hi = e >> 3;
+            b_k[q] = (e & 7) + 8 * (hi / (BN / 2));
+            b_c[q] = (hi % (BN / 2)) * 2;
+        } else {  // consecutive column pairs along a k row
+            b_c[q] = (e % (BN / 2)) * 2;
+            b_k[q] = e / (BN / 2);
         }
-        const int col = n0 + b_c[q];
-        b_ok[q] = col < N;
-        b_coloff[q] = b_ok[q] ? pr.colB(pid, col) : 0;
+        b_so[q] = b_k[q] * C::LDB + b_c[q];
     }
 
-    double2 rb[8];
-    double ra[4];
-    auto load_chunk = [&](int k0) {
+    // ---- issue side: walks (tile, chunk) ahead of the compute side
+    int is_it = 0, is_c = 0, is_pid = 0, is_K = 0, is_nch = 1;
+    long long is_arow[C::AQ], is_bcol[C::BQ];
+    unsigned is_aok = 0, is_bok = 0;
+    auto is_load_tile = [&](int it) {
+        const Tile t = tiles[blockIdx.x + it * gridDim.x];
+        is_pid = t.prob;
+        const int M = pr.M(is_pid), N = pr.N(is_pid);
+        is_K = pr.K(is_pid);
+        is_nch = is_K > 0 ? (is_K + BK - 1) / BK : 1;
+        is_aok = is_bok = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int k = k0 + a_k[q];
-            ra[q] = (a_rowoff[q] >= 0 && k < K) ? __ldg(pr.A + a_rowoff[q] + pr.colA(pid, k)) : 0.0;
+        for (int q = 0; q < C::AQ; ++q) {
+            const int row = t.m0 + a_row[q];
+            const bool ok = row < M;
+            is_aok |= (ok ? 1u : 0u) << q;
+            is_arow[q] = ok ? pr.rowA(is_pid, row) : 0;
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int k = k0 + b_k[q];
-            if (b_ok[q] && k < K) {
-                rb[q] = __ldg(reinterpret_cast<const double2*>(pr.Bm + pr.rowB(pid, k) + b_coloff[q]));
-            } else {
-                rb[q] = make_double2(0.0, 0.0);
+        for (int q = 0; q < C::BQ; ++q) {
+            const int col = t.n0 + b_c[q];
+            const bool ok = col < N;
+            is_bok |= (ok ? 1u : 0u) << q;
+            is_bcol[q] = ok ? pr.colB(is_pid, col) : 0;
+        }
+    };
+    int step_issue = 0;
+    auto issue_next = [&]() {
+        if (is_it < nmine) {
+            const int buf = step_issue % ST;
+            const int k0 = is_c * BK;
+            double* as = As + buf * C::A_STAGE;
+            double* bs = Bs + buf * C::B_STAGE;
+#pragma unroll
+            for (int q = 0; q < C::AQ; ++q) {
+                const int k = k0 + a_k[q];
+                const bool ok = ((is_aok >> q) & 1u) && k < is_K;
+                cp_async8_zfill(as + a_so[q], ok ? pr.A + is_arow[q] + pr.colA(is_pid, k) : pr.A, ok);
+            }
+#pragma unroll
+            for (int q = 0; q < C::BQ; ++q) {
+                const int k = k0 + b_k[q];
+                const bool ok = ((is_bok >> q) & 1u) && k < is_K;
+                cp_async16_zfill(bs + b_so[q], ok ? pr.Bm + pr.rowB(is_pid, k) + is_bcol[q] : pr.Bm, ok);
+            }
+            if (++is_c == is_nch) {
+                is_c = 0;
+                if (++is_it < nmine) is_load_tile(is_it);
             }
         }
-    };
-    auto store_chunk = [&](int buf) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) As[buf][a_row[q]][a_k[q]] = ra[q];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) *reinterpret_cast<double2*>(&Bs[buf][b_k[q]][b_c[q]]) = rb[q];
+        cp_async_commit();
+        ++step_issue;
     };
 
-    double acc[4][4][2];
+    if (nmine > 0) is_load_tile(0);
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int s = 0; s < ST - 1; ++s) issue_next();
 
-    const int fm_active = min(4, (M - m0 + 7) >> 3);
-    const int nchunks = (K + BK - 1) / BK;
-    load_chunk(0);
-    store_chunk(0);
-    __syncthreads();
-    for (int c = 0; c < nchunks; ++c) {
-        const int buf = c & 1;
-        if (c + 1 < nchunks) load_chunk((c + 1) * BK);
+    int step = 0;
+    for (int it = 0; it < nmine; ++it) {
+        const Tile t = tiles[blockIdx.x + it * gridDim.x];
+        const int pid = t.prob, m0 = t.m0, n0 = t.n0;
+        const int M = pr.M(pid), N = pr.N(pid), K = pr.K(pid);
+        const int nch = K > 0 ? (K + BK - 1) / BK : 1;
+        const int fm_active = max(0, min(4, (M - m0 - wr + 7) >> 3));
+        const int fn_active = max(0, min(4, (N - n0 - wc + 7) >> 3));
+        double acc[4][4][2];
 #pragma unroll
-        for (int kk = 0; kk < BK; kk += 4) {
-            double a[4], b[4];
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int fm = 0; fm < 4; ++fm) a[fm] = As[buf][fm * 8 + (lane >> 2)][kk + (lane & 3)];
+            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int c = 0; c < nch; ++c, ++step) {
+            cp_async_wait_group<ST - 2>();
+            __syncthreads();
+            issue_next();
+            const int buf = step % ST;
+            const double* as = As + buf * C::A_STAGE;
+            const double* bs = Bs + buf * C::B_STAGE;
 #pragma unroll
-            for (int fn = 0; fn < 4; ++fn) b[fn] = Bs[buf][kk + (lane & 3)][warp * 32 + fn * 8 + (lane >> 2)];
+            for (int kk = 0; kk < BK; kk += 4) {
+                double af[4], bf[4];
 #pragma unroll
-            for (int fm = 0; fm < 4; ++fm) {
-                if (fm < fm_active) {
+                for (int fm = 0; fm < 4; ++fm) {
+                    const int r = wr + fm * 8 + (lane >> 2), k = kk + (lane & 3);
+                    af[fm] = P::A_KCONTIG ? as[r * C::LDA + k] : as[k * C::LDA + r];
+                }
 #pragma unroll
-                    for (int fn = 0; fn < 4; ++fn) dmma884(acc[fm][fn], a[fm], b[fn]);
+                for (int fn = 0; fn < 4; ++fn) {
+                    const int n = wc + fn * 8 + (lane >> 2), k = kk + (lane & 3);
+                    bf[fn] = bs[k * C::LDB + n];
+                }
+#pragma unroll
+                for (int fm = 0; fm < 4; ++fm) {
+                    if (fm < fm_active) {
+#pragma unroll
+                        for (int fn = 0; fn < 4; ++fn)
+                            if (fn < fn_active) dmma884(acc[fm][fn], af[fm], bf[fn]);
+                    }
                 }
             }
         }
-        if (c + 1 < nchunks) store_chunk(buf ^ 1);
-        __syncthreads();
-    }
-    // ---- epilogue
+        // ---- epilogue (registers -> global)
 #pragma unroll
-    for (int fm = 0; fm < 4; ++fm) {
-        const int row = m0 + fm * 8 + (lane >> 2);
-        if (row >= M) continue;
-        const long long ro = pr.rowC(pid, row);
+        for (int fm = 0; fm < 4; ++fm) {
+            const int row = m0 + wr + fm * 8 + (lane >> 2);
+            if (row >= M) continue;
+            const long long ro = pr.rowC(pid, row);
 #pragma unroll
-        for (int fn = 0; fn < 4; ++fn) {
-            const int col = n0 + warp * 32 + fn * 8 + 2 * (lane & 3);
-            if (col >= N) continue;
-            const double s = pr.scaleC(pid, col);
-            *reinterpret_cast<double2*>(pr.C + ro + pr.colC(pid, col)) =
-                make_double2(s * acc[fm][fn][0], s * acc[fm][fn][1]);
+            for (int fn = 0; fn < 4; ++fn) {
+                const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
+                if (col >= N) continue;
+                const double sc = pr.scaleC(pid, col);
+                *reinterpret_cast<double2*>(pr.C + ro + pr.colC(pid, col)) =
+                    make_double2(sc * acc[fm][fn][0], sc * acc[fm][fn][1]);
+            }
         }
     }
+    cp_async_wait_group<0>();
 }
 
 // ------------------------------------------------------------------ launchers
@@ -766,37 +858,52 @@ int launch_az_inverse(const Geo& g, const double* G, double* samples, size_t sam
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-template <class P>
+template <class P, int WM>
 static int gemm_launch(const P& p, const Tile* tiles, int ntiles, cudaStream_t s) {
     if (ntiles <= 0) return 0;
-    gemm_dmma_kernel<P><<<ntiles, 128, 0, s>>>(p, tiles);
+    constexpr size_t smem = GemmCfg<P, WM>::SMEM;
+    static int resident = 0;
+    if (!resident) {
+        cudaFuncSetAttribute(gemm_dmma_kernel<P, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gemm_dmma_kernel<P, WM>, 128, smem);
+        resident = std::max(1, sms * std::max(1, per));
+    }
+#if SGL_GEMM_PERSISTENT
+    const int grid = std::min(resident, ntiles);
+#else
+    const int grid = ntiles;  // one tile per CTA; the block scheduler balances the ragged tiles
+#endif
+    gemm_dmma_kernel<P, WM><<<grid, 128, smem, s>>>(p, tiles, ntiles);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-int launch_legendre_forward(const Geo& g, const double* G, double* S, const double* tab,
+int launch_legendre_forward(const Geo& g, const SView& sv, const double* G, double* S, const double* tab,
                             const long long* tab_off, const Tile* tiles, int ntiles, cudaStream_t s) {
-    LegFwd p{g, tab, tab_off, G, S};
-    return gemm_launch(p, tiles, ntiles, s);
+    LegFwd p{g, tab, tab_off, G, S, sv};
+    return gemm_launch<LegFwd, kWM_LEG>(p, tiles, ntiles, s);
 }
 
-int launch_legendre_inverse(const Geo& g, const double* S, double* G, const double* tab,
+int launch_legendre_inverse(const Geo& g, const SView& sv, const double* S, double* G, const double* tab,
                             const long long* tab_off, const Tile* tiles, int ntiles, cudaStream_t s) {
-    LegInv p{g, tab, tab_off, S, G};
-    return gemm_launch(p, tiles, ntiles, s);
+    LegInv p{g, tab, tab_off, S, G, sv};
+    return gemm_launch<LegInv, kWM_LEG>(p, tiles, ntiles, s);
 }
 
 int launch_radial_forward(const Geo& g, const RadialBlocks& rb, const double* S, double* C,
                           const double* W, const long long* w_off, const Tile* tiles, int ntiles,
                           cudaStream_t s) {
     RadFwd p{g, W, w_off, S, C, degree_offset(g.B + 1), ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
-    return gemm_launch(p, tiles, ntiles, s);
+    return gemm_launch<RadFwd, kWM_RAD>(p, tiles, ntiles, s);
 }
 
 int launch_radial_inverse(const Geo& g, const RadialBlocks& rb, const double* C, double* S,
                           const double* V, const long long* v_off, const Tile* tiles, int ntiles,
                           cudaStream_t s) {
     RadInv p{g, V, v_off, C, S, degree_offset(g.B + 1), ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
-    return gemm_launch(p, tiles, ntiles, s);
+    return gemm_launch<RadInv, kWM_RAD>(p, tiles, ntiles, s);
 }
 
 }  // namespace sglk

@@ -15,9 +15,18 @@ struct Tile {
     int prob, m0, n0, pad;
 };
 
-constexpr int kBM = 32;   // CTA tile rows
-constexpr int kBN = 128;  // CTA tile cols (reals)
 constexpr int kBK = 16;   // k chunk
+// Warp arrangement of the 4-warp GEMM CTA: tile = (32 WM) rows x (128 / WM) cols.
+#ifndef SGL_WM_LEG
+#define SGL_WM_LEG 1
+#endif
+#ifndef SGL_WM_RAD
+#define SGL_WM_RAD 4
+#endif
+constexpr int kWM_LEG = SGL_WM_LEG;
+constexpr int kWM_RAD = SGL_WM_RAD;
+constexpr int tile_rows(int wm) { return 32 * wm; }
+constexpr int tile_cols(int wm) { return 128 / wm; }
 
 // Geometry shared by the stages.  "shell" is a flat index s = f * SC + i over
 // the functions of the batch and the SC radial shells handled by the call.
@@ -38,12 +47,21 @@ int launch_az_forward(const Geo& g, const double* samples, size_t sample_stride,
 int launch_az_inverse(const Geo& g, const double* G, double* samples, size_t sample_stride,
                       const double* twiddle, cudaStream_t s);
 
+// Window of the nu-major intermediate S[nu][f][i] a Legendre call touches: the
+// g.SC shells of the G chunk are shells [i0, i0 + g.SC) of an S with `sc`
+// shells per function and NB = batch * sc * 2 reals per nu row.
+struct SView {
+    long long NB;
+    int sc;
+    int i0;
+};
+
 // Polar stage: per (|m|, parity) DMMA contraction against the normalized
 // Legendre table.  tab: rows Pbar_{l,|m|}(cos theta_j'), j' < B.
-int launch_legendre_forward(const Geo& g, const double* G, double* S, const double* tab,
+int launch_legendre_forward(const Geo& g, const SView& sv, const double* G, double* S, const double* tab,
                             const long long* tab_off, const Tile* tiles, int ntiles,
                             cudaStream_t s);
-int launch_legendre_inverse(const Geo& g, const double* S, double* G, const double* tab,
+int launch_legendre_inverse(const Geo& g, const SView& sv, const double* S, double* G, const double* tab,
                             const long long* tab_off, const Tile* tiles, int ntiles,
                             cudaStream_t s);
 
