@@ -85,17 +85,22 @@ int sglgpu_inverse(sglgpu_plan* plan, const double* coeffs, double* samples, siz
  * the reference's shells[i][nu] buffer (sgl_transform.cpp:281, 319).
  *   spherical_forward: samples of shells [shell_begin, shell_begin+shell_count)
  *                      (psi-order slice, per function 4B^2*shell_count complex,
- *                      function stride `sample_stride` complex) -> shells
- *   radial_forward:    shells (shell_count == 2B) for degrees l in [l_begin, l_end)
- *                      -> coefficients (omega-order, function stride Omega)
- *   radial_inverse / spherical_inverse: the mirror images. */
+ *                      function stride `sample_stride` complex) -> shells (all nu)
+ *   radial_forward:    degrees l in [l_begin, l_end) -> coefficients (omega-order,
+ *                      function stride Omega; only those l's entries are written).
+ *                      The 2B shells arrive as 2B/shells_per_block blocks
+ *                      S_b[nu - l_begin^2][f][i_local] placed back to back (block b
+ *                      holds shells [b*spb, (b+1)*spb)) -- exactly what an
+ *                      all-to-all of per-rank spherical outputs delivers.
+ *   radial_inverse:    the mirror image (writes the same block layout)
+ *   spherical_inverse: shells (all nu, local shells) -> samples of those shells. */
 int sglgpu_spherical_forward(sglgpu_plan* plan, const double* samples, size_t sample_stride,
                              double* shells, int shell_begin, int shell_count, size_t batch,
                              void* stream);
 int sglgpu_radial_forward(sglgpu_plan* plan, const double* shells, double* coeffs, int l_begin,
-                          int l_end, size_t batch, void* stream);
+                          int l_end, int shells_per_block, size_t batch, void* stream);
 int sglgpu_radial_inverse(sglgpu_plan* plan, const double* coeffs, double* shells, int l_begin,
-                          int l_end, size_t batch, void* stream);
+                          int l_end, int shells_per_block, size_t batch, void* stream);
 int sglgpu_spherical_inverse(sglgpu_plan* plan, const double* shells, double* samples,
                              size_t sample_stride, int shell_begin, int shell_count,
                              size_t batch, void* stream);

@@ -60,7 +60,10 @@ def lib():
             getattr(L, name).argtypes = [_vp, _vp, ctypes.c_size_t, _vp, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_size_t, _vp]
         for name in ("sglgpu_radial_forward", "sglgpu_radial_inverse"):
-            getattr(L, name).argtypes = [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_size_t, _vp]
+            getattr(L, name).argtypes = [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_size_t,
+                                         _vp]
+        L.sglgpu_profile_begin.argtypes = [_vp]
+        L.sglgpu_profile_end.argtypes = [_vp, _vp, _vp]
         _lib = L
     return _lib
 

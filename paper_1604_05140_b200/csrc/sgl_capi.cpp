@@ -163,10 +163,15 @@ std::pair<sglk::Tile*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int 
         problem_shape(kind, B, batch, NB, pid, M, N, K);
         if (M <= 0 || N <= 0) continue;
         if (K <= 0 && kind != kLegInv) continue;  // LegInv with K = 0 must still write zeros
-        const int wm = (kind == kLegFwd || kind == kLegInv) ? sglk::kWM_LEG : sglk::kWM_RAD;
-        const int bm = sglk::tile_rows(wm), bn = sglk::tile_cols(wm);
+        const bool leg = kind == kLegFwd || kind == kLegInv;
+        const int wm = leg ? sglk::kWM_LEG : sglk::kWM_RAD;
+        const int bm = sglk::tile_rows(wm, leg ? sglk::kFM_LEG : sglk::kFM_RAD), bn = sglk::tile_cols(wm);
+        // Legendre tiles never straddle the +m / -m halves of N (so column
+        // addresses are affine inside a tile)
+        const int half = leg ? (int)NB : N;
         for (int m0 = 0; m0 < M; m0 += bm)
-            for (int n0 = 0; n0 < N; n0 += bn) v.push_back({pid, m0, n0, K});
+            for (int h0 = 0; h0 < N; h0 += half)
+                for (int n0 = h0; n0 < std::min(N, h0 + half); n0 += bn) v.push_back({pid, m0, n0, K});
     }
     std::stable_sort(v.begin(), v.end(), [](const sglk::Tile& a, const sglk::Tile& b) { return a.pad > b.pad; });
     sglk::Tile* d = nullptr;
@@ -594,18 +599,21 @@ int sglgpu_spherical_inverse(sglgpu_plan* p, const double* shells, double* sampl
 }
 
 int sglgpu_radial_forward(sglgpu_plan* p, const double* shells, double* coeffs, int l_begin, int l_end,
-                          size_t batch, void* stream) {
+                          int shells_per_block, size_t batch, void* stream) {
     return guarded([&] {
         check_plan(p);
         const int B = p->B;
         if (l_begin < 0 || l_end > B || l_begin > l_end) fail(SGLGPU_EINVAL, "sglgpu_radial_forward: bad l range");
+        if (shells_per_block < 1 || (2 * B) % shells_per_block != 0)
+            fail(SGLGPU_EINVAL, "sglgpu_radial_forward: shells_per_block must divide 2B");
         if (batch == 0 || l_begin == l_end) return;
         std::lock_guard<std::mutex> lock(p->mu);
         set_device(p);
-        const int nb = (int)batch;
-        sglk::Geo g{B, 2 * B, nb, 2LL * nb * 2 * B};
-        auto rt = tiles_for(p, kRadFwd, nb, 2 * B, l_begin, l_end);
-        int k = sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, (long long)l_begin * l_begin}, shells,
+        const int nb = (int)batch, sc = shells_per_block;
+        sglk::Geo g{B, sc, nb, 2LL * nb * sc};
+        const long long nu0 = (long long)l_begin * l_begin, nnu = (long long)l_end * l_end - nu0;
+        auto rt = tiles_for(p, kRadFwd, nb, sc, l_begin, l_end);
+        int k = sglk::launch_radial_forward(g, sglk::RadialBlocks{sc, nnu * g.NB, nu0}, shells,
                                             coeffs, p->d_W, p->d_W_off, rt.first, rt.second,
                                             static_cast<cudaStream_t>(stream));
         ck_launch(k, "radial_forward");
@@ -614,18 +622,21 @@ int sglgpu_radial_forward(sglgpu_plan* p, const double* shells, double* coeffs, 
 }
 
 int sglgpu_radial_inverse(sglgpu_plan* p, const double* coeffs, double* shells, int l_begin, int l_end,
-                          size_t batch, void* stream) {
+                          int shells_per_block, size_t batch, void* stream) {
     return guarded([&] {
         check_plan(p);
         const int B = p->B;
         if (l_begin < 0 || l_end > B || l_begin > l_end) fail(SGLGPU_EINVAL, "sglgpu_radial_inverse: bad l range");
+        if (shells_per_block < 1 || (2 * B) % shells_per_block != 0)
+            fail(SGLGPU_EINVAL, "sglgpu_radial_inverse: shells_per_block must divide 2B");
         if (batch == 0 || l_begin == l_end) return;
         std::lock_guard<std::mutex> lock(p->mu);
         set_device(p);
-        const int nb = (int)batch;
-        sglk::Geo g{B, 2 * B, nb, 2LL * nb * 2 * B};
-        auto rt = tiles_for(p, kRadInv, nb, 2 * B, l_begin, l_end);
-        int k = sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, (long long)l_begin * l_begin}, coeffs,
+        const int nb = (int)batch, sc = shells_per_block;
+        sglk::Geo g{B, sc, nb, 2LL * nb * sc};
+        const long long nu0 = (long long)l_begin * l_begin, nnu = (long long)l_end * l_end - nu0;
+        auto rt = tiles_for(p, kRadInv, nb, sc, l_begin, l_end);
+        int k = sglk::launch_radial_inverse(g, sglk::RadialBlocks{sc, nnu * g.NB, nu0}, coeffs,
                                             shells, p->d_V, p->d_V_off, rt.first, rt.second,
                                             static_cast<cudaStream_t>(stream));
         ck_launch(k, "radial_inverse");

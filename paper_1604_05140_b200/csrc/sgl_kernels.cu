@@ -448,8 +448,11 @@ struct LegFwd {
     __device__ int M(int pid) const { const int r = g.B - am(pid) - (pid & 1); return r > 0 ? (r + 1) / 2 : 0; }
     __device__ int N(int pid) const { return am(pid) == 0 ? (int)g.NB : 2 * (int)g.NB; }
     __device__ int K(int) const { return g.B; }
+    static constexpr bool B_COL_AFFINE = true;  // within a sign-half-aligned tile
     __device__ long long rowA(int pid, int r) const { return aoff[pid] + (long long)r * g.B; }
     __device__ long long colA(int, int k) const { return k; }
+    __device__ int a_sr(int) const { return g.B; }
+    __device__ int a_sk(int) const { return 1; }
     __device__ long long rowB(int pid, int k) const {
         return ((((long long)(pid & 1) * g.B + am(pid)) * g.B + k) * 2) * g.NB;
     }
@@ -476,8 +479,11 @@ struct LegInv {
     __device__ int M(int) const { return g.B; }
     __device__ int N(int pid) const { return am(pid) == 0 ? (int)g.NB : 2 * (int)g.NB; }
     __device__ int K(int pid) const { const int r = g.B - am(pid) - (pid & 1); return r > 0 ? (r + 1) / 2 : 0; }
+    static constexpr bool B_COL_AFFINE = true;
     __device__ long long rowA(int pid, int j) const { return aoff[pid] + j; }
     __device__ long long colA(int, int k) const { return (long long)k * g.B; }
+    __device__ int a_sr(int) const { return 1; }
+    __device__ int a_sk(int) const { return g.B; }
     __device__ long long rowB(int pid, int k) const {
         const long long l = am(pid) + (pid & 1) + 2 * k;
         return l * (l + 1) * sv.NB;
@@ -522,8 +528,11 @@ struct RadFwd {
     __device__ int M(int l) const { return g.B - l; }
     __device__ int N(int l) const { return (2 * l + 1) * g.batch * 2; }
     __device__ int K(int) const { return 2 * g.B; }
+    static constexpr bool B_COL_AFFINE = false;
     __device__ long long rowA(int l, int r) const { return aoff[l] + (long long)r * 2 * g.B; }
     __device__ long long colA(int, int k) const { return k; }
+    __device__ int a_sr(int) const { return 2 * g.B; }
+    __device__ int a_sk(int) const { return 1; }
     __device__ long long rowB(int, int k) const { return sb.row(k); }
     __device__ long long colB(int l, int n) const {
         const int mf = n >> 1, w = 2 * l + 1;
@@ -553,8 +562,11 @@ struct RadInv {
     __device__ int M(int) const { return 2 * g.B; }
     __device__ int N(int l) const { return (2 * l + 1) * g.batch * 2; }
     __device__ int K(int l) const { return g.B - l; }
+    static constexpr bool B_COL_AFFINE = false;
     __device__ long long rowA(int l, int i) const { return aoff[l] + (long long)i * (g.B - l); }
     __device__ long long colA(int, int k) const { return k; }
+    __device__ int a_sr(int l) const { return g.B - l; }
+    __device__ int a_sk(int) const { return 1; }
     __device__ long long rowB(int l, int k) const { return 2 * degree_offset(l + 1 + k); }
     __device__ long long colB(int l, int n) const {
         const int mf = n >> 1, w = 2 * l + 1;
@@ -575,6 +587,9 @@ struct RadInv {
 #endif
 #ifndef SGL_GEMM_MINB
 #define SGL_GEMM_MINB 4
+#endif
+#ifndef SGL_GEMM_MINB_WIDE
+#define SGL_GEMM_MINB_WIDE 3
 #endif
 #ifndef SGL_GEMM_PERSISTENT
 #define SGL_GEMM_PERSISTENT 0
@@ -598,9 +613,9 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem_dst, const void* gme
 // for the radial problems whose N = 2(2l+1) is narrow.  Shared-memory tiles are
 // stored with the operand's contiguous dimension innermost (row- or k-major)
 // so both the cp.async fills and the fragment loads are bank-conflict free.
-template <class P, int WM>
+template <class P, int WM, int FM>
 struct GemmCfg {
-    static constexpr int BM = 32 * WM, BN = 128 / WM, BK = kBK, ST = SGL_GEMM_STAGES;
+    static constexpr int BM = 8 * FM * WM, BN = 128 / WM, BK = kBK, ST = SGL_GEMM_STAGES;
     static constexpr int A_ELEMS = BM * BK;  // per stage
     static constexpr int B_ELEMS = BK * BN;
     // padded smem strides (B is always [k][n]; its (re, im) pairs move as 16 B)
@@ -613,17 +628,17 @@ struct GemmCfg {
     static constexpr int BQ = B_ELEMS / 256;  // B (re, im) pairs per thread
 };
 
-template <class P, int WM>
-__global__ void __launch_bounds__(128, SGL_GEMM_MINB)
+template <class P, int WM, int FM>
+__global__ void __launch_bounds__(128, FM > 4 ? SGL_GEMM_MINB_WIDE : SGL_GEMM_MINB)
 gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles, int ntiles) {
-    using C = GemmCfg<P, WM>;
+    using C = GemmCfg<P, WM, FM>;
     constexpr int BM = C::BM, BN = C::BN, BK = C::BK, ST = C::ST;
     extern __shared__ __align__(16) double gsm[];
     double* As = gsm;
     double* Bs = gsm + ST * C::A_STAGE;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wr = (warp % WM) * 32, wc = (warp / WM) * 32;
+    const int wr = (warp % WM) * 8 * FM, wc = (warp / WM) * 32;
     const int nmine = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
     // fixed per-thread load coordinates (tile-relative) and smem offsets
@@ -656,30 +671,35 @@ gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles, int ntiles) {
         b_so[q] = b_k[q] * C::LDB + b_c[q];
     }
 
-    // ---- issue side: walks (tile, chunk) ahead of the compute side
-    int is_it = 0, is_c = 0, is_pid = 0, is_K = 0, is_nch = 1;
-    long long is_arow[C::AQ], is_bcol[C::BQ];
-    unsigned is_aok = 0, is_bok = 0;
+    // ---- issue side: walks (tile, chunk) ahead of the compute side.  A rows
+    // are affine (base + row * sr + k * sk); B columns are affine within a
+    // tile for the Legendre problems (tiles never straddle the sign halves),
+    // else kept per load.
+    constexpr int BQC = P::B_COL_AFFINE ? 1 : C::BQ;
+    int is_it = 0, is_c = 0, is_pid = 0, is_K = 0, is_nch = 1, is_M = 0, is_N = 0, is_m0 = 0, is_n0 = 0;
+    int is_sr = 0, is_sk = 0;
+    long long is_abase = 0;
+    long long is_bcol[BQC];
     auto is_load_tile = [&](int it) {
         const Tile t = tiles[blockIdx.x + it * gridDim.x];
         is_pid = t.prob;
-        const int M = pr.M(is_pid), N = pr.N(is_pid);
+        is_m0 = t.m0;
+        is_n0 = t.n0;
+        is_M = pr.M(is_pid);
+        is_N = pr.N(is_pid);
         is_K = pr.K(is_pid);
         is_nch = is_K > 0 ? (is_K + BK - 1) / BK : 1;
-        is_aok = is_bok = 0;
+        is_abase = pr.rowA(is_pid, t.m0);
+        is_sr = pr.a_sr(is_pid);
+        is_sk = pr.a_sk(is_pid);
+        if constexpr (P::B_COL_AFFINE) {
+            is_bcol[0] = pr.colB(is_pid, t.n0);
+        } else {
 #pragma unroll
-        for (int q = 0; q < C::AQ; ++q) {
-            const int row = t.m0 + a_row[q];
-            const bool ok = row < M;
-            is_aok |= (ok ? 1u : 0u) << q;
-            is_arow[q] = ok ? pr.rowA(is_pid, row) : 0;
-        }
-#pragma unroll
-        for (int q = 0; q < C::BQ; ++q) {
-            const int col = t.n0 + b_c[q];
-            const bool ok = col < N;
-            is_bok |= (ok ? 1u : 0u) << q;
-            is_bcol[q] = ok ? pr.colB(is_pid, col) : 0;
+            for (int q = 0; q < C::BQ; ++q) {
+                const int col = t.n0 + b_c[q];
+                is_bcol[q] = col < is_N ? pr.colB(is_pid, col) : 0;
+            }
         }
     };
     int step_issue = 0;
@@ -692,14 +712,16 @@ gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles, int ntiles) {
 #pragma unroll
             for (int q = 0; q < C::AQ; ++q) {
                 const int k = k0 + a_k[q];
-                const bool ok = ((is_aok >> q) & 1u) && k < is_K;
-                cp_async8_zfill(as + a_so[q], ok ? pr.A + is_arow[q] + pr.colA(is_pid, k) : pr.A, ok);
+                const bool ok = is_m0 + a_row[q] < is_M && k < is_K;
+                const double* src = pr.A + is_abase + (long long)a_row[q] * is_sr + (long long)k * is_sk;
+                cp_async8_zfill(as + a_so[q], ok ? src : pr.A, ok);
             }
 #pragma unroll
             for (int q = 0; q < C::BQ; ++q) {
                 const int k = k0 + b_k[q];
-                const bool ok = ((is_bok >> q) & 1u) && k < is_K;
-                cp_async16_zfill(bs + b_so[q], ok ? pr.Bm + pr.rowB(is_pid, k) + is_bcol[q] : pr.Bm, ok);
+                const bool ok = is_n0 + b_c[q] < is_N && k < is_K;
+                const long long col = P::B_COL_AFFINE ? is_bcol[0] + b_c[q] : is_bcol[P::B_COL_AFFINE ? 0 : q];
+                cp_async16_zfill(bs + b_so[q], ok ? pr.Bm + pr.rowB(is_pid, k) + col : pr.Bm, ok);
             }
             if (++is_c == is_nch) {
                 is_c = 0;
@@ -720,11 +742,11 @@ gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles, int ntiles) {
         const int pid = t.prob, m0 = t.m0, n0 = t.n0;
         const int M = pr.M(pid), N = pr.N(pid), K = pr.K(pid);
         const int nch = K > 0 ? (K + BK - 1) / BK : 1;
-        const int fm_active = max(0, min(4, (M - m0 - wr + 7) >> 3));
+        const int fm_active = max(0, min(FM, (M - m0 - wr + 7) >> 3));
         const int fn_active = max(0, min(4, (N - n0 - wc + 7) >> 3));
-        double acc[4][4][2];
+        double acc[FM][4][2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < FM; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
         for (int c = 0; c < nch; ++c, ++step) {
@@ -736,9 +758,9 @@ gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles, int ntiles) {
             const double* bs = Bs + buf * C::B_STAGE;
 #pragma unroll
             for (int kk = 0; kk < BK; kk += 4) {
-                double af[4], bf[4];
+                double af[FM], bf[4];
 #pragma unroll
-                for (int fm = 0; fm < 4; ++fm) {
+                for (int fm = 0; fm < FM; ++fm) {
                     const int r = wr + fm * 8 + (lane >> 2), k = kk + (lane & 3);
                     af[fm] = P::A_KCONTIG ? as[r * C::LDA + k] : as[k * C::LDA + r];
                 }
@@ -748,7 +770,7 @@ gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles, int ntiles) {
                     bf[fn] = bs[k * C::LDB + n];
                 }
 #pragma unroll
-                for (int fm = 0; fm < 4; ++fm) {
+                for (int fm = 0; fm < FM; ++fm) {
                     if (fm < fm_active) {
 #pragma unroll
                         for (int fn = 0; fn < 4; ++fn)
@@ -759,7 +781,7 @@ gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles, int ntiles) {
         }
         // ---- epilogue (registers -> global)
 #pragma unroll
-        for (int fm = 0; fm < 4; ++fm) {
+        for (int fm = 0; fm < FM; ++fm) {
             const int row = m0 + wr + fm * 8 + (lane >> 2);
             if (row >= M) continue;
             const long long ro = pr.rowC(pid, row);
@@ -858,17 +880,17 @@ int launch_az_inverse(const Geo& g, const double* G, double* samples, size_t sam
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-template <class P, int WM>
+template <class P, int WM, int FM>
 static int gemm_launch(const P& p, const Tile* tiles, int ntiles, cudaStream_t s) {
     if (ntiles <= 0) return 0;
-    constexpr size_t smem = GemmCfg<P, WM>::SMEM;
+    constexpr size_t smem = GemmCfg<P, WM, FM>::SMEM;
     static int resident = 0;
     if (!resident) {
-        cudaFuncSetAttribute(gemm_dmma_kernel<P, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(gemm_dmma_kernel<P, WM, FM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int dev = 0, sms = 0, per = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gemm_dmma_kernel<P, WM>, 128, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gemm_dmma_kernel<P, WM, FM>, 128, smem);
         resident = std::max(1, sms * std::max(1, per));
     }
 #if SGL_GEMM_PERSISTENT
@@ -876,34 +898,34 @@ static int gemm_launch(const P& p, const Tile* tiles, int ntiles, cudaStream_t s
 #else
     const int grid = ntiles;  // one tile per CTA; the block scheduler balances the ragged tiles
 #endif
-    gemm_dmma_kernel<P, WM><<<grid, 128, smem, s>>>(p, tiles, ntiles);
+    gemm_dmma_kernel<P, WM, FM><<<grid, 128, smem, s>>>(p, tiles, ntiles);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 int launch_legendre_forward(const Geo& g, const SView& sv, const double* G, double* S, const double* tab,
                             const long long* tab_off, const Tile* tiles, int ntiles, cudaStream_t s) {
     LegFwd p{g, tab, tab_off, G, S, sv};
-    return gemm_launch<LegFwd, kWM_LEG>(p, tiles, ntiles, s);
+    return gemm_launch<LegFwd, kWM_LEG, kFM_LEG>(p, tiles, ntiles, s);
 }
 
 int launch_legendre_inverse(const Geo& g, const SView& sv, const double* S, double* G, const double* tab,
                             const long long* tab_off, const Tile* tiles, int ntiles, cudaStream_t s) {
     LegInv p{g, tab, tab_off, S, G, sv};
-    return gemm_launch<LegInv, kWM_LEG>(p, tiles, ntiles, s);
+    return gemm_launch<LegInv, kWM_LEG, kFM_LEG>(p, tiles, ntiles, s);
 }
 
 int launch_radial_forward(const Geo& g, const RadialBlocks& rb, const double* S, double* C,
                           const double* W, const long long* w_off, const Tile* tiles, int ntiles,
                           cudaStream_t s) {
     RadFwd p{g, W, w_off, S, C, degree_offset(g.B + 1), ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
-    return gemm_launch<RadFwd, kWM_RAD>(p, tiles, ntiles, s);
+    return gemm_launch<RadFwd, kWM_RAD, kFM_RAD>(p, tiles, ntiles, s);
 }
 
 int launch_radial_inverse(const Geo& g, const RadialBlocks& rb, const double* C, double* S,
                           const double* V, const long long* v_off, const Tile* tiles, int ntiles,
                           cudaStream_t s) {
     RadInv p{g, V, v_off, C, S, degree_offset(g.B + 1), ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
-    return gemm_launch<RadInv, kWM_RAD>(p, tiles, ntiles, s);
+    return gemm_launch<RadInv, kWM_RAD, kFM_RAD>(p, tiles, ntiles, s);
 }
 
 }  // namespace sglk

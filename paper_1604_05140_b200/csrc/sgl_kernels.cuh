@@ -23,9 +23,17 @@ constexpr int kBK = 16;   // k chunk
 #ifndef SGL_WM_RAD
 #define SGL_WM_RAD 4
 #endif
+#ifndef SGL_FM_LEG
+#define SGL_FM_LEG 8
+#endif
+#ifndef SGL_FM_RAD
+#define SGL_FM_RAD 4
+#endif
 constexpr int kWM_LEG = SGL_WM_LEG;
 constexpr int kWM_RAD = SGL_WM_RAD;
-constexpr int tile_rows(int wm) { return 32 * wm; }
+constexpr int kFM_LEG = SGL_FM_LEG;  // 8-row DMMA fragments per warp along M
+constexpr int kFM_RAD = SGL_FM_RAD;
+constexpr int tile_rows(int wm, int fm) { return 8 * fm * wm; }
 constexpr int tile_cols(int wm) { return 128 / wm; }
 
 // Geometry shared by the stages.  "shell" is a flat index s = f * SC + i over

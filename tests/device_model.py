@@ -115,3 +115,69 @@ class DeviceModel:
                 rings[:, jp, m % N] = (Y[0] + Y[1]).T
                 rings[:, N - 1 - jp, m % N] = (Y[0] - Y[1]).T
         return (np.fft.ifft(rings, axis=2) * N).reshape(-1)
+
+
+class ModelStages:
+    """CPU stand-in for distributed.CudaStages (test infrastructure): the same four
+    stage entry points and layouts, computed with the oracle's stage functions
+    (sft_seminaive_* and drt_* restatements).  Lets the multi-GPU orchestration
+    run over gloo on CPU."""
+
+    def __init__(self, B):
+        from oracle_bindings import Oracle
+
+        self.B = B
+        self.o = Oracle(B)
+
+    def spherical_forward(self, samples_local, s0, sc, batch):
+        import torch
+
+        B = self.B
+        x = samples_local.numpy().reshape(batch, sc, 4 * B * B)
+        out = np.zeros((B * B, batch, sc), dtype=np.complex128)
+        for f in range(batch):
+            for i in range(sc):
+                out[:, f, i] = self.o.sft_forward(x[f, i])
+        return torch.from_numpy(out.reshape(-1))
+
+    def radial_forward(self, blocks, l0, l1, spb, batch, coeffs_out):
+        B = self.B
+        nb = 2 * B // spb
+        nnu = l1 * l1 - l0 * l0
+        blk = blocks.numpy().reshape(nb, nnu, batch, spb)
+        c = coeffs_out.numpy()
+        for l in range(l0, l1):
+            for m in range(-l, l + 1):
+                nu = l * (l + 1) + m - l0 * l0
+                for f in range(batch):
+                    s = blk[:, nu, f, :].reshape(-1)
+                    t = self.o.drt_forward(l, s)
+                    for n in range(l + 1, B + 1):
+                        c[f, (n - 1) * n * (2 * n - 1) // 6 + l * (l + 1) + m] = t[n - l - 1]
+
+    def radial_inverse(self, coeffs, l0, l1, spb, batch):
+        import torch
+
+        B = self.B
+        nb = 2 * B // spb
+        nnu = l1 * l1 - l0 * l0
+        out = np.zeros((nb, nnu, batch, spb), dtype=np.complex128)
+        c = coeffs.numpy()
+        for l in range(l0, l1):
+            for m in range(-l, l + 1):
+                nu = l * (l + 1) + m - l0 * l0
+                for f in range(batch):
+                    t = np.array([c[f, (n - 1) * n * (2 * n - 1) // 6 + l * (l + 1) + m] for n in range(l + 1, B + 1)])
+                    out[:, nu, f, :] = self.o.drt_inverse(l, t).reshape(nb, spb)
+        return torch.from_numpy(out.reshape(-1))
+
+    def spherical_inverse(self, shells_local, s0, sc, batch):
+        import torch
+
+        B = self.B
+        S = shells_local.numpy().reshape(B * B, batch, sc)
+        out = np.zeros((batch, sc, 4 * B * B), dtype=np.complex128)
+        for f in range(batch):
+            for i in range(sc):
+                out[f, i] = self.o.sft_inverse(S[:, f, i])
+        return torch.from_numpy(out.reshape(-1))

@@ -87,3 +87,204 @@ def test_roundtrip_b256():
     assert np.isfinite(g).all()
     back = sgl.fsglft(sgl.SampleGrid(B, g), plan).values
     assert normwise(back, c) <= TOL
+
+
+# ----------------------------------------------------------------- golden fixtures (reference outputs)
+import os  # noqa: E402
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _gold(name):
+    return np.fromfile(os.path.join(GOLDEN, name), dtype="<f8").view(np.complex128)
+
+
+@pytest.mark.parametrize("B", [2, 4, 8, 16])
+def test_gpu_matches_reference_golden(B):
+    plan, _ = plan_for(B)
+    c = _gold(f"rt_B{B}_coeffs.bin")
+    g = sgl.ifsglft(sgl.SglCoefficients(B, c), plan).values
+    assert per_shell(g, _gold(f"rt_B{B}_grid.bin"), B) <= 1e-13
+    f = sgl.fsglft(sgl.SampleGrid(B, _gold(f"rt_B{B}_grid.bin")), plan).values
+    assert normwise(f, _gold(f"rt_B{B}_back.bin")) <= 1e-13
+
+
+def test_gpu_matrix_semantics_b2():
+    """fsglft is the reference's matrix (test_sgl_transform.cpp:303-330), and ifsglft is
+    the conjugate transpose of the weight-stripped forward (:332-345)."""
+    import torch
+
+    B = 2
+    plan, orc = plan_for(B)
+    mat = _gold("mat_B2_forward.bin").reshape(sgl.sample_count(B), sgl.coefficient_count(B))
+    eye = torch.eye(sgl.sample_count(B), dtype=torch.complex128).cuda().contiguous()
+    cols = sgl.fsglft_batch(plan, eye).cpu().numpy()
+    assert np.abs(cols - mat).max() < 1e-12
+    eye_c = torch.eye(sgl.coefficient_count(B), dtype=torch.complex128).cuda().contiguous()
+    inv_cols = sgl.ifsglft_batch(plan, eye_c).cpu().numpy()  # [omega][psi]
+    w = (np.exp(-orc.r ** 2) * orc.a_mod)[:, None, None] * orc.b_cal[None, :, None]
+    w = np.broadcast_to(w, (2 * B, 2 * B, 2 * B)).reshape(-1)
+    stripped = mat / w[:, None]
+    assert np.abs(inv_cols - np.conj(stripped).T).max() < 1e-12
+
+
+def test_gpu_exact_on_sampled_basis():
+    """test_sgl_transform.cpp:176-191: fsglft(sampled H_nlm) = unit vector, B = 4."""
+    import torch
+
+    B = 4
+    plan, orc = plan_for(B)
+    grids, targets = [], []
+    for n in range(1, B + 1):
+        for l in range(n):
+            for m in range(-l, l + 1):
+                grids.append(orc.sample_basis(n, l, m))
+                t = np.zeros(sgl.coefficient_count(B), dtype=np.complex128)
+                t[sgl.omega_index(n, l, m)] = 1.0
+                targets.append(t)
+    out = sgl.fsglft_batch(plan, torch.from_numpy(np.stack(grids)).cuda()).cpu().numpy()
+    assert np.abs(out - np.stack(targets)).max() < 1e-10
+
+
+def test_gpu_unit_coefficient_b3_golden():
+    B = 3
+    plan, _ = plan_for(B)
+    u = np.zeros(sgl.coefficient_count(B), dtype=np.complex128)
+    u[sgl.omega_index(2, 1, 0)] = 1.0
+    g = sgl.ifsglft(sgl.SglCoefficients(B, u), plan).values
+    assert np.abs(g - _gold("basis_B3_210.bin")).max() < 1e-11
+
+
+def test_gpu_zero_and_linearity():
+    B = 8
+    plan, _ = plan_for(B)
+    z = sgl.fsglft(sgl.SampleGrid(B, np.zeros(sgl.sample_count(B), complex)), plan).values
+    assert not np.abs(z).any()
+    z = sgl.ifsglft(sgl.SglCoefficients(B, np.zeros(sgl.coefficient_count(B), complex)), plan).values
+    assert not np.abs(z).any()
+    rng = np.random.default_rng(3)
+    g1, g2 = (complex_normal(rng, sgl.sample_count(B)) for _ in range(2))
+    a = 1.4 - 0.3j
+    f = lambda g: sgl.fsglft(sgl.SampleGrid(B, g), plan).values  # noqa: E731
+    assert np.abs(f(a * g1 + g2) - (a * f(g1) + f(g2))).max() < 1e-11
+
+
+def test_gpu_deterministic():
+    B = 16
+    plan, _ = plan_for(B)
+    g = complex_normal(np.random.default_rng(5), sgl.sample_count(B))
+    a = sgl.fsglft(sgl.SampleGrid(B, g), plan).values
+    b = sgl.fsglft(sgl.SampleGrid(B, g), plan).values
+    assert np.array_equal(a, b)
+
+
+# ----------------------------------------------------------------- BASELINE configs (reduced batch)
+def test_config_c2_batch_b64():
+    """C2: B = 64, coefficients x exp(-n/16), batched (here 4 functions)."""
+    import torch
+
+    B = 64
+    plan, orc = plan_for(B)
+    n_of = np.concatenate([[n] * (n * n) for n in range(1, B + 1)])
+    rng = np.random.default_rng(64)
+    c = complex_normal(rng, (4, sgl.coefficient_count(B))) * np.exp(-n_of / 16.0)
+    g = sgl.ifsglft_batch(plan, torch.from_numpy(c).cuda())
+    back = sgl.fsglft_batch(plan, g).cpu().numpy()
+    g = g.cpu().numpy()
+    for f in range(4):
+        assert per_shell(g[f], orc.inverse(c[f]), B) <= TOL
+        assert normwise(back[f], c[f]) <= TOL
+
+
+def test_config_c5_real_valued_b32():
+    """C5: B = 32 real-valued functions, f_{nl,-m} = (-1)^m conj(f_nlm): samples are
+    real to roundoff and the round trip holds (here 8 functions)."""
+    import torch
+
+    B = 32
+    plan, _ = plan_for(B)
+    rng = np.random.default_rng(32)
+    nb = 8
+    c = np.zeros((nb, sgl.coefficient_count(B)), dtype=np.complex128)
+    for n in range(1, B + 1):
+        for l in range(n):
+            for m in range(0, l + 1):
+                w = sgl.omega_index(n, l, m)
+                if m == 0:
+                    c[:, w] = rng.standard_normal(nb) * np.exp(-n / 8.0)
+                else:
+                    v = complex_normal(rng, nb) * np.exp(-n / 8.0)
+                    c[:, w] = v
+                    c[:, sgl.omega_index(n, l, -m)] = (-1) ** m * np.conj(v)
+    g = sgl.ifsglft_batch(plan, torch.from_numpy(c).cuda())
+    gi = g.imag.abs().max().item() / g.abs().max().item()
+    assert gi < 1e-13
+    back = sgl.fsglft_batch(plan, g).cpu().numpy()
+    assert normwise(back, c) <= TOL
+
+
+# ----------------------------------------------------------------- multi-GPU stage entry points
+@pytest.mark.parametrize("B,W,batch", [(16, 2, 1), (16, 4, 3), (64, 8, 1)])
+def test_stage_entry_points_emulated_split(B, W, batch):
+    """The shell / (l, m) decomposition of paper_1604_05140_b200.distributed with the
+    CUDA stages, all ranks emulated one after another on one GPU (the all-to-all
+    becomes tensor slicing; nothing waits on another rank)."""
+    import torch
+
+    from paper_1604_05140_b200.distributed import CudaStages, Partition
+
+    plan, orc = plan_for(B)
+    st = CudaStages(plan)
+    part = Partition.make(B, W)
+    rng = np.random.default_rng(B + W)
+    c = complex_normal(rng, (batch, sgl.coefficient_count(B)))
+    g_full = np.stack([orc.inverse(c[f]) for f in range(batch)])
+    sc, n_sh = part.shells_per_rank, 4 * B * B
+    dg = torch.from_numpy(g_full).cuda()
+    S_loc = []
+    for r in range(W):
+        s0, s1 = part.shell_range(r)
+        S_loc.append(st.spherical_forward(dg[:, s0 * n_sh:s1 * n_sh].contiguous(), s0, sc, batch)
+                     .view(B * B, batch * sc))
+    coeffs = torch.zeros((batch, sgl.coefficient_count(B)), dtype=torch.complex128, device="cuda")
+    for q in range(W):
+        nu0, nu1 = part.nu_range(q)
+        l0, l1 = part.l_ranges[q]
+        if l1 == l0:
+            continue
+        blocks = torch.cat([S_loc[r][nu0:nu1].reshape(-1) for r in range(W)])
+        part_c = torch.zeros_like(coeffs)
+        st.radial_forward(blocks, l0, l1, sc, batch, part_c)
+        coeffs += part_c
+    ref = np.stack([orc.forward(g_full[f]) for f in range(batch)])
+    assert normwise(coeffs.cpu().numpy(), ref) <= TOL
+    # inverse
+    dc = torch.from_numpy(c).cuda()
+    sent = []
+    for q in range(W):
+        l0, l1 = part.l_ranges[q]
+        nu0, nu1 = part.nu_range(q)
+        blk = st.radial_inverse(dc, l0, l1, sc, batch) if l1 > l0 else torch.zeros(0, dtype=torch.complex128, device="cuda")
+        sent.append(blk.view(W, -1))
+    for r in range(W):
+        S_r = torch.cat([sent[q][r] for q in range(W)])
+        s0, s1 = part.shell_range(r)
+        x = st.spherical_inverse(S_r.contiguous(), s0, sc, batch).view(batch, -1).cpu().numpy()
+        for f in range(batch):
+            assert normwise(x[f], g_full[f, s0 * n_sh:s1 * n_sh]) <= 1e-12
+
+
+# ----------------------------------------------------------------- C++ API (the drop-in surface)
+def test_cpp_api_driver():
+    import subprocess
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join("/tmp", "sgl_b200_test_sgl_api")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(repo, "include"),
+                    os.path.join(repo, "tests", "cpp", "test_sgl_api.cpp"),
+                    "-L", os.path.join(repo, "paper_1604_05140_b200"), "-lsglb200",
+                    "-Wl,-rpath," + os.path.join(repo, "paper_1604_05140_b200"), "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "[FAIL]" not in out.stdout
