@@ -449,6 +449,8 @@ struct LegFwd {
     __device__ int N(int pid) const { return am(pid) == 0 ? (int)g.NB : 2 * (int)g.NB; }
     __device__ int K(int) const { return g.B; }
     static constexpr bool B_COL_AFFINE = true;  // within a sign-half-aligned tile
+    // end (exclusive) of the sign half that column n0 lies in
+    __device__ int nlim(int pid, int n0) const { return n0 < g.NB ? (int)g.NB : N(pid); }
     __device__ long long rowA(int pid, int r) const { return aoff[pid] + (long long)r * g.B; }
     __device__ long long colA(int, int k) const { return k; }
     __device__ int a_sr(int) const { return g.B; }
@@ -480,6 +482,7 @@ struct LegInv {
     __device__ int N(int pid) const { return am(pid) == 0 ? (int)g.NB : 2 * (int)g.NB; }
     __device__ int K(int pid) const { const int r = g.B - am(pid) - (pid & 1); return r > 0 ? (r + 1) / 2 : 0; }
     static constexpr bool B_COL_AFFINE = true;
+    __device__ int nlim(int pid, int n0) const { return n0 < g.NB ? (int)g.NB : N(pid); }
     __device__ long long rowA(int pid, int j) const { return aoff[pid] + j; }
     __device__ long long colA(int, int k) const { return (long long)k * g.B; }
     __device__ int a_sr(int) const { return 1; }
@@ -529,6 +532,7 @@ struct RadFwd {
     __device__ int N(int l) const { return (2 * l + 1) * g.batch * 2; }
     __device__ int K(int) const { return 2 * g.B; }
     static constexpr bool B_COL_AFFINE = false;
+    __device__ int nlim(int l, int) const { return N(l); }
     __device__ long long rowA(int l, int r) const { return aoff[l] + (long long)r * 2 * g.B; }
     __device__ long long colA(int, int k) const { return k; }
     __device__ int a_sr(int) const { return 2 * g.B; }
@@ -563,6 +567,7 @@ struct RadInv {
     __device__ int N(int l) const { return (2 * l + 1) * g.batch * 2; }
     __device__ int K(int l) const { return g.B - l; }
     static constexpr bool B_COL_AFFINE = false;
+    __device__ int nlim(int l, int) const { return N(l); }
     __device__ long long rowA(int l, int i) const { return aoff[l] + (long long)i * (g.B - l); }
     __device__ long long colA(int, int k) const { return k; }
     __device__ int a_sr(int l) const { return g.B - l; }
@@ -686,7 +691,7 @@ gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles, int ntiles) {
         is_m0 = t.m0;
         is_n0 = t.n0;
         is_M = pr.M(is_pid);
-        is_N = pr.N(is_pid);
+        is_N = pr.nlim(is_pid, t.n0);
         is_K = pr.K(is_pid);
         is_nch = is_K > 0 ? (is_K + BK - 1) / BK : 1;
         is_abase = pr.rowA(is_pid, t.m0);
@@ -740,7 +745,7 @@ gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles, int ntiles) {
     for (int it = 0; it < nmine; ++it) {
         const Tile t = tiles[blockIdx.x + it * gridDim.x];
         const int pid = t.prob, m0 = t.m0, n0 = t.n0;
-        const int M = pr.M(pid), N = pr.N(pid), K = pr.K(pid);
+        const int M = pr.M(pid), N = pr.nlim(pid, n0), K = pr.K(pid);
         const int nch = K > 0 ? (K + BK - 1) / BK : 1;
         const int fm_active = max(0, min(FM, (M - m0 - wr + 7) >> 3));
         const int fn_active = max(0, min(4, (N - n0 - wc + 7) >> 3));
