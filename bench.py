@@ -197,12 +197,19 @@ def main():
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="split", choices=["split", "replicas"],
+                    help="N>1: split one transform by shells / (l, m) (strong scaling, default) "
+                         "or run independent replicas (weak scaling)")
+    ap.add_argument("--force-split", action="store_true", help="run the split path even at N=1 (testing)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = env_rank()
 
     if args.impl == "reference":
         reference_arm(args, rank, world)
+        return
+    if (world > 1 and args.mode == "split") or args.force_split:
+        split_arm(args, rank, world, local)
         return
 
     import torch
@@ -351,6 +358,97 @@ def main():
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def split_arm(args, rank, world, local):
+    """N > 1: one B = 128 transform per step split over the ranks -- spherical stage
+    by radial shell, radial stage by degree range, NCCL all-to-all in between
+    (paper_1604_05140_b200.distributed).  Strong scaling."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1604_05140_b200 as sgl
+    from paper_1604_05140_b200 import workload as wl
+    from paper_1604_05140_b200.distributed import CudaStages, Partition, fsglft_distributed, ifsglft_distributed
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    B, nb = args.B, args.batch
+    Om, Ps = sgl.coefficient_count(B), sgl.sample_count(B)
+    plan = sgl.TransformPlan.compute(B, device=local)
+    st = CudaStages(plan)
+    part = Partition.make(B, world)
+    nrot = max(2, min(64, math.ceil(2 * 126e6 / (16 * Om * nb))))
+    rng = np.random.default_rng(0)  # same coefficients on every rank
+    cin = torch.from_numpy(complex_normal(rng, (nrot, nb, Om))).cuda()
+    stream = torch.cuda.current_stream()
+
+    def step(s):
+        loc = ifsglft_distributed(cin[s % nrot], part, st, dist, batch=nb)
+        return fsglft_distributed(loc, part, st, dist, batch=nb)
+
+    for s in range(args.warmup):
+        out = step(s)
+    torch.cuda.synchronize()
+    ref = cin[(args.warmup - 1) % nrot]
+    err = float((out - ref).abs().max() / ref.abs().max())
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for s in range(args.steps):
+            step(s)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = nb / (ms / 1000.0)
+    # e2e: host coefficients in, host shell slice out and back in, host coefficients out
+    sc = part.shells_per_rank
+    hc = torch.empty((nb, Om), dtype=torch.complex128).pin_memory()
+    hc.copy_(cin[0].cpu())
+    hloc = torch.empty((nb, sc * 4 * B * B), dtype=torch.complex128).pin_memory()
+    hout = torch.empty((nb, Om), dtype=torch.complex128).pin_memory()
+    ke = args.e2e_steps
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        loc = ifsglft_distributed(hc.cuda(non_blocking=True), part, st, dist, batch=nb)
+        hloc.copy_(loc.view(nb, -1), non_blocking=True)
+        c2 = fsglft_distributed(hloc.cuda(non_blocking=True), part, st, dist, batch=nb)
+        hout.copy_(c2, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_ms = 1000.0 * (time.perf_counter() - t0) / ke
+    t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    whole = 2 * wl.f_fwd(B) * nb / (ms * 1e-3) / 1e12
+    line = {
+        "metric": f"fwd+inv SGL transforms/s at B={B} fp64", "value": value, "unit": "transforms/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: iid complex normal coefficients (numpy PCG64, seed 0)",
+        "config": {"workload": f"C3: B={B}, {nb} function(s) per step split over {world} GPUs "
+                               "(shells / degree ranges, NCCL all-to-all)",
+                   "B": B, "batch": nb, "parallelism": f"shell/(l,m) split x{world}",
+                   "l2": f"inputs rotated over {nrot} buffers; per-step grid {16 * Ps * nb / 2**20:.0f} MiB > L2"},
+        "e2e": {"value": nb / (e2e_ms / 1000.0), "unit": "transforms/s",
+                "h2d_bytes_per_step": 16 * (Om + sc * 4 * B * B) * nb,
+                "d2h_bytes_per_step": 16 * (sc * 4 * B * B + Om) * nb, "ms_per_step": e2e_ms,
+                "api": "paper_1604_05140_b200.distributed.{ifsglft,fsglft}_distributed"},
+        "gpu_launches": 6 * args.steps,
+        "transform_fp64_tflops": whole,
+        "transform_roofline_frac": whole / FP64_PEAK_TFLOPS,
+        "clocks": clk.summary(),
+        "roundtrip_normwise_err": err,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

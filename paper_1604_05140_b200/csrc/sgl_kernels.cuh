@@ -24,7 +24,7 @@ constexpr int kBK = 16;   // k chunk
 #define SGL_WM_RAD 4
 #endif
 #ifndef SGL_FM_LEG
-#define SGL_FM_LEG 8
+#define SGL_FM_LEG 4
 #endif
 #ifndef SGL_FM_RAD
 #define SGL_FM_RAD 4
