@@ -158,22 +158,46 @@ std::pair<sglk::Tile*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int 
         plo = 0;
         phi = 2 * B;
     }
+    std::vector<long long> work;  // per tile, for heaviest-first ordering
+    const char* wm_env = std::getenv(kind == kLegFwd || kind == kLegInv ? "SGL_WM_LEG" : "SGL_WM_RAD");
+    const int wm_force = wm_env ? std::atoi(wm_env) : 0;
     for (int pid = plo; pid < phi; ++pid) {
         int M, N, K;
         problem_shape(kind, B, batch, NB, pid, M, N, K);
         if (M <= 0 || N <= 0) continue;
         if (K <= 0 && kind != kLegInv) continue;  // LegInv with K = 0 must still write zeros
         const bool leg = kind == kLegFwd || kind == kLegInv;
-        const int wm = leg ? sglk::kWM_LEG : sglk::kWM_RAD;
-        const int bm = sglk::tile_rows(wm, leg ? sglk::kFM_LEG : sglk::kFM_RAD), bn = sglk::tile_cols(wm);
-        // Legendre tiles never straddle the +m / -m halves of N (so column
-        // addresses are affine inside a tile)
+        // Legendre tiles never straddle the +m / -m halves of N (column addresses
+        // stay affine inside a tile)
         const int half = leg ? (int)NB : N;
+        // warp layout: fewest (32 wm) x (128 / wm) tiles covering this problem
+        int wm = 1;
+        long long best = -1;
+        for (int cand : {1, 2, 4}) {
+            const long long nt = (long long)((M + 32 * cand - 1) / (32 * cand)) *
+                                 ((N + 128 / cand - 1) / (128 / cand));
+            if (best < 0 || nt < best) {
+                best = nt;
+                wm = cand;
+            }
+        }
+        if (wm_force == 1 || wm_force == 2 || wm_force == 4) wm = wm_force;
+        const int bm = sglk::tile_rows(wm), bn = sglk::tile_cols(wm);
         for (int m0 = 0; m0 < M; m0 += bm)
             for (int h0 = 0; h0 < N; h0 += half)
-                for (int n0 = h0; n0 < std::min(N, h0 + half); n0 += bn) v.push_back({pid, m0, n0, K});
+                for (int n0 = h0; n0 < std::min(N, h0 + half); n0 += bn) {
+                    v.push_back({pid, m0, n0, wm});
+                    const long long rows = (std::min(bm, M - m0) + 7) / 8 * 8;
+                    const long long cols = (std::min(bn, std::min(N, h0 + half) - n0) + 7) / 8 * 8;
+                    work.push_back(rows * cols * std::max(K, 1));
+                }
     }
-    std::stable_sort(v.begin(), v.end(), [](const sglk::Tile& a, const sglk::Tile& b) { return a.pad > b.pad; });
+    std::vector<size_t> order(v.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return work[a] > work[b]; });
+    std::vector<sglk::Tile> sorted(v.size());
+    for (size_t i = 0; i < order.size(); ++i) sorted[i] = v[order[i]];
+    v.swap(sorted);
     sglk::Tile* d = nullptr;
     if (!v.empty()) d = dev_upload(v);
     const auto res = std::make_pair(d, (int)v.size());

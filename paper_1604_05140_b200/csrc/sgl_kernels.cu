@@ -609,59 +609,50 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem_dst, const void* gme
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem_src), "r"(ok ? 16 : 0));
 }
 
-// Persistent grouped DMMA GEMM.  Each CTA walks its tiles (blockIdx.x,
-// + gridDim.x, ...) as one flat sequence of (tile, k-chunk) steps through a
-// STAGES-deep cp.async pipeline, so global loads stay in flight across tile
-// boundaries and the short-K tiles of the triangular problems pay no prologue.
-// 4 warps of 32 x 32 (4 x 4 m8n8k4 fragments), arranged WM x (4/WM): the CTA
-// tile is (32 WM) x (128 / WM).  WM = 1 for the wide Legendre problems, WM = 4
-// for the radial problems whose N = 2(2l+1) is narrow.  Shared-memory tiles are
-// stored with the operand's contiguous dimension innermost (row- or k-major)
-// so both the cp.async fills and the fragment loads are bank-conflict free.
-template <class P, int WM, int FM>
+// Grouped DMMA GEMM, one tile per CTA (the block scheduler balances the
+// ragged tiles; tiles are issued heaviest first).  4 warps of 32 x 32
+// (4 x 4 m8n8k4 fragments) arranged WM x (4/WM): the CTA tile is (32 WM) x
+// (128 / WM), chosen per tile by the host to fit the problem's M x N
+// (narrow-N radial problems use 128 x 32, wide Legendre ones 32 x 128).
+// k-chunks of 16 flow through a STAGES-deep cp.async pipeline with zero-fill
+// predication; shared-memory tiles keep the operand's contiguous dimension
+// innermost (padded) so fills and fragment loads are bank-conflict free.
+// 8-row fragments past M, 8-col fragments past N and k-steps past K are skipped.
+template <class P, int WM>
 struct GemmCfg {
-    static constexpr int BM = 8 * FM * WM, BN = 128 / WM, BK = kBK, ST = SGL_GEMM_STAGES;
-    static constexpr int A_ELEMS = BM * BK;  // per stage
-    static constexpr int B_ELEMS = BK * BN;
-    // padded smem strides (B is always [k][n]; its (re, im) pairs move as 16 B)
+    static constexpr int FM = 4;
+    static constexpr int BM = 32 * WM, BN = 128 / WM, BK = kBK, ST = SGL_GEMM_STAGES;
     static constexpr int LDA = P::A_KCONTIG ? BK + 4 : BM + 4;
     static constexpr int LDB = BN + 4;
     static constexpr int A_STAGE = P::A_KCONTIG ? BM * LDA : BK * LDA;
     static constexpr int B_STAGE = BK * LDB;
-    static constexpr size_t SMEM = sizeof(double) * ST * (A_STAGE + B_STAGE);
-    static constexpr int AQ = A_ELEMS / 128;  // A elements per thread
-    static constexpr int BQ = B_ELEMS / 256;  // B (re, im) pairs per thread
+    static constexpr int STAGE = A_STAGE + B_STAGE;
+    static constexpr int AQ = BM * BK / 128;  // A elements per thread
+    static constexpr int BQ = BK * BN / 256;  // B (re, im) pairs per thread
 };
 
-template <class P, int WM, int FM>
-__global__ void __launch_bounds__(128, FM > 4 ? SGL_GEMM_MINB_WIDE : SGL_GEMM_MINB)
-gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles, int ntiles) {
-    using C = GemmCfg<P, WM, FM>;
-    constexpr int BM = C::BM, BN = C::BN, BK = C::BK, ST = C::ST;
-    extern __shared__ __align__(16) double gsm[];
-    double* As = gsm;
-    double* Bs = gsm + ST * C::A_STAGE;
+template <class P>
+constexpr size_t gemm_smem_bytes() {
+    constexpr int s1 = GemmCfg<P, 1>::STAGE, s2 = GemmCfg<P, 2>::STAGE, s4 = GemmCfg<P, 4>::STAGE;
+    constexpr int m = s1 > s2 ? (s1 > s4 ? s1 : s4) : (s2 > s4 ? s2 : s4);
+    return sizeof(double) * SGL_GEMM_STAGES * m;
+}
 
+template <class P, int WM>
+__device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* smem) {
+    using C = GemmCfg<P, WM>;
+    constexpr int BM = C::BM, BN = C::BN, BK = C::BK, ST = C::ST, FM = C::FM;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wr = (warp % WM) * 8 * FM, wc = (warp / WM) * 32;
-    const int nmine = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int wr = (warp % WM) * 32, wc = (warp / WM) * 32;
+    const int pid = t.prob, m0 = t.m0, n0 = t.n0;
+    const int M = pr.M(pid), N = pr.nlim(pid, n0), K = pr.K(pid);
+    const int nch = K > 0 ? (K + BK - 1) / BK : 1;
 
-    // fixed per-thread load coordinates (tile-relative) and smem offsets
-    int a_row[C::AQ], a_k[C::AQ], a_so[C::AQ];
-#pragma unroll
-    for (int q = 0; q < C::AQ; ++q) {
-        if (P::A_KCONTIG) {
-            a_row[q] = (tid >> 2) + 32 * (q >> 2);
-            a_k[q] = (tid & 3) * 4 + (q & 3);
-            a_so[q] = a_row[q] * C::LDA + a_k[q];
-        } else {
-            const int e = tid + 128 * q;
-            a_row[q] = e % BM;
-            a_k[q] = e / BM;
-            a_so[q] = a_k[q] * C::LDA + a_row[q];
-        }
-    }
-    int b_k[C::BQ], b_c[C::BQ], b_so[C::BQ];
+    // ---- loads of one k-chunk into stage buffer `buf`
+    const long long abase = pr.rowA(pid, m0);
+    const int a_sr = pr.a_sr(pid), a_sk = pr.a_sk(pid);
+    long long bcol[P::B_COL_AFFINE ? 1 : C::BQ];
+    int b_k[C::BQ], b_c[C::BQ];
 #pragma unroll
     for (int q = 0; q < C::BQ; ++q) {
         const int e = tid + 128 * q;
@@ -669,100 +660,69 @@ gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles, int ntiles) {
             const int hi = e >> 3;
             b_k[q] = (e & 7) + 8 * (hi / (BN / 2));
             b_c[q] = (hi % (BN / 2)) * 2;
-        } else {  // consecutive column pairs along a k row
+        } else {
             b_c[q] = (e % (BN / 2)) * 2;
             b_k[q] = e / (BN / 2);
         }
-        b_so[q] = b_k[q] * C::LDB + b_c[q];
+        if constexpr (!P::B_COL_AFFINE) bcol[q] = n0 + b_c[q] < N ? pr.colB(pid, n0 + b_c[q]) : 0;
     }
+    if constexpr (P::B_COL_AFFINE) bcol[0] = pr.colB(pid, n0);
 
-    // ---- issue side: walks (tile, chunk) ahead of the compute side.  A rows
-    // are affine (base + row * sr + k * sk); B columns are affine within a
-    // tile for the Legendre problems (tiles never straddle the sign halves),
-    // else kept per load.
-    constexpr int BQC = P::B_COL_AFFINE ? 1 : C::BQ;
-    int is_it = 0, is_c = 0, is_pid = 0, is_K = 0, is_nch = 1, is_M = 0, is_N = 0, is_m0 = 0, is_n0 = 0;
-    int is_sr = 0, is_sk = 0;
-    long long is_abase = 0;
-    long long is_bcol[BQC];
-    auto is_load_tile = [&](int it) {
-        const Tile t = tiles[blockIdx.x + it * gridDim.x];
-        is_pid = t.prob;
-        is_m0 = t.m0;
-        is_n0 = t.n0;
-        is_M = pr.M(is_pid);
-        is_N = pr.nlim(is_pid, t.n0);
-        is_K = pr.K(is_pid);
-        is_nch = is_K > 0 ? (is_K + BK - 1) / BK : 1;
-        is_abase = pr.rowA(is_pid, t.m0);
-        is_sr = pr.a_sr(is_pid);
-        is_sk = pr.a_sk(is_pid);
-        if constexpr (P::B_COL_AFFINE) {
-            is_bcol[0] = pr.colB(is_pid, t.n0);
-        } else {
+    auto issue = [&](int c) {
+        double* as = smem + (c % ST) * C::STAGE;
+        double* bs = as + C::A_STAGE;
+        const int k0 = c * BK;
 #pragma unroll
-            for (int q = 0; q < C::BQ; ++q) {
-                const int col = t.n0 + b_c[q];
-                is_bcol[q] = col < is_N ? pr.colB(is_pid, col) : 0;
+        for (int q = 0; q < C::AQ; ++q) {
+            int row, k, so;
+            if (P::A_KCONTIG) {
+                row = (tid >> 2) + 32 * (q >> 2);
+                k = (tid & 3) * 4 + (q & 3);
+                so = row * C::LDA + k;
+            } else {
+                const int e = tid + 128 * q;
+                row = e % BM;
+                k = e / BM;
+                so = k * C::LDA + row;
             }
+            const bool ok = m0 + row < M && k0 + k < K;
+            const double* src = pr.A + abase + (long long)row * a_sr + (long long)(k0 + k) * a_sk;
+            cp_async8_zfill(as + so, ok ? src : pr.A, ok);
         }
-    };
-    int step_issue = 0;
-    auto issue_next = [&]() {
-        if (is_it < nmine) {
-            const int buf = step_issue % ST;
-            const int k0 = is_c * BK;
-            double* as = As + buf * C::A_STAGE;
-            double* bs = Bs + buf * C::B_STAGE;
 #pragma unroll
-            for (int q = 0; q < C::AQ; ++q) {
-                const int k = k0 + a_k[q];
-                const bool ok = is_m0 + a_row[q] < is_M && k < is_K;
-                const double* src = pr.A + is_abase + (long long)a_row[q] * is_sr + (long long)k * is_sk;
-                cp_async8_zfill(as + a_so[q], ok ? src : pr.A, ok);
-            }
-#pragma unroll
-            for (int q = 0; q < C::BQ; ++q) {
-                const int k = k0 + b_k[q];
-                const bool ok = is_n0 + b_c[q] < is_N && k < is_K;
-                const long long col = P::B_COL_AFFINE ? is_bcol[0] + b_c[q] : is_bcol[P::B_COL_AFFINE ? 0 : q];
-                cp_async16_zfill(bs + b_so[q], ok ? pr.Bm + pr.rowB(is_pid, k) + col : pr.Bm, ok);
-            }
-            if (++is_c == is_nch) {
-                is_c = 0;
-                if (++is_it < nmine) is_load_tile(is_it);
-            }
+        for (int q = 0; q < C::BQ; ++q) {
+            const int k = k0 + b_k[q];
+            const bool ok = n0 + b_c[q] < N && k < K;
+            const long long col = P::B_COL_AFFINE ? bcol[0] + b_c[q] : bcol[P::B_COL_AFFINE ? 0 : q];
+            cp_async16_zfill(bs + b_k[q] * C::LDB + b_c[q], ok ? pr.Bm + pr.rowB(pid, k) + col : pr.Bm, ok);
         }
         cp_async_commit();
-        ++step_issue;
     };
 
-    if (nmine > 0) is_load_tile(0);
+    const int fm_active = max(0, min(FM, (M - m0 - wr + 7) >> 3));
+    const int fn_active = max(0, min(4, (N - n0 - wc + 7) >> 3));
+    double acc[FM][4][2];
 #pragma unroll
-    for (int s = 0; s < ST - 1; ++s) issue_next();
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    int step = 0;
-    for (int it = 0; it < nmine; ++it) {
-        const Tile t = tiles[blockIdx.x + it * gridDim.x];
-        const int pid = t.prob, m0 = t.m0, n0 = t.n0;
-        const int M = pr.M(pid), N = pr.nlim(pid, n0), K = pr.K(pid);
-        const int nch = K > 0 ? (K + BK - 1) / BK : 1;
-        const int fm_active = max(0, min(FM, (M - m0 - wr + 7) >> 3));
-        const int fn_active = max(0, min(4, (N - n0 - wc + 7) >> 3));
-        double acc[FM][4][2];
 #pragma unroll
-        for (int i = 0; i < FM; ++i)
+    for (int c = 0; c < ST - 1; ++c) {
+        if (c < nch) issue(c);
+        else cp_async_commit();
+    }
+    for (int c = 0; c < nch; ++c) {
+        cp_async_wait_group<ST - 2>();
+        __syncthreads();
+        if (c + ST - 1 < nch) issue(c + ST - 1);
+        else cp_async_commit();
+        const double* as = smem + (c % ST) * C::STAGE;
+        const double* bs = as + C::A_STAGE;
+        const int ksteps = min(BK, K - c * BK);  // k-steps past K carry zeros: skip them
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-        for (int c = 0; c < nch; ++c, ++step) {
-            cp_async_wait_group<ST - 2>();
-            __syncthreads();
-            issue_next();
-            const int buf = step % ST;
-            const double* as = As + buf * C::A_STAGE;
-            const double* bs = Bs + buf * C::B_STAGE;
-#pragma unroll
-            for (int kk = 0; kk < BK; kk += 4) {
+        for (int kk = 0; kk < BK; kk += 4) {
+            if (kk < ksteps) {
                 double af[FM], bf[4];
 #pragma unroll
                 for (int fm = 0; fm < FM; ++fm) {
@@ -770,10 +730,7 @@ gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles, int ntiles) {
                     af[fm] = P::A_KCONTIG ? as[r * C::LDA + k] : as[k * C::LDA + r];
                 }
 #pragma unroll
-                for (int fn = 0; fn < 4; ++fn) {
-                    const int n = wc + fn * 8 + (lane >> 2), k = kk + (lane & 3);
-                    bf[fn] = bs[k * C::LDB + n];
-                }
+                for (int fn = 0; fn < 4; ++fn) bf[fn] = bs[(kk + (lane & 3)) * C::LDB + wc + fn * 8 + (lane >> 2)];
 #pragma unroll
                 for (int fm = 0; fm < FM; ++fm) {
                     if (fm < fm_active) {
@@ -784,23 +741,34 @@ gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles, int ntiles) {
                 }
             }
         }
-        // ---- epilogue (registers -> global)
-#pragma unroll
-        for (int fm = 0; fm < FM; ++fm) {
-            const int row = m0 + wr + fm * 8 + (lane >> 2);
-            if (row >= M) continue;
-            const long long ro = pr.rowC(pid, row);
-#pragma unroll
-            for (int fn = 0; fn < 4; ++fn) {
-                const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
-                if (col >= N) continue;
-                const double sc = pr.scaleC(pid, col);
-                *reinterpret_cast<double2*>(pr.C + ro + pr.colC(pid, col)) =
-                    make_double2(sc * acc[fm][fn][0], sc * acc[fm][fn][1]);
-            }
-        }
     }
     cp_async_wait_group<0>();
+    // ---- epilogue (registers -> global)
+#pragma unroll
+    for (int fm = 0; fm < FM; ++fm) {
+        const int row = m0 + wr + fm * 8 + (lane >> 2);
+        if (row >= M) continue;
+        const long long ro = pr.rowC(pid, row);
+#pragma unroll
+        for (int fn = 0; fn < 4; ++fn) {
+            const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
+            if (col >= N) continue;
+            const double sc = pr.scaleC(pid, col);
+            *reinterpret_cast<double2*>(pr.C + ro + pr.colC(pid, col)) =
+                make_double2(sc * acc[fm][fn][0], sc * acc[fm][fn][1]);
+        }
+    }
+}
+
+template <class P>
+__global__ void __launch_bounds__(128, SGL_GEMM_MINB) gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles) {
+    extern __shared__ __align__(16) double gsm[];
+    const Tile t = tiles[blockIdx.x];
+    switch (t.pad) {  // warp layout chosen per tile
+        case 1: gemm_tile<P, 1>(pr, t, gsm); break;
+        case 2: gemm_tile<P, 2>(pr, t, gsm); break;
+        default: gemm_tile<P, 4>(pr, t, gsm); break;
+    }
 }
 
 // ------------------------------------------------------------------ launchers
@@ -885,52 +853,43 @@ int launch_az_inverse(const Geo& g, const double* G, double* samples, size_t sam
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-template <class P, int WM, int FM>
+template <class P>
 static int gemm_launch(const P& p, const Tile* tiles, int ntiles, cudaStream_t s) {
     if (ntiles <= 0) return 0;
-    constexpr size_t smem = GemmCfg<P, WM, FM>::SMEM;
-    static int resident = 0;
-    if (!resident) {
-        cudaFuncSetAttribute(gemm_dmma_kernel<P, WM, FM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int dev = 0, sms = 0, per = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gemm_dmma_kernel<P, WM, FM>, 128, smem);
-        resident = std::max(1, sms * std::max(1, per));
+    constexpr size_t smem = gemm_smem_bytes<P>();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(gemm_dmma_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
     }
-#if SGL_GEMM_PERSISTENT
-    const int grid = std::min(resident, ntiles);
-#else
-    const int grid = ntiles;  // one tile per CTA; the block scheduler balances the ragged tiles
-#endif
-    gemm_dmma_kernel<P, WM, FM><<<grid, 128, smem, s>>>(p, tiles, ntiles);
+    gemm_dmma_kernel<P><<<ntiles, 128, smem, s>>>(p, tiles);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 int launch_legendre_forward(const Geo& g, const SView& sv, const double* G, double* S, const double* tab,
                             const long long* tab_off, const Tile* tiles, int ntiles, cudaStream_t s) {
     LegFwd p{g, tab, tab_off, G, S, sv};
-    return gemm_launch<LegFwd, kWM_LEG, kFM_LEG>(p, tiles, ntiles, s);
+    return gemm_launch<LegFwd>(p, tiles, ntiles, s);
 }
 
 int launch_legendre_inverse(const Geo& g, const SView& sv, const double* S, double* G, const double* tab,
                             const long long* tab_off, const Tile* tiles, int ntiles, cudaStream_t s) {
     LegInv p{g, tab, tab_off, S, G, sv};
-    return gemm_launch<LegInv, kWM_LEG, kFM_LEG>(p, tiles, ntiles, s);
+    return gemm_launch<LegInv>(p, tiles, ntiles, s);
 }
 
 int launch_radial_forward(const Geo& g, const RadialBlocks& rb, const double* S, double* C,
                           const double* W, const long long* w_off, const Tile* tiles, int ntiles,
                           cudaStream_t s) {
     RadFwd p{g, W, w_off, S, C, degree_offset(g.B + 1), ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
-    return gemm_launch<RadFwd, kWM_RAD, kFM_RAD>(p, tiles, ntiles, s);
+    return gemm_launch<RadFwd>(p, tiles, ntiles, s);
 }
 
 int launch_radial_inverse(const Geo& g, const RadialBlocks& rb, const double* C, double* S,
                           const double* V, const long long* v_off, const Tile* tiles, int ntiles,
                           cudaStream_t s) {
     RadInv p{g, V, v_off, C, S, degree_offset(g.B + 1), ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
-    return gemm_launch<RadInv, kWM_RAD, kFM_RAD>(p, tiles, ntiles, s);
+    return gemm_launch<RadInv>(p, tiles, ntiles, s);
 }
 
 }  // namespace sglk

@@ -10,30 +10,15 @@
 
 namespace sglk {
 
-// Tile descriptor for the grouped DMMA contraction: {problem, m0, n0, unused}.
+// Tile descriptor for the grouped DMMA contraction: {problem, m0, n0, warp layout wm}.
 struct Tile {
     int prob, m0, n0, pad;
 };
 
 constexpr int kBK = 16;   // k chunk
-// Warp arrangement of the 4-warp GEMM CTA: tile = (32 WM) rows x (128 / WM) cols.
-#ifndef SGL_WM_LEG
-#define SGL_WM_LEG 1
-#endif
-#ifndef SGL_WM_RAD
-#define SGL_WM_RAD 4
-#endif
-#ifndef SGL_FM_LEG
-#define SGL_FM_LEG 4
-#endif
-#ifndef SGL_FM_RAD
-#define SGL_FM_RAD 4
-#endif
-constexpr int kWM_LEG = SGL_WM_LEG;
-constexpr int kWM_RAD = SGL_WM_RAD;
-constexpr int kFM_LEG = SGL_FM_LEG;  // 8-row DMMA fragments per warp along M
-constexpr int kFM_RAD = SGL_FM_RAD;
-constexpr int tile_rows(int wm, int fm) { return 8 * fm * wm; }
+// The 4-warp GEMM CTA computes a (32 wm) x (128 / wm) tile, wm in {1, 2, 4}
+// chosen per tile (Tile::pad) by the host.
+constexpr int tile_rows(int wm) { return 32 * wm; }
 constexpr int tile_cols(int wm) { return 128 / wm; }
 
 // Geometry shared by the stages.  "shell" is a flat index s = f * SC + i over
