@@ -638,6 +638,44 @@ constexpr size_t gemm_smem_bytes() {
     return sizeof(double) * SGL_GEMM_STAGES * m;
 }
 
+// One k-chunk of MMAs for a warp with FA x NA active 8 x 8 fragments.
+template <class P, int WM, int FA, int NA, bool FULL>
+__device__ __forceinline__ void mma_chunk(const double* as, const double* bs, double (&acc)[4][4][2], int ksteps,
+                                          int wr, int wc, int lane) {
+    using C = GemmCfg<P, WM>;
+#pragma unroll
+    for (int kk = 0; kk < C::BK; kk += 4) {
+        if (!FULL && kk >= ksteps) break;
+        double af[FA > 0 ? FA : 1], bf[NA > 0 ? NA : 1];
+#pragma unroll
+        for (int fm = 0; fm < FA; ++fm) {
+            const int r = wr + fm * 8 + (lane >> 2), k = kk + (lane & 3);
+            af[fm] = P::A_KCONTIG ? as[r * C::LDA + k] : as[k * C::LDA + r];
+        }
+#pragma unroll
+        for (int fn = 0; fn < NA; ++fn) bf[fn] = bs[(kk + (lane & 3)) * C::LDB + wc + fn * 8 + (lane >> 2)];
+#pragma unroll
+        for (int fm = 0; fm < FA; ++fm)
+#pragma unroll
+            for (int fn = 0; fn < NA; ++fn) dmma884(acc[fm][fn], af[fm], bf[fn]);
+    }
+}
+
+template <class P, int WM, bool FULL>
+__device__ __forceinline__ void dispatch_chunk(int fa, int na, const double* as, const double* bs,
+                                               double (&acc)[4][4][2], int ksteps, int wr, int wc, int lane) {
+#define SGL_MMA_CASE(A_, N_) \
+    case A_ * 8 + N_: mma_chunk<P, WM, A_, N_, FULL>(as, bs, acc, ksteps, wr, wc, lane); break;
+    switch (fa * 8 + na) {
+        SGL_MMA_CASE(4, 4) SGL_MMA_CASE(4, 3) SGL_MMA_CASE(4, 2) SGL_MMA_CASE(4, 1)
+        SGL_MMA_CASE(3, 4) SGL_MMA_CASE(3, 3) SGL_MMA_CASE(3, 2) SGL_MMA_CASE(3, 1)
+        SGL_MMA_CASE(2, 4) SGL_MMA_CASE(2, 3) SGL_MMA_CASE(2, 2) SGL_MMA_CASE(2, 1)
+        SGL_MMA_CASE(1, 4) SGL_MMA_CASE(1, 3) SGL_MMA_CASE(1, 2) SGL_MMA_CASE(1, 1)
+        default: break;  // a warp with no active fragment only helps with the loads
+    }
+#undef SGL_MMA_CASE
+}
+
 template <class P, int WM>
 __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* smem) {
     using C = GemmCfg<P, WM>;
@@ -676,8 +714,9 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
         for (int q = 0; q < C::AQ; ++q) {
             int row, k, so;
             if (P::A_KCONTIG) {
-                row = (tid >> 2) + 32 * (q >> 2);
-                k = (tid & 3) * 4 + (q & 3);
+                constexpr int KPT = BK / 4;  // 4 threads per row, KPT consecutive k each
+                row = (tid >> 2) + 32 * (q / KPT);
+                k = (tid & 3) * KPT + (q % KPT);
                 so = row * C::LDA + k;
             } else {
                 const int e = tid + 128 * q;
@@ -720,26 +759,12 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
         const double* as = smem + (c % ST) * C::STAGE;
         const double* bs = as + C::A_STAGE;
         const int ksteps = min(BK, K - c * BK);  // k-steps past K carry zeros: skip them
-#pragma unroll
-        for (int kk = 0; kk < BK; kk += 4) {
-            if (kk < ksteps) {
-                double af[FM], bf[4];
-#pragma unroll
-                for (int fm = 0; fm < FM; ++fm) {
-                    const int r = wr + fm * 8 + (lane >> 2), k = kk + (lane & 3);
-                    af[fm] = P::A_KCONTIG ? as[r * C::LDA + k] : as[k * C::LDA + r];
-                }
-#pragma unroll
-                for (int fn = 0; fn < 4; ++fn) bf[fn] = bs[(kk + (lane & 3)) * C::LDB + wc + fn * 8 + (lane >> 2)];
-#pragma unroll
-                for (int fm = 0; fm < FM; ++fm) {
-                    if (fm < fm_active) {
-#pragma unroll
-                        for (int fn = 0; fn < 4; ++fn)
-                            if (fn < fn_active) dmma884(acc[fm][fn], af[fm], bf[fn]);
-                    }
-                }
-            }
+        // warp-uniform dispatch to straight-line MMA code: no per-MMA guards
+        // (a guarded mma.sync costs ISETP + WARPSYNC + NOP per DMMA)
+        if (ksteps == BK) {
+            dispatch_chunk<P, WM, true>(fm_active, fn_active, as, bs, acc, BK, wr, wc, lane);
+        } else {
+            dispatch_chunk<P, WM, false>(fm_active, fn_active, as, bs, acc, ksteps, wr, wc, lane);
         }
     }
     cp_async_wait_group<0>();
