@@ -348,6 +348,18 @@ def main():
                 "peak_source": "measured fp64 DMMA (mma.sync m8n8k4) peak, profiles/fp64_peak_r01.txt; "
                                "MEASURED_PEAKS.json has no fp64 entry"}
     roof["launch_ms"] = per_launch_ms
+    # DRAM traffic of this kernel from the committed ncu --set full capture (B = 128)
+    try:
+        with open(os.path.join(REPO, "profiles", "r01_traffic.json")) as f:
+            tr = json.load(f)["bytes"]
+        kname = {0: f"void az_forward_kernel<{2 * B}>", 1: "void gemm_dmma_kernel<LegFwd>",
+                 2: "void gemm_dmma_kernel<RadFwd>", 3: "void gemm_dmma_kernel<RadInv>",
+                 4: "void gemm_dmma_kernel<LegInv>", 5: f"void az_inverse_kernel<{2 * B}>"}[dom]
+        if B == 128 and nb == 1 and kname in tr:
+            roof["traffic"] = tr[kname]
+            roof["traffic_source"] = "profiles/r01_ncu_full.txt (dram__bytes_read.sum + dram__bytes_write.sum)"
+    except (OSError, KeyError, ValueError):
+        pass
     roof["timing"] = ("live: CUDA events around each stage launch inside the timed region" if live_profile else
                       "separate profiled pass (eager launches) after the CUDA-graph timed region")
     whole = 2 * wl.f_fwd(B) * nb / (ms * 1e-3) / 1e12
