@@ -458,6 +458,7 @@ struct LegFwd {
     __device__ long long rowB(int pid, int k) const {
         return ((((long long)(pid & 1) * g.B + am(pid)) * g.B + k) * 2) * g.NB;
     }
+    __device__ long long b_kstep(int) const { return 2 * g.NB; }
     __device__ long long colB(int, int n) const { return n; }
     __device__ long long rowC(int pid, int r) const {
         const long long l = am(pid) + (pid & 1) + 2 * r;
@@ -465,6 +466,9 @@ struct LegFwd {
     }
     __device__ long long colC(int pid, int n) const { return s_col(g, sv, am(pid), n); }
     __device__ double scaleC(int pid, int n) const { return (n >= g.NB && (am(pid) & 1)) ? -1.0 : 1.0; }
+    // tiles start at multiples of bn inside a sign half; no function boundary inside
+    // the tile when bn divides the per-function width 2 SC
+    __device__ bool c_affine(int, int, int bn) const { return (2 * g.SC) % bn == 0; }
 };
 
 // Legendre inverse: prob = 2|m| + p.  rows j' (M = B), K = #l of parity p, cols n'.
@@ -491,12 +495,14 @@ struct LegInv {
         const long long l = am(pid) + (pid & 1) + 2 * k;
         return l * (l + 1) * sv.NB;
     }
+    __device__ long long b_kstep(int) const { return 0; }
     __device__ long long colB(int pid, int n) const { return s_col(g, sv, am(pid), n); }
     __device__ long long rowC(int pid, int j) const {
         return ((((long long)(pid & 1) * g.B + am(pid)) * g.B + j) * 2) * g.NB;
     }
     __device__ long long colC(int, int n) const { return n; }
     __device__ double scaleC(int pid, int n) const { return (n >= g.NB && (am(pid) & 1)) ? -1.0 : 1.0; }
+    __device__ bool c_affine(int, int, int) const { return true; }
 };
 
 __host__ __device__ inline long long degree_offset(long long n) { return (n - 1) * n * (2 * n - 1) / 6; }
@@ -538,6 +544,7 @@ struct RadFwd {
     __device__ int a_sr(int) const { return 2 * g.B; }
     __device__ int a_sk(int) const { return 1; }
     __device__ long long rowB(int, int k) const { return sb.row(k); }
+    __device__ long long b_kstep(int) const { return sb.sc_blk == 2 * g.B ? 2 : 0; }
     __device__ long long colB(int l, int n) const {
         const int mf = n >> 1, w = 2 * l + 1;
         const int f = mf / w, mm = mf - f * w;  // mm = m + l
@@ -550,6 +557,7 @@ struct RadFwd {
         return (long long)f * 2 * omega + 2LL * ((long long)l * l + mm) + (n & 1);
     }
     __device__ double scaleC(int, int) const { return 1.0; }
+    __device__ bool c_affine(int, int, int) const { return false; }
 };
 
 // Radial inverse: prob = l.  rows i (M = 2B), K = B-l (n), cols (mf, c).
@@ -573,6 +581,7 @@ struct RadInv {
     __device__ int a_sr(int l) const { return g.B - l; }
     __device__ int a_sk(int) const { return 1; }
     __device__ long long rowB(int l, int k) const { return 2 * degree_offset(l + 1 + k); }
+    __device__ long long b_kstep(int) const { return 0; }
     __device__ long long colB(int l, int n) const {
         const int mf = n >> 1, w = 2 * l + 1;
         const int f = mf / w, mm = mf - f * w;
@@ -585,6 +594,7 @@ struct RadInv {
         return ((long long)l * l + mm - sb.nu0) * g.NB + (long long)f * 2 * g.SC + (n & 1);
     }
     __device__ double scaleC(int, int) const { return 1.0; }
+    __device__ bool c_affine(int, int, int) const { return false; }
 };
 
 #ifndef SGL_GEMM_STAGES
@@ -686,54 +696,79 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
     const int M = pr.M(pid), N = pr.nlim(pid, n0), K = pr.K(pid);
     const int nch = K > 0 ? (K + BK - 1) / BK : 1;
 
-    // ---- loads of one k-chunk into stage buffer `buf`
-    const long long abase = pr.rowA(pid, m0);
-    const int a_sr = pr.a_sr(pid), a_sk = pr.a_sk(pid);
-    long long bcol[P::B_COL_AFFINE ? 1 : C::BQ];
-    int b_k[C::BQ], b_c[C::BQ];
+    // ---- per-tile load plan: every address this thread will fetch is
+    // base + k0 * step, so a chunk issue is a handful of 64-bit adds
+    const int a_sk = pr.a_sk(pid);
+    const double* a_ptr[C::AQ];
+    int a_so[C::AQ], a_k[C::AQ];
+    unsigned a_ok = 0;
+    {
+        const long long abase = pr.rowA(pid, m0);
+        const int a_sr = pr.a_sr(pid);
 #pragma unroll
-    for (int q = 0; q < C::BQ; ++q) {
-        const int e = tid + 128 * q;
-        if (P::B_KCONTIG) {  // 8 consecutive k per column pair: 128 B global runs
-            const int hi = e >> 3;
-            b_k[q] = (e & 7) + 8 * (hi / (BN / 2));
-            b_c[q] = (hi % (BN / 2)) * 2;
-        } else {
-            b_c[q] = (e % (BN / 2)) * 2;
-            b_k[q] = e / (BN / 2);
+        for (int q = 0; q < C::AQ; ++q) {
+            int row, k;
+            if (P::A_KCONTIG) {
+                constexpr int KPT = BK / 4;  // 4 threads per row, KPT consecutive k each
+                row = (tid >> 2) + 32 * (q / KPT);
+                k = (tid & 3) * KPT + (q % KPT);
+                a_so[q] = row * C::LDA + k;
+            } else {
+                const int e = tid + 128 * q;
+                row = e % BM;
+                k = e / BM;
+                a_so[q] = k * C::LDA + row;
+            }
+            a_k[q] = k;
+            const bool ok = m0 + row < M;
+            a_ok |= (ok ? 1u : 0u) << q;
+            a_ptr[q] = ok ? pr.A + abase + (long long)row * a_sr + (long long)k * a_sk : pr.A;
         }
-        if constexpr (!P::B_COL_AFFINE) bcol[q] = n0 + b_c[q] < N ? pr.colB(pid, n0 + b_c[q]) : 0;
     }
-    if constexpr (P::B_COL_AFFINE) bcol[0] = pr.colB(pid, n0);
+    const long long b_step = pr.b_kstep(pid);  // > 0: rowB is affine in k with this stride
+    const double* b_ptr[C::BQ];
+    int b_k[C::BQ], b_so[C::BQ];
+    unsigned b_ok = 0;
+    {
+        const long long bcol0 = P::B_COL_AFFINE ? pr.colB(pid, n0) : 0;
+#pragma unroll
+        for (int q = 0; q < C::BQ; ++q) {
+            const int e = tid + 128 * q;
+            int bc;
+            if (P::B_KCONTIG) {  // 8 consecutive k per column pair: 128 B global runs
+                const int hi = e >> 3;
+                b_k[q] = (e & 7) + 8 * (hi / (BN / 2));
+                bc = (hi % (BN / 2)) * 2;
+            } else {
+                bc = (e % (BN / 2)) * 2;
+                b_k[q] = e / (BN / 2);
+            }
+            b_so[q] = b_k[q] * C::LDB + bc;
+            const bool ok = n0 + bc < N;
+            b_ok |= (ok ? 1u : 0u) << q;
+            const long long col = !ok ? 0 : (P::B_COL_AFFINE ? bcol0 + bc : pr.colB(pid, n0 + bc));
+            // with an affine row map the k = b_k[q] row offset is folded in here
+            b_ptr[q] = pr.Bm + col + (b_step > 0 ? pr.rowB(pid, 0) + (long long)b_k[q] * b_step : 0);
+        }
+    }
 
     auto issue = [&](int c) {
         double* as = smem + (c % ST) * C::STAGE;
         double* bs = as + C::A_STAGE;
         const int k0 = c * BK;
+        const long long a_adv = (long long)k0 * a_sk;
 #pragma unroll
         for (int q = 0; q < C::AQ; ++q) {
-            int row, k, so;
-            if (P::A_KCONTIG) {
-                constexpr int KPT = BK / 4;  // 4 threads per row, KPT consecutive k each
-                row = (tid >> 2) + 32 * (q / KPT);
-                k = (tid & 3) * KPT + (q % KPT);
-                so = row * C::LDA + k;
-            } else {
-                const int e = tid + 128 * q;
-                row = e % BM;
-                k = e / BM;
-                so = k * C::LDA + row;
-            }
-            const bool ok = m0 + row < M && k0 + k < K;
-            const double* src = pr.A + abase + (long long)row * a_sr + (long long)(k0 + k) * a_sk;
-            cp_async8_zfill(as + so, ok ? src : pr.A, ok);
+            const bool ok = ((a_ok >> q) & 1u) && k0 + a_k[q] < K;
+            cp_async8_zfill(as + a_so[q], ok ? a_ptr[q] + a_adv : pr.A, ok);
         }
+        const long long b_adv = (long long)k0 * b_step;
 #pragma unroll
         for (int q = 0; q < C::BQ; ++q) {
             const int k = k0 + b_k[q];
-            const bool ok = n0 + b_c[q] < N && k < K;
-            const long long col = P::B_COL_AFFINE ? bcol[0] + b_c[q] : bcol[P::B_COL_AFFINE ? 0 : q];
-            cp_async16_zfill(bs + b_k[q] * C::LDB + b_c[q], ok ? pr.Bm + pr.rowB(pid, k) + col : pr.Bm, ok);
+            const bool ok = ((b_ok >> q) & 1u) && k < K;
+            const double* src = b_step > 0 ? b_ptr[q] + b_adv : b_ptr[q] + pr.rowB(pid, k);
+            cp_async16_zfill(bs + b_so[q], ok ? src : pr.Bm, ok);
         }
         cp_async_commit();
     };
@@ -768,19 +803,30 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
         }
     }
     cp_async_wait_group<0>();
-    // ---- epilogue (registers -> global)
+    // ---- epilogue (registers -> global).  The column part of the output address
+    // and the sign are per column only: computed once per fragment column (and,
+    // where the problem's columns are affine inside this tile, from one base).
+    long long cofs[4];
+    double csc[4];
+    const bool caff = pr.c_affine(pid, n0, BN);
+    const long long cbase = caff ? pr.colC(pid, n0) : 0;
+#pragma unroll
+    for (int fn = 0; fn < 4; ++fn) {
+        const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
+        const bool ok = col < N;
+        cofs[fn] = ok ? (caff ? cbase + (col - n0) : pr.colC(pid, col)) : 0;
+        csc[fn] = ok ? pr.scaleC(pid, col) : 0.0;
+    }
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm) {
         const int row = m0 + wr + fm * 8 + (lane >> 2);
         if (row >= M) continue;
-        const long long ro = pr.rowC(pid, row);
+        double* out = pr.C + pr.rowC(pid, row);
 #pragma unroll
         for (int fn = 0; fn < 4; ++fn) {
             const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
             if (col >= N) continue;
-            const double sc = pr.scaleC(pid, col);
-            *reinterpret_cast<double2*>(pr.C + ro + pr.colC(pid, col)) =
-                make_double2(sc * acc[fm][fn][0], sc * acc[fm][fn][1]);
+            *reinterpret_cast<double2*>(out + cofs[fn]) = make_double2(csc[fn] * acc[fm][fn][0], csc[fn] * acc[fm][fn][1]);
         }
     }
 }
