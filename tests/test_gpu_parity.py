@@ -313,3 +313,20 @@ def test_graph_replay_matches_eager():
     s.synchronize()
     for o in outs[1:]:
         assert torch.equal(o, outs[0])
+
+
+def test_cli_roundtrip_and_transform(tmp_path):
+    """The CLI front end (reference formats) on the GPU: roundtrip CSV row and a
+    fwd/inv file transform that reproduces the reference's golden grid."""
+    from paper_1604_05140_b200 import cli
+
+    csv = tmp_path / "bench.csv"
+    assert cli.main(["bench", "--bandlimits", "4,16", "--repetitions", "3", "--csv", str(csv)]) == 0
+    rows = cli.read_csv(str(csv))
+    assert [r["B"] for r in rows] == [4, 16]
+    assert all(r["mean_max_abs_err"] < 1e-10 and r["mean_max_rel_err"] < 1e-6 for r in rows)
+    src = os.path.join(GOLDEN, "rt_B8_coeffs.bin")
+    out = tmp_path / "grid.bin"
+    assert cli.main(["transform", "--direction", "inv", "--bandlimit", "8", "--in", src, "--out", str(out)]) == 0
+    g = np.fromfile(out, dtype="<f8").view(np.complex128)
+    assert per_shell(g, _gold("rt_B8_grid.bin"), 8) <= 1e-13
