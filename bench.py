@@ -53,6 +53,26 @@ def complex_normal(rng, shape):
     return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) / np.sqrt(2.0)
 
 
+def real_valued_coeffs(rng, B, shape):
+    """BASELINE config C5: m > 0 complex normal x exp(-n/8), m = 0 real normal x
+    exp(-n/8), f_{n,l,-m} = (-1)^m conj(f_nlm)."""
+    n_of, l_of, m_of = [], [], []
+    for n in range(1, B + 1):
+        for l in range(n):
+            for m in range(-l, l + 1):
+                n_of.append(n)
+                l_of.append(l)
+                m_of.append(m)
+    n_of, l_of, m_of = (np.array(a) for a in (n_of, l_of, m_of))
+    c = complex_normal(rng, shape + (len(n_of),)) * np.exp(-n_of / 8.0)
+    zero = m_of == 0
+    c[..., zero] = c[..., zero].real * np.sqrt(2.0)
+    neg = np.nonzero(m_of < 0)[0]
+    mirror = neg - 2 * m_of[neg]  # omega(n, l, -m) = omega(n, l, m) - 2m
+    c[..., neg] = ((-1.0) ** m_of[neg]) * np.conj(c[..., mirror])
+    return c
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """Samples SM clock and throttle reasons via NVML while the timed region runs."""
@@ -201,6 +221,9 @@ def main():
                     help="N>1: split one transform by shells / (l, m) (strong scaling, default) "
                          "or run independent replicas (weak scaling)")
     ap.add_argument("--force-split", action="store_true", help="run the split path even at N=1 (testing)")
+    ap.add_argument("--real", action="store_true",
+                    help="real-valued functions through the real fast path (config C5: f_{nl,-m} = (-1)^m conj f_nlm, "
+                         "|f_nlm| ~ exp(-n/8))")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = env_rank()
@@ -236,8 +259,12 @@ def main():
     l2 = 126e6
     nrot = max(2, min(64, math.ceil(2 * l2 / (16 * Om * nb))))
     rng = np.random.default_rng(rank)
-    cin = torch.from_numpy(complex_normal(rng, (nrot, nb, Om))).cuda()
-    grid = torch.empty((nb, Ps), dtype=torch.complex128, device="cuda")
+    if args.real:
+        nrot = max(2, min(nrot, 8))
+        cin = torch.from_numpy(real_valued_coeffs(rng, B, (nrot, nb))).cuda()
+    else:
+        cin = torch.from_numpy(complex_normal(rng, (nrot, nb, Om))).cuda()
+    grid = torch.empty((nb, Ps), dtype=torch.float64 if args.real else torch.complex128, device="cuda")
     cout = torch.empty((nb, Om), dtype=torch.complex128, device="cuda")
     # a dedicated (non-default) stream: the library replays CUDA graphs of small,
     # launch-bound transforms on it
@@ -249,9 +276,12 @@ def main():
     graphs = (B ** 3) * nb <= 4 * 64 ** 3
     live_profile = not graphs
 
+    inv = sgl.ifsglft_real_batch if args.real else sgl.ifsglft_batch
+    fwd = sgl.fsglft_real_batch if args.real else sgl.fsglft_batch
+
     def step(s):
-        sgl.ifsglft_batch(plan, cin[s % nrot], out=grid)
-        sgl.fsglft_batch(plan, grid, out=cout)
+        inv(plan, cin[s % nrot], out=grid)
+        fwd(plan, grid, out=cout)
 
     for s in range(max(args.warmup, nrot + 2 if graphs else 0)):  # graphs need each input seen twice
         step(s)
@@ -296,17 +326,17 @@ def main():
     # ---- e2e through the public host API (pinned host buffers, copies timed)
     hc = torch.empty((nb, Om), dtype=torch.complex128).pin_memory().numpy()
     hc[:] = cin[0].cpu().numpy()
-    hg = torch.empty((nb, Ps), dtype=torch.complex128).pin_memory().numpy()
+    hg = torch.empty((nb, Ps), dtype=torch.float64 if args.real else torch.complex128).pin_memory().numpy()
     hb = torch.empty((nb, Om), dtype=torch.complex128).pin_memory().numpy()
-    sgl.ifsglft_batch(plan, hc, out=hg)
-    sgl.fsglft_batch(plan, hg, out=hb)
+    inv(plan, hc, out=hg)
+    fwd(plan, hg, out=hb)
     ke = args.e2e_steps
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(ke):
-        sgl.ifsglft_batch(plan, hc, out=hg)
-        sgl.fsglft_batch(plan, hg, out=hb)
+        inv(plan, hc, out=hg)
+        fwd(plan, hg, out=hb)
     e2e_ms = 1000.0 * (time.perf_counter() - t0) / ke
     if dist:
         t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
@@ -369,12 +399,14 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: iid complex normal coefficients (numpy PCG64, seed = rank)",
-        "config": {"workload": f"C3: B={B}, {nb} function(s) per step per GPU, ifsglft then fsglft",
+        "config": {"workload": (f"C5: B={B}, {nb} real-valued functions per step per GPU (real fast path)"
+                                if args.real else f"C3: B={B}, {nb} function(s) per step per GPU, ifsglft then fsglft"),
                    "B": B, "batch_per_gpu": nb, "parallelism": f"replicas x{world}" if world > 1 else "single",
                    "l2": f"inputs rotated over {nrot} coefficient buffers ({nrot * 16 * Om * nb / 1e6:.0f} MB) "
                          f"and every step writes/reads a {16 * Ps * nb / 2**20:.0f} MiB grid (> 126 MB L2)"},
         "e2e": {"value": world * nb / (e2e_ms / 1000.0), "unit": "transforms/s",
-                "h2d_bytes_per_step": 16 * (Om + Ps) * nb, "d2h_bytes_per_step": 16 * (Ps + Om) * nb,
+                "h2d_bytes_per_step": (16 * Om + (8 if args.real else 16) * Ps) * nb,
+                "d2h_bytes_per_step": ((8 if args.real else 16) * Ps + 16 * Om) * nb,
                 "ms_per_step": e2e_ms, "api": "paper_1604_05140_b200.ifsglft_batch/fsglft_batch (C ABI, host mem)"},
         "gpu_launches": gpu_launches,
         "roofline": roof,

@@ -79,6 +79,21 @@ int sglgpu_forward(sglgpu_plan* plan, const double* samples, double* coeffs, siz
 int sglgpu_inverse(sglgpu_plan* plan, const double* coeffs, double* samples, size_t batch,
                    int mem_kind, void* stream);
 
+/* Real-valued fast path (BASELINE config C5).
+ * forward_real: `samples` are 8B^3 REAL doubles per function (psi-order); returns
+ *   the full omega-order complex coefficients, identical (to rounding) to
+ *   sglgpu_forward of the same samples promoted to complex, which for real data
+ *   satisfy f_{n,l,-m} = (-1)^m conj(f_nlm).
+ * inverse_real: reads only the m >= 0 coefficients, assumes that symmetry, and
+ *   returns the 8B^3 real samples (the real part of sglgpu_inverse).
+ * Ring pairs are packed into one complex FFT and only m >= 0 is propagated
+ * through the polar and radial stages: about half the bytes and flops of the
+ * complex path.  Requires 2B a power of two >= 4. */
+int sglgpu_forward_real(sglgpu_plan* plan, const double* samples, double* coeffs, size_t batch,
+                        int mem_kind, void* stream);
+int sglgpu_inverse_real(sglgpu_plan* plan, const double* coeffs, double* samples, size_t batch,
+                        int mem_kind, void* stream);
+
 /* Stage entry points (device memory only, asynchronous on `stream`), used by the
  * multi-GPU shell / (l, m) decomposition.  `shells` is the nu-major intermediate
  * S[nu][f][i] (nu = l(l+1)+m, f < batch, i < shell_count), i.e. the transpose of

@@ -54,7 +54,7 @@ def lib():
         L.sglgpu_plan_table_bytes.argtypes = [_vp]
         L.sglgpu_plan_table_bytes.restype = ctypes.c_size_t
         L.sglgpu_last_launch_count.argtypes = [_vp]
-        for name in ("sglgpu_forward", "sglgpu_inverse"):
+        for name in ("sglgpu_forward", "sglgpu_inverse", "sglgpu_forward_real", "sglgpu_inverse_real"):
             getattr(L, name).argtypes = [_vp, _vp, _vp, ctypes.c_size_t, ctypes.c_int, _vp]
         for name in ("sglgpu_spherical_forward", "sglgpu_spherical_inverse"):
             getattr(L, name).argtypes = [_vp, _vp, ctypes.c_size_t, _vp, ctypes.c_int, ctypes.c_int,
@@ -328,6 +328,50 @@ def ifsglft_batch(plan: TransformPlan, coeffs, out=None, stream=None):
     return _batch_call(lib().sglgpu_inverse, plan, coeffs, coefficient_count(B), sample_count(B), out, stream)
 
 
+def _batch_call_real(fn, plan, src, n_in, n_out, in_dtype, out_dtype, out=None, stream=None):
+    if _is_torch(src):
+        import torch
+
+        td = {np.float64: torch.float64, np.complex128: torch.complex128}
+        if src.dtype != td[in_dtype] or not src.is_contiguous():
+            raise ValueError(f"expected a contiguous {td[in_dtype]} tensor")
+        if src.numel() % n_in:
+            raise ValueError("input length is not a whole number of functions")
+        batch = src.numel() // n_in
+        if out is None:
+            out = torch.empty((batch, n_out), dtype=td[out_dtype], device=src.device)
+        if src.is_cuda:
+            st = stream if stream is not None else torch.cuda.current_stream(src.device).cuda_stream
+            _check(fn(plan.handle, src.data_ptr(), out.data_ptr(), batch, MEM_DEVICE, st))
+        else:
+            _check(fn(plan.handle, src.data_ptr(), out.data_ptr(), batch, MEM_HOST, None))
+        return out
+    a = np.ascontiguousarray(src, dtype=in_dtype)
+    if a.size % n_in:
+        raise ValueError("input length is not a whole number of functions")
+    batch = a.size // n_in
+    if out is None:
+        out = np.empty((batch, n_out), dtype=out_dtype)
+    _check(fn(plan.handle, a.ctypes.data, out.ctypes.data, batch, MEM_HOST, None))
+    return out
+
+
+def fsglft_real_batch(plan: TransformPlan, samples, out=None, stream=None):
+    """Real-valued fast path: real samples [batch, 8B^3] (float64) -> complex
+    coefficients [batch, Omega] with f_{n,l,-m} = (-1)^m conj(f_nlm)."""
+    B = plan.bandlimit
+    return _batch_call_real(lib().sglgpu_forward_real, plan, samples, sample_count(B), coefficient_count(B),
+                            np.float64, np.complex128, out, stream)
+
+
+def ifsglft_real_batch(plan: TransformPlan, coeffs, out=None, stream=None):
+    """Real-valued fast path: Hermitian coefficients [batch, Omega] -> real samples
+    [batch, 8B^3] (float64).  Only the m >= 0 entries are read."""
+    B = plan.bandlimit
+    return _batch_call_real(lib().sglgpu_inverse_real, plan, coeffs, coefficient_count(B), sample_count(B),
+                            np.complex128, np.float64, out, stream)
+
+
 @dataclass
 class RoundtripError:
     max_abs: float = 0.0
@@ -357,6 +401,6 @@ def roundtrip_error(reference, actual) -> RoundtripError:
 
 __all__ = [
     "SphericalRule", "RadialRule", "TransformPlan", "SglCoefficients", "SampleGrid", "fsglft", "ifsglft",
-    "fsglft_batch", "ifsglft_batch", "roundtrip_error", "sphere_rule", "load_radial_rule", "sample_count",
+    "fsglft_batch", "ifsglft_batch", "fsglft_real_batch", "ifsglft_real_batch", "roundtrip_error", "sphere_rule", "load_radial_rule", "sample_count",
     "coefficient_count", "psi_index", "nu_index", "omega_index", "lib",
 ]

@@ -132,38 +132,39 @@ struct sglgpu_plan {
 namespace {
 
 // Host-side mirror of the per-problem shapes in sgl_kernels.cu.
-void problem_shape(Kind kind, int B, int batch, long long NB, int pid, int& M, int& N, int& K) {
+void problem_shape(Kind kind, int B, int batch, long long NB, int pid, bool real, int& M, int& N, int& K) {
     switch (kind) {
         case kLegFwd: {
             const int am = pid >> 1, r = B - am - (pid & 1);
             M = r > 0 ? (r + 1) / 2 : 0;
-            N = am == 0 ? (int)NB : 2 * (int)NB;
+            N = am == 0 || real ? (int)NB : 2 * (int)NB;
             K = B;
             break;
         }
         case kLegInv: {
             const int am = pid >> 1, r = B - am - (pid & 1);
             M = B;
-            N = am == 0 ? (int)NB : 2 * (int)NB;
+            N = am == 0 || real ? (int)NB : 2 * (int)NB;
             K = r > 0 ? (r + 1) / 2 : 0;
             break;
         }
         case kRadFwd:
             M = B - pid;
-            N = (2 * pid + 1) * batch * 2;
+            N = (real ? pid + 1 : 2 * pid + 1) * batch * 2;
             K = 2 * B;
             break;
         case kRadInv:
             M = 2 * B;
-            N = (2 * pid + 1) * batch * 2;
+            N = (real ? pid + 1 : 2 * pid + 1) * batch * 2;
             K = B - pid;
             break;
     }
 }
 
 // Tile list for one grouped contraction, heaviest K first, cached per shape.
-std::pair<sglk::Tile*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int SC, int lo, int hi) {
-    const auto key = std::make_tuple((int)kind, batch, SC, lo, hi);
+std::pair<sglk::Tile*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int SC, int lo, int hi,
+                                      bool real = false) {
+    const auto key = std::make_tuple((int)kind + (real ? 16 : 0), batch, SC, lo, hi);
     auto it = p->tiles.find(key);
     if (it != p->tiles.end()) return it->second;
     const int B = p->B;
@@ -179,7 +180,7 @@ std::pair<sglk::Tile*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int 
     const int wm_force = wm_env ? std::atoi(wm_env) : 0;
     for (int pid = plo; pid < phi; ++pid) {
         int M, N, K;
-        problem_shape(kind, B, batch, NB, pid, M, N, K);
+        problem_shape(kind, B, batch, NB, pid, real, M, N, K);
         if (M <= 0 || N <= 0) continue;
         if (K <= 0 && kind != kLegInv) continue;  // LegInv with K = 0 must still write zeros
         const bool leg = kind == kLegFwd || kind == kLegInv;
@@ -560,6 +561,104 @@ void check_plan(const sglgpu_plan* p) {
     if (!p) fail(SGLGPU_EINVAL, "sglgpu: null plan");
 }
 
+// Real-valued fast path (samples real, coefficients Hermitian in m): same three
+// stages with only m >= 0 computed; the radial epilogue writes m < 0 by symmetry.
+int real_device(sglgpu_plan* p, const double* in, double* out, int nb, cudaStream_t st, bool forward) {
+    const int B = p->B;
+    const size_t psi = (size_t)sample_count(B), om2 = 2 * (size_t)coefficient_count(B);
+    const Slices sl = plan_slices(B, nb);
+    p->S.ensure((size_t)4 * B * B * B * nb);
+    int n = 0, k;
+    for (int f0 = 0; f0 < nb; f0 += sl.functions) {
+        const int fb = std::min(sl.functions, nb - f0);
+        sglk::Geo g{B, 2 * B, fb, 2LL * fb * 2 * B, 1};
+        p->G.ensure((size_t)4 * B * B * g.NB);
+        const sglk::SView sv{g.NB, 2 * B, 0};
+        if (forward) {
+            auto lt = tiles_for(p, kLegFwd, fb, 2 * B, 0, 2 * B, true);
+            auto rt = tiles_for(p, kRadFwd, fb, 2 * B, 0, B, true);
+            k = staged(p, 0, st, [&] {
+                return sglk::launch_az_forward_real(g, in + (size_t)f0 * psi, psi, p->G.p, p->d_bcal, p->d_tw, st);
+            });
+            if (k == -2) fail(SGLGPU_EINVAL, "sglgpu real path: 2B must be a power of two >= 4");
+            ck_launch(k, "az_forward_real");
+            n += k;
+            k = staged(p, 1, st, [&] {
+                return sglk::launch_legendre_forward(g, sv, p->G.p, p->S.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+            });
+            ck_launch(k, "legendre_forward");
+            n += k;
+            k = staged(p, 2, st, [&] {
+                return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, p->S.p, out + (size_t)f0 * om2,
+                                                   p->d_W, p->d_W_off, rt.first, rt.second, st);
+            });
+            ck_launch(k, "radial_forward");
+            n += k;
+        } else {
+            auto rt = tiles_for(p, kRadInv, fb, 2 * B, 0, B, true);
+            auto lt = tiles_for(p, kLegInv, fb, 2 * B, 0, 2 * B, true);
+            k = staged(p, 3, st, [&] {
+                return sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, 0}, in + (size_t)f0 * om2, p->S.p,
+                                                   p->d_V, p->d_V_off, rt.first, rt.second, st);
+            });
+            ck_launch(k, "radial_inverse");
+            n += k;
+            k = staged(p, 4, st, [&] {
+                return sglk::launch_legendre_inverse(g, sv, p->S.p, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+            });
+            ck_launch(k, "legendre_inverse");
+            n += k;
+            k = staged(p, 5, st, [&] {
+                return sglk::launch_az_inverse_real(g, p->G.p, out + (size_t)f0 * psi, psi, p->d_tw, st);
+            });
+            if (k == -2) fail(SGLGPU_EINVAL, "sglgpu real path: 2B must be a power of two >= 4");
+            ck_launch(k, "az_inverse_real");
+            n += k;
+        }
+    }
+    return n;
+}
+
+int run_real(sglgpu_plan* p, const double* in, double* out, size_t batch, int mem_kind, void* stream, bool forward) {
+    return guarded([&] {
+        check_plan(p);
+        if (mem_kind != SGLGPU_MEM_HOST && mem_kind != SGLGPU_MEM_DEVICE)
+            fail(SGLGPU_EINVAL, "sglgpu: unknown mem_kind");
+        if (batch == 0) return;
+        if (!in || !out) fail(SGLGPU_EINVAL, "sglgpu: null data pointer");
+        const int B = p->B;
+        if (B < 2 || ((2 * B) & (2 * B - 1)) != 0)
+            fail(SGLGPU_EINVAL, "sglgpu real path: 2B must be a power of two >= 4");
+        std::lock_guard<std::mutex> lock(p->mu);
+        set_device(p);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const size_t psi = (size_t)sample_count(B), om = 2 * (size_t)coefficient_count(B);
+        const size_t in_len = forward ? psi : om, out_len = forward ? om : psi;
+        const size_t chunk = batch_chunk(B, batch);
+        int launches = 0;
+        if (mem_kind == SGLGPU_MEM_DEVICE) {
+            for (size_t b0 = 0; b0 < batch; b0 += chunk) {
+                const int nb = (int)std::min(chunk, batch - b0);
+                launches += real_device(p, in + b0 * in_len, out + b0 * out_len, nb, st, forward);
+            }
+        } else {
+            p->in.ensure(in_len * chunk);
+            p->out.ensure(out_len * chunk);
+            for (size_t b0 = 0; b0 < batch; b0 += chunk) {
+                const int nb = (int)std::min(chunk, batch - b0);
+                ck(cudaMemcpyAsync(p->in.p, in + b0 * in_len, nb * in_len * sizeof(double), cudaMemcpyHostToDevice, st),
+                   "H2D");
+                launches += real_device(p, p->in.p, p->out.p, nb, st, forward);
+                ck(cudaMemcpyAsync(out + b0 * out_len, p->out.p, nb * out_len * sizeof(double), cudaMemcpyDeviceToHost,
+                                   st),
+                   "D2H");
+            }
+            ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        }
+        p->last_launches = launches;
+    });
+}
+
 int run(sglgpu_plan* p, const double* in, double* out, size_t batch, int mem_kind, void* stream,
         bool forward) {
     return guarded([&] {
@@ -771,6 +870,16 @@ int sglgpu_forward(sglgpu_plan* plan, const double* samples, double* coeffs, siz
 int sglgpu_inverse(sglgpu_plan* plan, const double* coeffs, double* samples, size_t batch, int mem_kind,
                    void* stream) {
     return run(plan, coeffs, samples, batch, mem_kind, stream, false);
+}
+
+int sglgpu_forward_real(sglgpu_plan* plan, const double* samples, double* coeffs, size_t batch, int mem_kind,
+                        void* stream) {
+    return run_real(plan, samples, coeffs, batch, mem_kind, stream, true);
+}
+
+int sglgpu_inverse_real(sglgpu_plan* plan, const double* coeffs, double* samples, size_t batch, int mem_kind,
+                        void* stream) {
+    return run_real(plan, coeffs, samples, batch, mem_kind, stream, false);
 }
 
 int sglgpu_spherical_forward(sglgpu_plan* p, const double* samples, size_t sample_stride, double* shells,

@@ -23,6 +23,7 @@
 #include "sgl_kernels.cuh"
 
 #include <algorithm>
+#include <type_traits>
 
 namespace sglk {
 
@@ -343,6 +344,197 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
     }
 }
 
+// ------------------------------------------------------------------ real-valued azimuthal stage
+// Real samples: the rings j' and 2B-1-j' of a shell are packed into one complex
+// ring z = x1 + i x2 and transformed with ONE complex FFT; with Z = FFT(z),
+//   X1[m] = (Z[m] + conj Z[-m]) / 2,   X2[m] = (Z[m] - conj Z[-m]) / (2i),
+// and for real data only m >= 0 is needed (G[-m] = conj G[m]).  Half the bytes
+// in (8 B per sample) and half the FFTs of the complex path.  CTA: 2*IG shells,
+// one packed ring each (same thread count and shared memory as the complex path).
+template <int N>
+__global__ void __launch_bounds__(FFTShape<N>::THREADS, SGL_AZ_MINB)
+az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, double2* __restrict__ G,
+                       const double* __restrict__ bcal, const double2* __restrict__ twg) {
+    using S = FFTShape<N>;
+    constexpr int B = N / 2;
+    constexpr int IGR = 2 * S::IG;
+    extern __shared__ double2 smem[];
+    double2* tw = smem;
+    double2* rings = smem + N;
+    const int tid = threadIdx.x;
+    const int jp = blockIdx.y;
+    const int s0 = blockIdx.x * IGR;
+    const int nshell = g.batch * g.SC;
+    for (int x = tid; x < N; x += S::THREADS) tw[x] = __ldg(twg + x);
+    __syncthreads();
+    {
+        const int q = tid / S::T, tt = tid - q * S::T;
+        const int s = s0 + q;
+        const double* src1 = X;
+        const double* src2 = X;
+        const bool ok = s < nshell;
+        if (ok) {
+            const int f = s / g.SC, i = s - f * g.SC;
+            src1 = X + f * fstride + ((size_t)i * N + jp) * N;
+            src2 = X + f * fstride + ((size_t)i * N + (N - 1 - jp)) * N;
+        }
+        double2* ring = rings + q * S::STRIDE;
+        ring_fft_io<N, -1, false>(
+            ring, tt, tw, [&](int x) { return ok ? make_double2(__ldcs(src1 + x), __ldcs(src2 + x)) : make_double2(0.0, 0.0); },
+            [&](int x, double2 v) { ring[phys(x)] = v; });
+    }
+    __syncthreads();
+    const double b = __ldg(bcal + jp);
+    const long long row_len = g.NB / 2;
+#pragma unroll 4
+    for (int idx = tid; idx < 2 * B * IGR; idx += S::THREADS) {
+        const int sl = idx % IGR;
+        const int rowi = idx / IGR;  // p * B + m
+        const int p = rowi / B, m = rowi - p * B;
+        const int s = s0 + sl;
+        if (s >= nshell) continue;
+        const double2 zm = rings[sl * S::STRIDE + phys(m)];
+        const double2 zn = rings[sl * S::STRIDE + phys((N - m) & (N - 1))];
+        const double2 x1 = make_double2(0.5 * (zm.x + zn.x), 0.5 * (zm.y - zn.y));
+        const double2 x2 = make_double2(0.5 * (zm.y + zn.y), -0.5 * (zm.x - zn.x));
+        const double2 v = p ? csub(x1, x2) : cadd(x1, x2);
+        G[((((long long)p * B + m) * B + jp) * 2) * row_len + s] = cscale(b, v);
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(FFTShape<N>::THREADS, SGL_AZ_MINB)
+az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict__ X, size_t fstride,
+                       const double2* __restrict__ twg) {
+    using S = FFTShape<N>;
+    constexpr int B = N / 2;
+    constexpr int IGR = 2 * S::IG;
+    constexpr int EOS = N + 1;  // per shell: E[0..B) then O[0..B), padded
+    extern __shared__ double2 smem[];
+    double2* tw = smem;
+    double2* rings = smem + N;
+    double2* eo = rings + IGR * S::STRIDE;
+    const int tid = threadIdx.x;
+    const int jp = blockIdx.y;
+    const int s0 = blockIdx.x * IGR;
+    const int nshell = g.batch * g.SC;
+    const long long row_len = g.NB / 2;
+#pragma unroll 4
+    for (int idx = tid; idx < 2 * B * IGR; idx += S::THREADS) {
+        const int sl = idx % IGR;
+        const int rowi = idx / IGR;  // p * B + m
+        const int p = rowi / B, m = rowi - p * B;
+        const int s = s0 + sl;
+        double2* dst = eo + sl * EOS + p * B + m;
+        if (s < nshell) {
+            cp_async16(dst, G + ((((long long)p * B + m) * B + jp) * 2) * row_len + s);
+        } else {
+            *dst = make_double2(0.0, 0.0);
+        }
+    }
+    for (int x = tid; x < N; x += S::THREADS) tw[x] = __ldg(twg + x);
+    cp_async_wait_all();
+    __syncthreads();
+    {
+        const int q = tid / S::T, tt = tid - q * S::T;
+        const int s = s0 + q;
+        const double2* e_buf = eo + q * EOS;
+        double* dst1 = X;
+        double* dst2 = X;
+        const bool ok = s < nshell;
+        if (ok) {
+            const int f = s / g.SC, i = s - f * g.SC;
+            dst1 = X + f * fstride + ((size_t)i * N + jp) * N;
+            dst2 = X + f * fstride + ((size_t)i * N + (N - 1 - jp)) * N;
+        }
+        double2* ring = rings + q * S::STRIDE;
+        ring_fft_io<N, +1, false>(
+            ring, tt, tw,
+            [&](int bin) {
+                if (bin == B) return make_double2(0.0, 0.0);
+                const int m = bin < B ? bin : N - bin;
+                const double2 e = e_buf[m], o = e_buf[B + m];
+                const double2 x1 = cadd(e, o), x2 = csub(e, o);
+                if (bin == 0) return make_double2(x1.x, x2.x);
+                if (bin < B) return make_double2(x1.x - x2.y, x1.y + x2.x);  // X1 + i X2
+                return make_double2(x1.x + x2.y, x2.x - x1.y);                // conj X1 + i conj X2
+            },
+            [&](int x, double2 v) {
+                if (ok) {
+                    __stcs(dst1 + x, v.x);
+                    __stcs(dst2 + x, v.y);
+                }
+            });
+    }
+}
+
+template <int N>
+static int az_fwd_real_launch(const Geo& g, const double* X, size_t fstride, double* G, const double* bcal,
+                              const double* tw, cudaStream_t s) {
+    using S = FFTShape<N>;
+    constexpr int IGR = 2 * S::IG;
+    const size_t smem = sizeof(double2) * (N + IGR * S::STRIDE);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(az_forward_real_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const int nshell = g.batch * g.SC;
+    dim3 grid((nshell + IGR - 1) / IGR, g.B);
+    az_forward_real_kernel<N><<<grid, S::THREADS, smem, s>>>(g, X, fstride, reinterpret_cast<double2*>(G), bcal,
+                                                              reinterpret_cast<const double2*>(tw));
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+template <int N>
+static int az_inv_real_launch(const Geo& g, const double* G, double* X, size_t fstride, const double* tw,
+                              cudaStream_t s) {
+    using S = FFTShape<N>;
+    constexpr int IGR = 2 * S::IG;
+    const size_t smem = sizeof(double2) * (N + IGR * S::STRIDE + IGR * (N + 1));
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(az_inverse_real_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const int nshell = g.batch * g.SC;
+    dim3 grid((nshell + IGR - 1) / IGR, g.B);
+    az_inverse_real_kernel<N><<<grid, S::THREADS, smem, s>>>(g, reinterpret_cast<const double2*>(G), X, fstride,
+                                                              reinterpret_cast<const double2*>(tw));
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// sample_stride: doubles per function (8B^3 for real samples)
+int launch_az_forward_real(const Geo& g, const double* samples, size_t sample_stride, double* G,
+                           const double* bcal, const double* twiddle, cudaStream_t s) {
+    switch (2 * g.B) {
+        case 4: return az_fwd_real_launch<4>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 8: return az_fwd_real_launch<8>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 16: return az_fwd_real_launch<16>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 32: return az_fwd_real_launch<32>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 64: return az_fwd_real_launch<64>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 128: return az_fwd_real_launch<128>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 256: return az_fwd_real_launch<256>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 512: return az_fwd_real_launch<512>(g, samples, sample_stride, G, bcal, twiddle, s);
+        default: return -2;  // real fast path needs a power-of-two 2B >= 4
+    }
+}
+
+int launch_az_inverse_real(const Geo& g, const double* G, double* samples, size_t sample_stride,
+                           const double* twiddle, cudaStream_t s) {
+    switch (2 * g.B) {
+        case 4: return az_inv_real_launch<4>(g, G, samples, sample_stride, twiddle, s);
+        case 8: return az_inv_real_launch<8>(g, G, samples, sample_stride, twiddle, s);
+        case 16: return az_inv_real_launch<16>(g, G, samples, sample_stride, twiddle, s);
+        case 32: return az_inv_real_launch<32>(g, G, samples, sample_stride, twiddle, s);
+        case 64: return az_inv_real_launch<64>(g, G, samples, sample_stride, twiddle, s);
+        case 128: return az_inv_real_launch<128>(g, G, samples, sample_stride, twiddle, s);
+        case 256: return az_inv_real_launch<256>(g, G, samples, sample_stride, twiddle, s);
+        case 512: return az_inv_real_launch<512>(g, G, samples, sample_stride, twiddle, s);
+        default: return -2;
+    }
+}
+
 // ------------------------------------------------------------------ naive azimuthal (non-pow2 2B)
 // Direct DFT per ring for bandlimits whose 2B is not a power of two (the
 // reference's naive fallback, kernels.cpp:35-45).  One CTA per (shell, j').
@@ -446,7 +638,7 @@ struct LegFwd {
     static constexpr bool B_KCONTIG = false;
     __device__ int am(int pid) const { return pid >> 1; }
     __device__ int M(int pid) const { const int r = g.B - am(pid) - (pid & 1); return r > 0 ? (r + 1) / 2 : 0; }
-    __device__ int N(int pid) const { return am(pid) == 0 ? (int)g.NB : 2 * (int)g.NB; }
+    __device__ int N(int pid) const { return am(pid) == 0 || g.real ? (int)g.NB : 2 * (int)g.NB; }
     __device__ int K(int) const { return g.B; }
     static constexpr bool B_COL_AFFINE = true;  // within a sign-half-aligned tile
     // end (exclusive) of the sign half that column n0 lies in
@@ -483,7 +675,7 @@ struct LegInv {
     static constexpr bool B_KCONTIG = false;
     __device__ int am(int pid) const { return pid >> 1; }
     __device__ int M(int) const { return g.B; }
-    __device__ int N(int pid) const { return am(pid) == 0 ? (int)g.NB : 2 * (int)g.NB; }
+    __device__ int N(int pid) const { return am(pid) == 0 || g.real ? (int)g.NB : 2 * (int)g.NB; }
     __device__ int K(int pid) const { const int r = g.B - am(pid) - (pid & 1); return r > 0 ? (r + 1) / 2 : 0; }
     static constexpr bool B_COL_AFFINE = true;
     __device__ int nlim(int pid, int n0) const { return n0 < g.NB ? (int)g.NB : N(pid); }
@@ -535,7 +727,8 @@ struct RadFwd {
     static constexpr bool A_KCONTIG = true;
     static constexpr bool B_KCONTIG = true;
     __device__ int M(int l) const { return g.B - l; }
-    __device__ int N(int l) const { return (2 * l + 1) * g.batch * 2; }
+    __device__ int mw(int l) const { return g.real ? l + 1 : 2 * l + 1; }  // orders per (l, f)
+    __device__ int N(int l) const { return mw(l) * g.batch * 2; }
     __device__ int K(int) const { return 2 * g.B; }
     static constexpr bool B_COL_AFFINE = false;
     __device__ int nlim(int l, int) const { return N(l); }
@@ -546,18 +739,28 @@ struct RadFwd {
     __device__ long long rowB(int, int k) const { return sb.row(k); }
     __device__ long long b_kstep(int) const { return sb.sc_blk == 2 * g.B ? 2 : 0; }
     __device__ long long colB(int l, int n) const {
-        const int mf = n >> 1, w = 2 * l + 1;
-        const int f = mf / w, mm = mf - f * w;  // mm = m + l
+        const int mf = n >> 1, w = mw(l);
+        const int f = mf / w, mm = mf - f * w + (g.real ? l : 0);  // mm = m + l
         return ((long long)l * l + mm - sb.nu0) * g.NB + (long long)f * 2 * g.SC + (n & 1);
     }
     __device__ long long rowC(int l, int r) const { return 2 * degree_offset(l + 1 + r); }
     __device__ long long colC(int l, int n) const {
-        const int mf = n >> 1, w = 2 * l + 1;
-        const int f = mf / w, mm = mf - f * w;
+        const int mf = n >> 1, w = mw(l);
+        const int f = mf / w, mm = mf - f * w + (g.real ? l : 0);
         return (long long)f * 2 * omega + 2LL * ((long long)l * l + mm) + (n & 1);
     }
     __device__ double scaleC(int, int) const { return 1.0; }
     __device__ bool c_affine(int, int, int) const { return false; }
+    // real-valued path: every m > 0 coefficient also lands at -m as (-1)^m conj
+    static constexpr bool MIRROR = true;
+    __device__ long long colC_mirror(int l, int n, double& sign) const {
+        if (!g.real) return -1;
+        const int mf = n >> 1, w = mw(l);
+        const int f = mf / w, m = mf - f * w;
+        if (m == 0) return -1;
+        sign = (m & 1) ? -1.0 : 1.0;
+        return (long long)f * 2 * omega + 2LL * ((long long)l * l + l - m) + (n & 1);
+    }
 };
 
 // Radial inverse: prob = l.  rows i (M = 2B), K = B-l (n), cols (mf, c).
@@ -572,7 +775,8 @@ struct RadInv {
     static constexpr bool A_KCONTIG = true;
     static constexpr bool B_KCONTIG = false;
     __device__ int M(int) const { return 2 * g.B; }
-    __device__ int N(int l) const { return (2 * l + 1) * g.batch * 2; }
+    __device__ int mw(int l) const { return g.real ? l + 1 : 2 * l + 1; }
+    __device__ int N(int l) const { return mw(l) * g.batch * 2; }
     __device__ int K(int l) const { return g.B - l; }
     static constexpr bool B_COL_AFFINE = false;
     __device__ int nlim(int l, int) const { return N(l); }
@@ -583,14 +787,14 @@ struct RadInv {
     __device__ long long rowB(int l, int k) const { return 2 * degree_offset(l + 1 + k); }
     __device__ long long b_kstep(int) const { return 0; }
     __device__ long long colB(int l, int n) const {
-        const int mf = n >> 1, w = 2 * l + 1;
-        const int f = mf / w, mm = mf - f * w;
+        const int mf = n >> 1, w = mw(l);
+        const int f = mf / w, mm = mf - f * w + (g.real ? l : 0);
         return (long long)f * 2 * omega + 2LL * ((long long)l * l + mm) + (n & 1);
     }
     __device__ long long rowC(int, int i) const { return sb.row(i); }
     __device__ long long colC(int l, int n) const {
-        const int mf = n >> 1, w = 2 * l + 1;
-        const int f = mf / w, mm = mf - f * w;
+        const int mf = n >> 1, w = mw(l);
+        const int f = mf / w, mm = mf - f * w + (g.real ? l : 0);
         return ((long long)l * l + mm - sb.nu0) * g.NB + (long long)f * 2 * g.SC + (n & 1);
     }
     __device__ double scaleC(int, int) const { return 1.0; }
@@ -628,6 +832,11 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem_dst, const void* gme
 // predication; shared-memory tiles keep the operand's contiguous dimension
 // innermost (padded) so fills and fragment loads are bank-conflict free.
 // 8-row fragments past M, 8-col fragments past N and k-steps past K are skipped.
+template <class P, class = void>
+struct has_mirror : std::false_type {};
+template <class P>
+struct has_mirror<P, std::void_t<decltype(P::MIRROR)>> : std::bool_constant<P::MIRROR> {};
+
 template <class P, int WM>
 struct GemmCfg {
     static constexpr int FM = 4;
@@ -827,6 +1036,12 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
             const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
             if (col >= N) continue;
             *reinterpret_cast<double2*>(out + cofs[fn]) = make_double2(csc[fn] * acc[fm][fn][0], csc[fn] * acc[fm][fn][1]);
+            if constexpr (has_mirror<P>::value) {
+                double sg = 1.0;
+                const long long mo = pr.colC_mirror(pid, col, sg);
+                if (mo >= 0)
+                    *reinterpret_cast<double2*>(out + mo) = make_double2(sg * acc[fm][fn][0], -sg * acc[fm][fn][1]);
+            }
         }
     }
 }

@@ -31,6 +31,7 @@ struct Geo {
     int SC;         // shells per function in this call (2B for the whole transform)
     int batch;      // functions
     long long NB;   // reals per nu-row of S and per G row half: batch * SC * 2
+    int real = 0;   // real-valued fast path: only m >= 0 is computed (f_{n,l,-m} = (-1)^m conj f_nlm)
 };
 
 // Azimuthal stage (forward): FFT of length 2B per ring (sign -1, kernels.cpp:478),
@@ -38,6 +39,12 @@ struct Geo {
 //   G[p][|m|][j'][sgn][f][i]  (complex), p = parity, j' < B, sgn = (m < 0).
 int launch_az_forward(const Geo& g, const double* samples, size_t sample_stride,
                       double* G, const double* bcal, const double* twiddle, cudaStream_t s);
+// Real-valued variants: samples are 8B^3 reals per function (psi-order); the ring
+// pair (j', 2B-1-j') is packed into one complex FFT and only m >= 0 is kept.
+int launch_az_forward_real(const Geo& g, const double* samples, size_t sample_stride, double* G,
+                           const double* bcal, const double* twiddle, cudaStream_t s);
+int launch_az_inverse_real(const Geo& g, const double* G, double* samples, size_t sample_stride,
+                           const double* twiddle, cudaStream_t s);
 // Azimuthal stage (inverse): unfold E/O, zero Nyquist bin, FFT sign +1 without
 // 1/N (kernels.cpp:491), write psi-order rings.
 int launch_az_inverse(const Geo& g, const double* G, double* samples, size_t sample_stride,
