@@ -377,3 +377,41 @@ def test_real_path_rejects_unsupported_bandlimit():
     plan, _ = plan_for(3)
     with pytest.raises(ValueError, match="power of two"):
         sgl.fsglft_real_batch(plan, np.zeros(sgl.sample_count(3)))
+
+
+def test_nccl_split_path_single_rank():
+    """The distributed path end to end over NCCL (torchrun, one rank on this GPU)."""
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                          "--master-addr", "127.0.0.1", "--master-port", "29561",
+                          os.path.join(here, "dist_split_check.py"), "16", "2"],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "NCCL split path OK" in out.stdout
+
+
+def test_full_size_properties_b128():
+    """Size-independent checks at the headline size: Parseval (quadrature norm of
+    the synthesis = coefficient norm, test_sgl_transform.cpp:257-279), linearity
+    and zero -> zero, all on the GPU path."""
+    import torch
+
+    B = 128
+    plan, orc = plan_for(B)
+    rng = np.random.default_rng(128)
+    n = sgl.coefficient_count(B)
+    c = torch.from_numpy(complex_normal(rng, (2, n))).cuda()
+    g = sgl.ifsglft_batch(plan, c)
+    w = torch.from_numpy((orc.a * orc.r ** 2)[:, None, None] * orc.b_cal[None, :, None]).cuda()
+    gn = (w * g.view(2, 2 * B, 2 * B, 2 * B).abs() ** 2).sum(dim=(1, 2, 3))
+    cn = (c.abs() ** 2).sum(dim=1)
+    assert torch.allclose(gn / cn, torch.ones_like(cn), rtol=1e-9, atol=0)
+    a = 0.3 - 1.1j
+    lin = sgl.ifsglft_batch(plan, (a * c[0] + c[1]).unsqueeze(0).contiguous())[0]
+    ref = a * g[0] + g[1]
+    assert float((lin - ref).abs().max() / ref.abs().max()) < 1e-13
+    z = sgl.fsglft_batch(plan, torch.zeros((1, sgl.sample_count(B)), dtype=torch.complex128, device="cuda"))
+    assert not bool(z.abs().max())
