@@ -111,14 +111,24 @@ __device__ __forceinline__ int phys(int x) { return x + (x >> 4); }
 #define SGL_AZ_MINB 4
 #endif
 
-template <int N>
+#ifndef SGL_AZI_ELEMS
+#define SGL_AZI_ELEMS SGL_AZ_ELEMS  // inverse kernel tile size
+#endif
+#ifndef SGL_AZI_MINB
+#define SGL_AZI_MINB SGL_AZ_MINB
+#endif
+#ifndef SGL_AZI_ASYNC
+#define SGL_AZI_ASYNC 0  // inverse prologue: cp.async (1) or register loads (0); measured: 0 is faster
+#endif
+
+template <int N, int ELEMS = SGL_AZ_ELEMS>
 struct FFTShape {
     static constexpr int RMAX = N < 16 ? N : 16;
     static constexpr int T = N / RMAX;              // threads per ring
     static constexpr int STRIDE = N + N / 16 + 1;   // padded ring stride (complex)
     static constexpr int LOGN = ilog2c(N);
     static constexpr int R0 = 1 << (LOGN % 4 == 0 ? (N < 16 ? LOGN : 4) : LOGN % 4);  // first radix
-    static constexpr int IG = (T * 2 <= 256) ? (SGL_AZ_ELEMS / 16) / T : 1;  // shell pairs per CTA
+    static constexpr int IG = (T * 2 <= 256) ? (ELEMS / 16) / T : 1;  // shell pairs per CTA
     static constexpr int THREADS = 2 * IG * T;
 };
 
@@ -285,10 +295,10 @@ az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2*
 // from both buffers (Nyquist bin B zero); the last pass writes the psi-order
 // samples straight to HBM (coalesced).
 template <int N>
-__global__ void __launch_bounds__(FFTShape<N>::THREADS, SGL_AZ_MINB)
+__global__ void __launch_bounds__(FFTShape<N, SGL_AZI_ELEMS>::THREADS, SGL_AZI_MINB)
 az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X, size_t fstride,
                   const double2* __restrict__ twg) {
-    using S = FFTShape<N>;
+    using S = FFTShape<N, SGL_AZI_ELEMS>;
     constexpr int B = N / 2;
     extern __shared__ double2 smem[];
     double2* tw = smem;
@@ -309,13 +319,15 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
             const int m = bin < B ? bin : bin - N;
             const int am = m < 0 ? -m : m;
             const int sgn = m < 0 ? 1 : 0;
-            cp_async16(dst, G + ((((long long)p * B + am) * B + jp) * 2 + sgn) * row_len + s);
+            const double2* src = G + ((((long long)p * B + am) * B + jp) * 2 + sgn) * row_len + s;
+            if (SGL_AZI_ASYNC) cp_async16(dst, src);
+            else *dst = __ldcs(src);
         } else {
             *dst = make_double2(0.0, 0.0);
         }
     }
     for (int x = tid; x < N; x += S::THREADS) tw[x] = __ldg(twg + x);
-    cp_async_wait_all();
+    if (SGL_AZI_ASYNC) cp_async_wait_all();
     __syncthreads();
     {
         const int q = tid / S::T, tt = tid - q * S::T;
@@ -1079,7 +1091,7 @@ static int az_fwd_launch(const Geo& g, const double* X, size_t fstride, double* 
 template <int N>
 static int az_inv_launch(const Geo& g, const double* G, double* X, size_t fstride, const double* tw,
                          cudaStream_t s) {
-    using S = FFTShape<N>;
+    using S = FFTShape<N, SGL_AZI_ELEMS>;
     const size_t smem = sizeof(double2) * (N + 2 * S::IG * S::STRIDE);
     static bool attr = false;
     if (!attr) {
