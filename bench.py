@@ -416,6 +416,9 @@ def main():
         "clocks": clk.summary(),
         "roundtrip_normwise_err": max(err, e2e_err),
     }
+    if not (line["roundtrip_normwise_err"] < 1e-10):
+        raise SystemExit(f"bench: round trip failed (normwise error {line['roundtrip_normwise_err']:.3e}); "
+                         "refusing to report a timing of wrong results")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(B)
     if rank == 0:
@@ -510,6 +513,8 @@ def split_arm(args, rank, world, local):
         "clocks": clk.summary(),
         "roundtrip_normwise_err": err,
     }
+    if not (err < 1e-10):
+        raise SystemExit(f"bench: distributed round trip failed (normwise error {err:.3e})")
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -339,7 +339,7 @@ int forward_device(sglgpu_plan* p, const double* X, double* C, int nb, cudaStrea
         ensure_aux(p);
         const int SC = sl.shells;
         sglk::Geo gc{B, SC, 1, 2LL * SC};
-        const size_t gslice = (size_t)4 * B * B * gc.NB;
+        const size_t gslice = 2 * (size_t)sglk::g_layout(gc);
         p->G.ensure(2 * gslice);
         const sglk::SView sv{2LL * 2 * B, 2 * B, 0};
         auto lt = tiles_for(p, kLegFwd, 1, SC, 0, 2 * B);
@@ -389,7 +389,7 @@ int forward_device(sglgpu_plan* p, const double* X, double* C, int nb, cudaStrea
         // shell slices: az + Legendre per slice into the full S, then radial once
         const int SC = sl.shells;
         sglk::Geo gc{B, SC, 1, 2LL * SC};
-        p->G.ensure((size_t)4 * B * B * gc.NB);
+        p->G.ensure(2 * (size_t)sglk::g_layout(gc));
         const sglk::SView sv{2LL * 2 * B, 2 * B, 0};
         auto lt = tiles_for(p, kLegFwd, 1, SC, 0, 2 * B);
         for (int c = 0; c < sl.count; ++c) {
@@ -420,7 +420,7 @@ int forward_device(sglgpu_plan* p, const double* X, double* C, int nb, cudaStrea
     for (int f0 = 0; f0 < nb; f0 += sl.functions) {
         const int fb = std::min(sl.functions, nb - f0);
         sglk::Geo g{B, 2 * B, fb, 2LL * fb * 2 * B};
-        p->G.ensure((size_t)4 * B * B * g.NB);
+        p->G.ensure(2 * (size_t)sglk::g_layout(g));
         const sglk::SView sv{g.NB, 2 * B, 0};
         auto lt = tiles_for(p, kLegFwd, fb, 2 * B, 0, 2 * B);
         auto rt = tiles_for(p, kRadFwd, fb, 2 * B, 0, B);
@@ -470,7 +470,7 @@ int inverse_device(sglgpu_plan* p, const double* C, double* X, int nb, cudaStrea
         n += k;
         const int SC = sl.shells;
         sglk::Geo gc{B, SC, 1, 2LL * SC};
-        const size_t gslice = (size_t)4 * B * B * gc.NB;
+        const size_t gslice = 2 * (size_t)sglk::g_layout(gc);
         p->G.ensure(2 * gslice);
         auto lt = tiles_for(p, kLegInv, 1, SC, 0, 2 * B);
         std::vector<cudaEvent_t> az_done(sl.count);
@@ -512,7 +512,7 @@ int inverse_device(sglgpu_plan* p, const double* C, double* X, int nb, cudaStrea
         n += k;
         const int SC = sl.shells;
         sglk::Geo gc{B, SC, 1, 2LL * SC};
-        p->G.ensure((size_t)4 * B * B * gc.NB);
+        p->G.ensure(2 * (size_t)sglk::g_layout(gc));
         auto lt = tiles_for(p, kLegInv, 1, SC, 0, 2 * B);
         for (int c = 0; c < sl.count; ++c) {
             const int i0 = c * SC;
@@ -533,7 +533,7 @@ int inverse_device(sglgpu_plan* p, const double* C, double* X, int nb, cudaStrea
     for (int f0 = 0; f0 < nb; f0 += sl.functions) {
         const int fb = std::min(sl.functions, nb - f0);
         sglk::Geo g{B, 2 * B, fb, 2LL * fb * 2 * B};
-        p->G.ensure((size_t)4 * B * B * g.NB);
+        p->G.ensure(2 * (size_t)sglk::g_layout(g));
         const sglk::SView sv{g.NB, 2 * B, 0};
         auto rt = tiles_for(p, kRadInv, fb, 2 * B, 0, B);
         auto lt = tiles_for(p, kLegInv, fb, 2 * B, 0, 2 * B);
@@ -572,7 +572,7 @@ int real_device(sglgpu_plan* p, const double* in, double* out, int nb, cudaStrea
     for (int f0 = 0; f0 < nb; f0 += sl.functions) {
         const int fb = std::min(sl.functions, nb - f0);
         sglk::Geo g{B, 2 * B, fb, 2LL * fb * 2 * B, 1};
-        p->G.ensure((size_t)4 * B * B * g.NB);
+        p->G.ensure(2 * (size_t)sglk::g_layout(g));
         const sglk::SView sv{g.NB, 2 * B, 0};
         if (forward) {
             auto lt = tiles_for(p, kLegFwd, fb, 2 * B, 0, 2 * B, true);
@@ -895,7 +895,7 @@ int sglgpu_spherical_forward(sglgpu_plan* p, const double* samples, size_t sampl
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         const int nb = (int)batch;
         sglk::Geo g{B, shell_count, nb, 2LL * nb * shell_count};
-        p->G.ensure((size_t)4 * B * B * g.NB);
+        p->G.ensure(2 * (size_t)sglk::g_layout(g));
         int n = sglk::launch_az_forward(g, samples, 2 * sample_stride, p->G.p, p->d_bcal, p->d_tw, st);
         ck_launch(n, "az_forward");
         auto lt = tiles_for(p, kLegFwd, nb, shell_count, 0, 2 * B);
@@ -919,7 +919,7 @@ int sglgpu_spherical_inverse(sglgpu_plan* p, const double* shells, double* sampl
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         const int nb = (int)batch;
         sglk::Geo g{B, shell_count, nb, 2LL * nb * shell_count};
-        p->G.ensure((size_t)4 * B * B * g.NB);
+        p->G.ensure(2 * (size_t)sglk::g_layout(g));
         auto lt = tiles_for(p, kLegInv, nb, shell_count, 0, 2 * B);
         const sglk::SView sv{g.NB, shell_count, 0};
         int k = sglk::launch_legendre_inverse(g, sv, shells, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);

@@ -271,7 +271,6 @@ az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2*
     __syncthreads();
     // epilogue: E/O fold, b_cal, scatter rows G[p][|m|][j'][sgn][s]
     const double b = __ldg(bcal + jp);
-    const long long row_len = g.NB / 2;  // complex per row
 #pragma unroll 4
     for (int idx = tid; idx < 2 * N * S::IG; idx += S::THREADS) {
         const int sl = idx % S::IG;
@@ -279,13 +278,10 @@ az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2*
         const int p = rowi / N, bin = rowi - p * N;
         const int s = s0 + sl;
         if (bin == B || s >= nshell) continue;
-        const int m = bin < B ? bin : bin - N;
-        const int am = m < 0 ? -m : m;
-        const int sgn = m < 0 ? 1 : 0;
         const double2 f1 = rings[(2 * sl) * S::STRIDE + phys(bin)];
         const double2 f2 = rings[(2 * sl + 1) * S::STRIDE + phys(bin)];
         const double2 v = p ? csub(f1, f2) : cadd(f1, f2);
-        G[((((long long)p * B + am) * B + jp) * 2 + sgn) * row_len + s] = cscale(b, v);
+        G[g_index(g, p, bin, jp, s)] = cscale(b, v);
     }
 }
 
@@ -307,7 +303,6 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
     const int jp = blockIdx.y;
     const int s0 = blockIdx.x * S::IG;
     const int nshell = g.batch * g.SC;
-    const long long row_len = g.NB / 2;
 #pragma unroll 4
     for (int idx = tid; idx < 2 * N * S::IG; idx += S::THREADS) {
         const int sl = idx % S::IG;
@@ -316,10 +311,7 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
         const int s = s0 + sl;
         double2* dst = rings + (2 * sl + p) * S::STRIDE + phys(bin);
         if (bin != B && s < nshell) {
-            const int m = bin < B ? bin : bin - N;
-            const int am = m < 0 ? -m : m;
-            const int sgn = m < 0 ? 1 : 0;
-            const double2* src = G + ((((long long)p * B + am) * B + jp) * 2 + sgn) * row_len + s;
+            const double2* src = G + g_index(g, p, bin, jp, s);
             if (SGL_AZI_ASYNC) cp_async16(dst, src);
             else *dst = __ldcs(src);
         } else {
@@ -397,7 +389,6 @@ az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, doub
     }
     __syncthreads();
     const double b = __ldg(bcal + jp);
-    const long long row_len = g.NB / 2;
 #pragma unroll 4
     for (int idx = tid; idx < 2 * B * IGR; idx += S::THREADS) {
         const int sl = idx % IGR;
@@ -410,7 +401,7 @@ az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, doub
         const double2 x1 = make_double2(0.5 * (zm.x + zn.x), 0.5 * (zm.y - zn.y));
         const double2 x2 = make_double2(0.5 * (zm.y + zn.y), -0.5 * (zm.x - zn.x));
         const double2 v = p ? csub(x1, x2) : cadd(x1, x2);
-        G[((((long long)p * B + m) * B + jp) * 2) * row_len + s] = cscale(b, v);
+        G[g_index(g, p, m, jp, s)] = cscale(b, v);
     }
 }
 
@@ -430,7 +421,6 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
     const int jp = blockIdx.y;
     const int s0 = blockIdx.x * IGR;
     const int nshell = g.batch * g.SC;
-    const long long row_len = g.NB / 2;
 #pragma unroll 4
     for (int idx = tid; idx < 2 * B * IGR; idx += S::THREADS) {
         const int sl = idx % IGR;
@@ -439,7 +429,7 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
         const int s = s0 + sl;
         double2* dst = eo + sl * EOS + p * B + m;
         if (s < nshell) {
-            cp_async16(dst, G + ((((long long)p * B + m) * B + jp) * 2) * row_len + s);
+            cp_async16(dst, G + g_index(g, p, m, jp, s));
         } else {
             *dst = make_double2(0.0, 0.0);
         }
@@ -564,7 +554,6 @@ __global__ void az_forward_naive_kernel(Geo g, const double2* __restrict__ X, si
         r2[e] = X[(size_t)f * fstride + ((size_t)i * N + (N - 1 - jp)) * N + e];
     }
     __syncthreads();
-    const long long row_len = g.NB / 2;
     for (int bin = threadIdx.x; bin < N; bin += blockDim.x) {
         if (bin == B) continue;
         double2 a1 = make_double2(0, 0), a2 = make_double2(0, 0);
@@ -573,11 +562,9 @@ __global__ void az_forward_naive_kernel(Geo g, const double2* __restrict__ X, si
             a1 = cadd(a1, cmul(r1[k], w));
             a2 = cadd(a2, cmul(r2[k], w));
         }
-        const int m = bin < B ? bin : bin - N;
-        const int am = m < 0 ? -m : m, sgn = m < 0;
         for (int p = 0; p < 2; ++p) {
             const double2 v = p ? csub(a1, a2) : cadd(a1, a2);
-            G[((((long long)p * B + am) * B + jp) * 2 + sgn) * row_len + s] = cscale(bcal[jp], v);
+            G[g_index(g, p, bin, jp, s)] = cscale(bcal[jp], v);
         }
     }
 }
@@ -590,14 +577,11 @@ __global__ void az_inverse_naive_kernel(Geo g, const double2* __restrict__ G, do
     const int f = s / g.SC, i = s - f * g.SC;
     double2* r1 = smem;
     double2* r2 = smem + N;
-    const long long row_len = g.NB / 2;
     for (int bin = threadIdx.x; bin < N; bin += blockDim.x) {
         double2 e = make_double2(0, 0), o = make_double2(0, 0);
         if (bin != B) {
-            const int m = bin < B ? bin : bin - N;
-            const int am = m < 0 ? -m : m, sgn = m < 0;
-            e = G[((((long long)0 * B + am) * B + jp) * 2 + sgn) * row_len + s];
-            o = G[((((long long)1 * B + am) * B + jp) * 2 + sgn) * row_len + s];
+            e = G[g_index(g, 0, bin, jp, s)];
+            o = G[g_index(g, 1, bin, jp, s)];
         }
         r1[bin] = cadd(e, o);
         r2[bin] = csub(e, o);
@@ -639,6 +623,19 @@ __device__ __forceinline__ long long s_col(const Geo& g, const SView& sv, int am
     return (sgn ? -am : am) * sv.NB + (long long)f * 2 * sv.sc + 2LL * sv.i0 + rem;
 }
 
+// Real offset of column n of a Legendre problem inside the blocked G (the row
+// part, j' * row stride, is separate): n = (sgn, flat shell s, re/im).
+__device__ __forceinline__ long long g_col(const Geo& g, int p, int am, int n) {
+    const int sgn = n >= g.NB;
+    const int nn = n - (sgn ? (int)g.NB : 0);
+    const int s = nn >> 1;
+    const int bin = sgn ? 2 * g.B - am : am;
+    const long long gx = s >> g.lgib;
+    const int sl = s & ((1 << g.lgib) - 1);
+    return 2 * ((((gx * 2 + p) * g.nbins + bin) << g.lgib) + sl) + (nn & 1);
+}
+__device__ __forceinline__ long long g_rowstride(const Geo& g) { return 2 * g.ngx * 2 * g.nbins << g.lgib; }
+
 struct LegFwd {
     Geo g;
     const double* A;        // table
@@ -652,18 +649,16 @@ struct LegFwd {
     __device__ int M(int pid) const { const int r = g.B - am(pid) - (pid & 1); return r > 0 ? (r + 1) / 2 : 0; }
     __device__ int N(int pid) const { return am(pid) == 0 || g.real ? (int)g.NB : 2 * (int)g.NB; }
     __device__ int K(int) const { return g.B; }
-    static constexpr bool B_COL_AFFINE = true;  // within a sign-half-aligned tile
+    static constexpr bool B_COL_AFFINE = false;  // blocked G: per-column offsets
     // end (exclusive) of the sign half that column n0 lies in
     __device__ int nlim(int pid, int n0) const { return n0 < g.NB ? (int)g.NB : N(pid); }
     __device__ long long rowA(int pid, int r) const { return aoff[pid] + (long long)r * g.B; }
     __device__ long long colA(int, int k) const { return k; }
     __device__ int a_sr(int) const { return g.B; }
     __device__ int a_sk(int) const { return 1; }
-    __device__ long long rowB(int pid, int k) const {
-        return ((((long long)(pid & 1) * g.B + am(pid)) * g.B + k) * 2) * g.NB;
-    }
-    __device__ long long b_kstep(int) const { return 2 * g.NB; }
-    __device__ long long colB(int, int n) const { return n; }
+    __device__ long long rowB(int, int k) const { return (long long)k * g_rowstride(g); }
+    __device__ long long b_kstep(int) const { return g_rowstride(g); }
+    __device__ long long colB(int pid, int n) const { return g_col(g, pid & 1, am(pid), n); }
     __device__ long long rowC(int pid, int r) const {
         const long long l = am(pid) + (pid & 1) + 2 * r;
         return l * (l + 1) * sv.NB;
@@ -701,12 +696,10 @@ struct LegInv {
     }
     __device__ long long b_kstep(int) const { return 0; }
     __device__ long long colB(int pid, int n) const { return s_col(g, sv, am(pid), n); }
-    __device__ long long rowC(int pid, int j) const {
-        return ((((long long)(pid & 1) * g.B + am(pid)) * g.B + j) * 2) * g.NB;
-    }
-    __device__ long long colC(int, int n) const { return n; }
+    __device__ long long rowC(int, int j) const { return (long long)j * g_rowstride(g); }
+    __device__ long long colC(int pid, int n) const { return g_col(g, pid & 1, am(pid), n); }
     __device__ double scaleC(int pid, int n) const { return (n >= g.NB && (am(pid) & 1)) ? -1.0 : 1.0; }
-    __device__ bool c_affine(int, int, int) const { return true; }
+    __device__ bool c_affine(int, int, int) const { return false; }  // blocked G: per-column offsets
 };
 
 __host__ __device__ inline long long degree_offset(long long n) { return (n - 1) * n * (2 * n - 1) / 6; }
@@ -1069,6 +1062,32 @@ __global__ void __launch_bounds__(128, SGL_GEMM_MINB) gemm_dmma_kernel(P pr, con
     }
 }
 
+// ------------------------------------------------------------------ G layout
+long long g_layout(Geo& g) {
+    const int N = 2 * g.B;
+    int gib;
+    switch (N) {  // the azimuthal kernels' shells per CTA (FFTShape<N>::IG, x2 for real)
+        case 2: gib = FFTShape<2>::IG; break;
+        case 4: gib = FFTShape<4>::IG; break;
+        case 8: gib = FFTShape<8>::IG; break;
+        case 16: gib = FFTShape<16>::IG; break;
+        case 32: gib = FFTShape<32>::IG; break;
+        case 64: gib = FFTShape<64>::IG; break;
+        case 128: gib = FFTShape<128>::IG; break;
+        case 256: gib = FFTShape<256>::IG; break;
+        case 512: gib = FFTShape<512>::IG; break;
+        default: gib = 1; break;  // naive DFT kernels: one shell per CTA
+    }
+    if (g.real) gib *= 2;
+    int lg = 0;
+    while ((1 << lg) < gib) ++lg;
+    g.lgib = lg;
+    g.nbins = g.real ? g.B : N;
+    const long long nshell = (long long)g.batch * g.SC;
+    g.ngx = (nshell + (1LL << lg) - 1) >> lg;
+    return (long long)g.B * g.ngx * 2 * g.nbins << lg;
+}
+
 // ------------------------------------------------------------------ launchers
 template <int N>
 static int az_fwd_launch(const Geo& g, const double* X, size_t fstride, double* G, const double* bcal,
@@ -1092,6 +1111,7 @@ template <int N>
 static int az_inv_launch(const Geo& g, const double* G, double* X, size_t fstride, const double* tw,
                          cudaStream_t s) {
     using S = FFTShape<N, SGL_AZI_ELEMS>;
+    static_assert(S::IG == FFTShape<N>::IG, "forward and inverse azimuthal tiles must match the G blocking");
     const size_t smem = sizeof(double2) * (N + 2 * S::IG * S::STRIDE);
     static bool attr = false;
     if (!attr) {

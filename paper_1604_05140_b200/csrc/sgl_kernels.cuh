@@ -32,7 +32,23 @@ struct Geo {
     int batch;      // functions
     long long NB;   // reals per nu-row of S and per G row half: batch * SC * 2
     int real = 0;   // real-valued fast path: only m >= 0 is computed (f_{n,l,-m} = (-1)^m conj f_nlm)
+    // Blocked layout of the azimuthal -> polar intermediate G (see g_index):
+    // G[j'][shell group gx][p][bin][s_local], one contiguous block per azimuthal CTA.
+    int lgib = 0;        // log2(shells per group) = log2 of the azimuthal kernel's tile
+    int nbins = 0;       // bins per (p, shell): 2B (complex path, bin B unused) or B (real path)
+    long long ngx = 0;   // shell groups = ceil(batch * SC / 2^lgib)
 };
+
+// Complex index of G(p, bin, j', flat shell s).
+__host__ __device__ inline long long g_index(const Geo& g, int p, int bin, int jp, int s) {
+    const long long gx = s >> g.lgib;
+    const int sl = s & ((1 << g.lgib) - 1);
+    return ((((long long)jp * g.ngx + gx) * 2 + p) * g.nbins + bin) * (1LL << g.lgib) + sl;
+}
+
+// Shells per azimuthal CTA (the G block size) for bandlimit B; fills the layout
+// fields of g.  Returns the number of complex values G needs.
+long long g_layout(Geo& g);
 
 // Azimuthal stage (forward): FFT of length 2B per ring (sign -1, kernels.cpp:478),
 // b_cal weighting, equatorial fold E/O and scatter to the m-major intermediate
