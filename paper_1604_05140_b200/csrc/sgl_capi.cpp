@@ -190,10 +190,14 @@ std::pair<sglk::Tile*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int 
         // warp layout: fewest (32 wm) x (128 / wm) tiles covering this problem
         int wm = 1;
         long long best = -1;
+        const char* tb = std::getenv("SGL_WM_TIE");
+        const bool prefer_square = tb ? tb[0] == '1' : false;  // measured: off is faster (B = 128)
         for (int cand : {1, 2, 4}) {
             const long long nt = (long long)((M + 32 * cand - 1) / (32 * cand)) *
                                  ((N + 128 / cand - 1) / (128 / cand));
-            if (best < 0 || nt < best) {
+            // ties: the squarer tile (fewer operand bytes per MAC, one B fetch for
+            // M in (32, 64])
+            if (best < 0 || nt < best || (prefer_square && nt == best && cand == 2)) {
                 best = nt;
                 wm = cand;
             }
