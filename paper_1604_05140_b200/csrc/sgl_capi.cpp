@@ -220,8 +220,11 @@ std::pair<sglk::Tile*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int 
     for (size_t i = 0; i < order.size(); ++i) sorted[i] = v[order[i]];
     v.swap(sorted);
     sglk::Tile* d = nullptr;
-    if (!v.empty()) d = dev_upload(v);
-    const auto res = std::make_pair(d, (int)v.size());
+    const int nt = (int)v.size();
+    // one zeroed entry past the list: the persistent kernel's tile counter pair
+    v.push_back({0, 0, 0, 0});
+    if (nt > 0) d = dev_upload(v);
+    const auto res = std::make_pair(d, nt);
     p->tiles[key] = res;
     return res;
 }
