@@ -46,7 +46,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
     target = out or LIB
     if not force and not _stale(target, deps):
         return target
-    objdir = os.path.join(PKG, "_obj")
+    # variant builds (--out=) get their own object directory so they can run in parallel
+    objdir = os.path.join(PKG, "_obj", os.path.basename(out)) if out else os.path.join(PKG, "_obj")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     common = ["-O3", "-std=c++20", "-Xcompiler", "-fPIC,-pthread", "-I", os.path.join(REPO, "include"),

@@ -612,6 +612,52 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+#ifndef SGL_MINB_RADINV
+#define SGL_MINB_RADINV 0
+#endif
+#ifndef SGL_ST_RADINV
+#define SGL_ST_RADINV 0
+#endif
+#ifndef SGL_BK_RADINV
+#define SGL_BK_RADINV 0
+#endif
+#ifndef SGL_MINB_RADFWD
+#define SGL_MINB_RADFWD 0
+#endif
+#ifndef SGL_ST_RADFWD
+#define SGL_ST_RADFWD 0
+#endif
+#ifndef SGL_BK_RADFWD
+#define SGL_BK_RADFWD 0
+#endif
+#ifndef SGL_MINB_LEGINV
+#define SGL_MINB_LEGINV 0
+#endif
+#ifndef SGL_ST_LEGINV
+#define SGL_ST_LEGINV 0
+#endif
+#ifndef SGL_BK_LEGINV
+#define SGL_BK_LEGINV 0
+#endif
+#ifndef SGL_MINB_LEGFWD
+#define SGL_MINB_LEGFWD 0
+#endif
+#ifndef SGL_ST_LEGFWD
+#define SGL_ST_LEGFWD 0
+#endif
+#ifndef SGL_BK_LEGFWD
+#define SGL_BK_LEGFWD 0
+#endif
+// Per-kind pipeline shape: k-chunk (BK), cp.async stages (ST), CTAs per SM
+// (__launch_bounds__).  Measured at B = 128 (exp/stage_times.py): BK 8 with 3
+// stages keeps more bytes in flight per CTA than BK 16 with 2 at the same
+// shared-memory footprint (4 CTAs / SM): 585 -> 565 us per round trip; LegFwd
+// runs 5 CTAs / SM (102 registers) and LegInv 4 stages (-1 us each).
+#define SGL_KIND_CFG(NAME, DBK, DST, DMINB)                  \
+    static constexpr int GEMM_BK = SGL_BK_##NAME > 0 ? SGL_BK_##NAME : DBK; \
+    static constexpr int GEMM_ST = SGL_ST_##NAME > 0 ? SGL_ST_##NAME : DST; \
+    static constexpr int GEMM_MINB = SGL_MINB_##NAME > 0 ? SGL_MINB_##NAME : DMINB;
+
 // --- problem kinds
 // Legendre forward: prob = 2|m| + p.  rows l = |m|+p+2r, K = B (j'), cols n' = sgn*NB + n.
 // Column n of a Legendre problem is (sgn, f, i_local, c) over the G chunk
@@ -638,6 +684,7 @@ __device__ __forceinline__ long long g_col(const Geo& g, int p, int am, int n) {
 __device__ __forceinline__ long long g_rowstride(const Geo& g) { return 2 * g.ngx * 2 * g.nbins << g.lgib; }
 
 struct LegFwd {
+    SGL_KIND_CFG(LEGFWD, 8, 3, 5)
     static constexpr int KIND_BIT = 1;
     Geo g;
     const double* A;        // table
@@ -674,6 +721,7 @@ struct LegFwd {
 
 // Legendre inverse: prob = 2|m| + p.  rows j' (M = B), K = #l of parity p, cols n'.
 struct LegInv {
+    SGL_KIND_CFG(LEGINV, 8, 4, 4)
     static constexpr int KIND_BIT = 2;
     Geo g;
     const double* A;
@@ -725,6 +773,7 @@ struct ShellBlocks {
 // Radial forward: prob = l.  rows n = l+1+r (M = B-l), K = 2B (i), cols (mf, c),
 // mf = f * (2l+1) + (m + l).  g.SC = sc_blk, g.NB = batch * sc_blk * 2.
 struct RadFwd {
+    SGL_KIND_CFG(RADFWD, 8, 3, 4)
     static constexpr int KIND_BIT = 4;
     Geo g;
     const double* A;        // W
@@ -774,6 +823,7 @@ struct RadFwd {
 
 // Radial inverse: prob = l.  rows i (M = 2B), K = B-l (n), cols (mf, c).
 struct RadInv {
+    SGL_KIND_CFG(RADINV, 8, 3, 4)
     static constexpr int KIND_BIT = 8;
     Geo g;
     const double* A;        // V
@@ -811,19 +861,6 @@ struct RadInv {
     __device__ bool c_affine(int, int, int) const { return false; }
 };
 
-#ifndef SGL_GEMM_STAGES
-#define SGL_GEMM_STAGES 2
-#endif
-#ifndef SGL_GEMM_MINB
-#define SGL_GEMM_MINB 4
-#endif
-#ifndef SGL_GEMM_MINB_WIDE
-#define SGL_GEMM_MINB_WIDE 3
-#endif
-#ifndef SGL_GEMM_PERSISTENT
-#define SGL_GEMM_PERSISTENT 0
-#endif
-
 __device__ __forceinline__ void cp_async8_zfill(void* smem_dst, const void* gmem_src, bool ok) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gmem_src), "r"(ok ? 8 : 0));
@@ -838,7 +875,7 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem_dst, const void* gme
 // (4 x 4 m8n8k4 fragments) arranged WM x (4/WM): the CTA tile is (32 WM) x
 // (128 / WM), chosen per tile by the host to fit the problem's M x N
 // (narrow-N radial problems use 128 x 32, wide Legendre ones 32 x 128).
-// k-chunks of 16 flow through a STAGES-deep cp.async pipeline with zero-fill
+// k-chunks of P::GEMM_BK flow through a P::GEMM_ST-deep cp.async pipeline with zero-fill
 // predication; shared-memory tiles keep the operand's contiguous dimension
 // innermost (padded) so fills and fragment loads are bank-conflict free.
 // 8-row fragments past M, 8-col fragments past N and k-steps past K are skipped.
@@ -850,7 +887,7 @@ struct has_mirror<P, std::void_t<decltype(P::MIRROR)>> : std::bool_constant<P::M
 template <class P, int WM>
 struct GemmCfg {
     static constexpr int FM = 4;
-    static constexpr int BM = 32 * WM, BN = 128 / WM, BK = kBK, ST = SGL_GEMM_STAGES;
+    static constexpr int BM = 32 * WM, BN = 128 / WM, BK = P::GEMM_BK, ST = P::GEMM_ST;
     static constexpr int LDA = P::A_KCONTIG ? BK + 4 : BM + 4;
     static constexpr int LDB = BN + 4;
     static constexpr int A_STAGE = P::A_KCONTIG ? BM * LDA : BK * LDA;
@@ -864,7 +901,7 @@ template <class P>
 constexpr size_t gemm_smem_bytes() {
     constexpr int s1 = GemmCfg<P, 1>::STAGE, s2 = GemmCfg<P, 2>::STAGE, s4 = GemmCfg<P, 4>::STAGE;
     constexpr int m = s1 > s2 ? (s1 > s4 ? s1 : s4) : (s2 > s4 ? s2 : s4);
-    return sizeof(double) * SGL_GEMM_STAGES * m;
+    return sizeof(double) * P::GEMM_ST * m;
 }
 
 // One k-chunk of MMAs for a warp with FA x NA active 8 x 8 fragments.
@@ -1071,7 +1108,7 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
 }
 
 template <class P>
-__global__ void __launch_bounds__(128, SGL_GEMM_MINB) gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles) {
+__global__ void __launch_bounds__(128, P::GEMM_MINB) gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles) {
     extern __shared__ __align__(16) double gsm[];
     const Tile t = tiles[blockIdx.x];
     switch (t.pad) {  // warp layout chosen per tile

@@ -15,10 +15,6 @@ struct Tile {
     int prob, m0, n0, pad;
 };
 
-#ifndef SGL_GEMM_BK
-#define SGL_GEMM_BK 16
-#endif
-constexpr int kBK = SGL_GEMM_BK;  // k chunk
 // The 4-warp GEMM CTA computes a (32 wm) x (128 / wm) tile, wm in {1, 2, 4}
 // chosen per tile (Tile::pad) by the host.
 constexpr int tile_rows(int wm) { return 32 * wm; }
