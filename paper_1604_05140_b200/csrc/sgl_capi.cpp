@@ -104,7 +104,7 @@ struct sglgpu_plan {
     double* d_V = nullptr;
     long long* d_V_off = nullptr;
     DevBuf G, S, in, out;
-    std::map<std::tuple<int, int, int, int, int>, std::pair<sglk::Tile*, int>> tiles;
+    std::map<std::tuple<int, int, int, int, int>, std::pair<sglk::TileMap*, int>> tiles;
     std::mutex mu;
     int last_launches = 0;
     // live per-stage timing (sglgpu_profile_begin/end)
@@ -161,70 +161,90 @@ void problem_shape(Kind kind, int B, int batch, long long NB, int pid, bool real
     }
 }
 
-// Tile list for one grouped contraction, heaviest K first, cached per shape.
-std::pair<sglk::Tile*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int SC, int lo, int hi,
-                                      bool real = false) {
+// Tile table for one grouped contraction (problems heaviest tile first), cached
+// per shape.  Each problem gets the warp layout wm with the fewest
+// (32 wm) x (128 / wm) tiles; SGL_WM_LEG / SGL_WM_RAD force one.
+std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int SC, int lo, int hi,
+                                         bool real = false) {
     const auto key = std::make_tuple((int)kind + (real ? 16 : 0), batch, SC, lo, hi);
     auto it = p->tiles.find(key);
     if (it != p->tiles.end()) return it->second;
     const int B = p->B;
     const long long NB = 2LL * batch * SC;
-    std::vector<sglk::Tile> v;
     int plo = lo, phi = hi;
-    if (kind == kLegFwd || kind == kLegInv) {
+    const bool leg = kind == kLegFwd || kind == kLegInv;
+    if (leg) {
         plo = 0;
         phi = 2 * B;
     }
-    std::vector<long long> work;  // per tile, for heaviest-first ordering
-    const char* wm_env = std::getenv(kind == kLegFwd || kind == kLegInv ? "SGL_WM_LEG" : "SGL_WM_RAD");
+    const char* wm_env = std::getenv(leg ? "SGL_WM_LEG" : "SGL_WM_RAD");
     const int wm_force = wm_env ? std::atoi(wm_env) : 0;
+    struct Entry {
+        int pid, lwm, halves, tm, tn, h0, mi0, ni0;
+        long long work;  // per tile, for heaviest-first ordering
+    };
+    std::vector<Entry> ents;
+    long long ntiles = 0;
     for (int pid = plo; pid < phi; ++pid) {
         int M, N, K;
         problem_shape(kind, B, batch, NB, pid, real, M, N, K);
         if (M <= 0 || N <= 0) continue;
         if (K <= 0 && kind != kLegInv) continue;  // LegInv with K = 0 must still write zeros
-        const bool leg = kind == kLegFwd || kind == kLegInv;
         // Legendre tiles never straddle the +m / -m halves of N (column addresses
         // stay affine inside a tile)
-        const int half = leg ? (int)NB : N;
-        // warp layout: fewest (32 wm) x (128 / wm) tiles covering this problem
-        int wm = 1;
+        const long long half = leg ? NB : N;
+        const int halves = (int)(N / half);
+        int lwm = 0;
         long long best = -1;
-        const char* tb = std::getenv("SGL_WM_TIE");
-        const bool prefer_square = tb ? tb[0] == '1' : false;  // measured: off is faster (B = 128)
-        for (int cand : {1, 2, 4}) {
-            const long long nt = (long long)((M + 32 * cand - 1) / (32 * cand)) *
-                                 ((N + 128 / cand - 1) / (128 / cand));
-            // ties: the squarer tile (fewer operand bytes per MAC, one B fetch for
-            // M in (32, 64])
-            if (best < 0 || nt < best || (prefer_square && nt == best && cand == 2)) {
+        for (int l2 = 0; l2 < 3; ++l2) {
+            const long long nt = (long long)((M + (32 << l2) - 1) / (32 << l2)) * ((half + (128 >> l2) - 1) / (128 >> l2));
+            if (best < 0 || nt < best) {
                 best = nt;
-                wm = cand;
+                lwm = l2;
             }
         }
-        if (wm_force == 1 || wm_force == 2 || wm_force == 4) wm = wm_force;
-        const int bm = sglk::tile_rows(wm), bn = sglk::tile_cols(wm);
-        for (int m0 = 0; m0 < M; m0 += bm)
-            for (int h0 = 0; h0 < N; h0 += half)
-                for (int n0 = h0; n0 < std::min(N, h0 + half); n0 += bn) {
-                    v.push_back({pid, m0, n0, wm});
-                    const long long rows = (std::min(bm, M - m0) + 7) / 8 * 8;
-                    const long long cols = (std::min(bn, std::min(N, h0 + half) - n0) + 7) / 8 * 8;
-                    work.push_back(rows * cols * std::max(K, 1));
-                }
+        if (wm_force == 1 || wm_force == 2 || wm_force == 4) lwm = wm_force == 1 ? 0 : wm_force == 2 ? 1 : 2;
+        const int bm = 32 << lwm, bn = 128 >> lwm;
+        const int tm = (M + bm - 1) / bm;
+        const long long tn = (half + bn - 1) / bn;
+        if (tn > (1 << 30) / 2) fail(SGLGPU_EINVAL, "tile table: problem too wide");
+        const long long kk = std::max(K, 1);
+        ents.push_back({pid, lwm, halves, tm, (int)tn, 0, 0, 0,
+                        (std::min(bm, M) + 7) / 8 * 8 * ((std::min<long long>(bn, half) + 7) / 8 * 8) * kk});
+        ntiles += (long long)tm * halves * tn;
     }
-    std::vector<size_t> order(v.size());
-    for (size_t i = 0; i < order.size(); ++i) order[i] = i;
-    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return work[a] > work[b]; });
-    std::vector<sglk::Tile> sorted(v.size());
-    for (size_t i = 0; i < order.size(); ++i) sorted[i] = v[order[i]];
-    v.swap(sorted);
-    sglk::Tile* d = nullptr;
-    const int nt = (int)v.size();
-    // one zeroed entry past the list: the persistent kernel's tile counter pair
-    v.push_back({0, 0, 0, 0});
-    if (nt > 0) d = dev_upload(v);
-    const auto res = std::make_pair(d, nt);
+    if (ntiles <= sglk::kMaxProblems) {  // one entry per tile, exact per-tile work
+        std::vector<Entry> per;
+        for (const Entry& e : ents) {
+            int M, N, K;
+            problem_shape(kind, B, batch, NB, e.pid, real, M, N, K);
+            const long long half = leg ? NB : N, kk = std::max(K, 1);
+            const int bm = 32 << e.lwm, bn = 128 >> e.lwm;
+            for (int mi = 0; mi < e.tm; ++mi)
+                for (int h = 0; h < e.halves; ++h)
+                    for (int ni = 0; ni < e.tn; ++ni) {
+                        const long long rows = std::min(bm, M - mi * bm), cols = std::min<long long>(bn, half - (long long)ni * bn);
+                        per.push_back({e.pid, e.lwm, 1, 1, 1, h, mi, ni, (rows + 7) / 8 * 8 * ((cols + 7) / 8 * 8) * kk});
+                    }
+        }
+        ents.swap(per);
+    }
+    if ((int)ents.size() > sglk::kMaxProblems) fail(SGLGPU_EINVAL, "tile table: too many problems");
+    std::stable_sort(ents.begin(), ents.end(), [](const Entry& a, const Entry& b) { return a.work > b.work; });
+    auto* tm = new sglk::TileMap{};
+    long long n = 0;
+    tm->nprob = (int)ents.size();
+    for (size_t q = 0; q < ents.size(); ++q) {
+        const Entry& e = ents[q];
+        tm->first[q] = (int)n;
+        tm->info[q] = e.pid | e.lwm << 16 | (e.halves - 1) << 18 | e.h0 << 19 | e.mi0 << 20;
+        tm->tn[q] = e.tn;
+        tm->ni0[q] = e.ni0;
+        n += (long long)e.tm * e.halves * e.tn;
+    }
+    if (n >= (1LL << 31) - 1) fail(SGLGPU_EINVAL, "tile table: too many tiles");
+    tm->first[ents.size()] = (int)n;
+    const auto res = std::make_pair(tm, (int)n);
     p->tiles[key] = res;
     return res;
 }
@@ -813,8 +833,7 @@ int sglgpu_plan_destroy(sglgpu_plan* p) {
     for (void* q : {(void*)p->d_tw, (void*)p->d_bcal, (void*)p->d_leg, (void*)p->d_leg_off, (void*)p->d_W,
                     (void*)p->d_W_off, (void*)p->d_V, (void*)p->d_V_off})
         if (q) cudaFree(q);
-    for (auto& kv : p->tiles)
-        if (kv.second.first) cudaFree(kv.second.first);
+    for (auto& kv : p->tiles) delete kv.second.first;
     for (auto& [stage, a, b] : p->prof) {
         cudaEventDestroy(a);
         cudaEventDestroy(b);

@@ -604,7 +604,7 @@ __global__ void az_inverse_naive_kernel(Geo g, const double2* __restrict__ G, do
 // ------------------------------------------------------------------ grouped DMMA GEMM
 // C[row][col] = sum_k A[row][k] * Bm[k][col], addresses separable:
 //   A:  A + rowA(row) + colA(k)        Bm: Bm + rowB(k) + colB(col)
-//   C:  C + rowC(row) + colC(col), value scaled by scaleC(col)
+//   C:  C + rowC(row) + colC(col), value negated where negC(col)
 // cols come in (re, im) pairs that are adjacent in memory for Bm and C.
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -685,7 +685,6 @@ __device__ __forceinline__ long long g_rowstride(const Geo& g) { return 2 * g.ng
 
 struct LegFwd {
     SGL_KIND_CFG(LEGFWD, 8, 3, 5)
-    static constexpr int KIND_BIT = 1;
     Geo g;
     const double* A;        // table
     const long long* aoff;  // per prob
@@ -713,7 +712,7 @@ struct LegFwd {
         return l * (l + 1) * sv.NB;
     }
     __device__ long long colC(int pid, int n) const { return s_col(g, sv, am(pid), n); }
-    __device__ double scaleC(int pid, int n) const { return (n >= g.NB && (am(pid) & 1)) ? -1.0 : 1.0; }
+    __device__ bool negC(int pid, int n) const { return n >= g.NB && (am(pid) & 1); }
     // tiles start at multiples of bn inside a sign half; no function boundary inside
     // the tile when bn divides the per-function width 2 SC
     __device__ bool c_affine(int, int, int bn) const { return (2 * g.SC) % bn == 0; }
@@ -722,7 +721,6 @@ struct LegFwd {
 // Legendre inverse: prob = 2|m| + p.  rows j' (M = B), K = #l of parity p, cols n'.
 struct LegInv {
     SGL_KIND_CFG(LEGINV, 8, 4, 4)
-    static constexpr int KIND_BIT = 2;
     Geo g;
     const double* A;
     const long long* aoff;
@@ -749,7 +747,7 @@ struct LegInv {
     __device__ long long colB(int pid, int n) const { return s_col(g, sv, am(pid), n); }
     __device__ long long rowC(int, int j) const { return (long long)j * g_rowstride(g); }
     __device__ long long colC(int pid, int n) const { return g_col(g, pid & 1, am(pid), n); }
-    __device__ double scaleC(int pid, int n) const { return (n >= g.NB && (am(pid) & 1)) ? -1.0 : 1.0; }
+    __device__ bool negC(int pid, int n) const { return n >= g.NB && (am(pid) & 1); }
     __device__ bool c_affine(int, int, int) const { return false; }  // blocked G: per-column offsets
 };
 
@@ -774,7 +772,6 @@ struct ShellBlocks {
 // mf = f * (2l+1) + (m + l).  g.SC = sc_blk, g.NB = batch * sc_blk * 2.
 struct RadFwd {
     SGL_KIND_CFG(RADFWD, 8, 3, 4)
-    static constexpr int KIND_BIT = 4;
     Geo g;
     const double* A;        // W
     const long long* aoff;
@@ -807,16 +804,16 @@ struct RadFwd {
         const int f = mf / w, mm = mf - f * w + (g.real ? l : 0);
         return (long long)f * 2 * omega + 2LL * ((long long)l * l + mm) + (n & 1);
     }
-    __device__ double scaleC(int, int) const { return 1.0; }
+    __device__ bool negC(int, int) const { return false; }
     __device__ bool c_affine(int, int, int) const { return false; }
     // real-valued path: every m > 0 coefficient also lands at -m as (-1)^m conj
     static constexpr bool MIRROR = true;
-    __device__ long long colC_mirror(int l, int n, double& sign) const {
+    __device__ long long colC_mirror(int l, int n, bool& neg) const {
         if (!g.real) return -1;
         const int mf = n >> 1, w = mw(l);
         const int f = mf / w, m = mf - f * w;
         if (m == 0) return -1;
-        sign = (m & 1) ? -1.0 : 1.0;
+        neg = m & 1;
         return (long long)f * 2 * omega + 2LL * ((long long)l * l + l - m) + (n & 1);
     }
 };
@@ -824,7 +821,6 @@ struct RadFwd {
 // Radial inverse: prob = l.  rows i (M = 2B), K = B-l (n), cols (mf, c).
 struct RadInv {
     SGL_KIND_CFG(RADINV, 8, 3, 4)
-    static constexpr int KIND_BIT = 8;
     Geo g;
     const double* A;        // V
     const long long* aoff;
@@ -857,7 +853,7 @@ struct RadInv {
         const int f = mf / w, mm = mf - f * w + (g.real ? l : 0);
         return ((long long)l * l + mm - sb.nu0) * g.NB + (long long)f * 2 * g.SC + (n & 1);
     }
-    __device__ double scaleC(int, int) const { return 1.0; }
+    __device__ bool negC(int, int) const { return false; }
     __device__ bool c_affine(int, int, int) const { return false; }
 };
 
@@ -950,8 +946,10 @@ __device__ __forceinline__ void gemm_epilogue(const P& pr, int pid, int m0, int 
                                               const double (&acc)[4][4][2], int wr, int wc, int lane) {
     using C = GemmCfg<P, WM>;
     constexpr int BN = C::BN, FM = C::FM;
+    // signs are applied as sign-bit flips (a DMUL would compete with the DMMAs
+    // for the FP64 pipe)
     long long cofs[4];
-    double csc[4];
+    unsigned long long csg[4];
     const bool caff = pr.c_affine(pid, n0, BN);
     const long long cbase = caff ? pr.colC(pid, n0) : 0;
 #pragma unroll
@@ -959,8 +957,9 @@ __device__ __forceinline__ void gemm_epilogue(const P& pr, int pid, int m0, int 
         const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
         const bool ok = col < N;
         cofs[fn] = ok ? (caff ? cbase + (col - n0) : pr.colC(pid, col)) : 0;
-        csc[fn] = ok ? pr.scaleC(pid, col) : 0.0;
+        csg[fn] = ok && pr.negC(pid, col) ? 0x8000000000000000ULL : 0ULL;
     }
+    auto flip = [](double v, unsigned long long m) { return __longlong_as_double(__double_as_longlong(v) ^ m); };
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm) {
         const int row = m0 + wr + fm * 8 + (lane >> 2);
@@ -970,12 +969,15 @@ __device__ __forceinline__ void gemm_epilogue(const P& pr, int pid, int m0, int 
         for (int fn = 0; fn < 4; ++fn) {
             const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
             if (col >= N) continue;
-            *reinterpret_cast<double2*>(out + cofs[fn]) = make_double2(csc[fn] * acc[fm][fn][0], csc[fn] * acc[fm][fn][1]);
+            *reinterpret_cast<double2*>(out + cofs[fn]) =
+                make_double2(flip(acc[fm][fn][0], csg[fn]), flip(acc[fm][fn][1], csg[fn]));
             if constexpr (has_mirror<P>::value) {
-                double sg = 1.0;
-                const long long mo = pr.colC_mirror(pid, col, sg);
-                if (mo >= 0)
-                    *reinterpret_cast<double2*>(out + mo) = make_double2(sg * acc[fm][fn][0], -sg * acc[fm][fn][1]);
+                bool neg = false;
+                const long long mo = pr.colC_mirror(pid, col, neg);
+                const unsigned long long ms = neg ? 0x8000000000000000ULL : 0ULL;
+                if (mo >= 0)  // (-1)^m conj
+                    *reinterpret_cast<double2*>(out + mo) =
+                        make_double2(flip(acc[fm][fn][0], ms), flip(acc[fm][fn][1], ms ^ 0x8000000000000000ULL));
             }
         }
     }
@@ -1107,267 +1109,33 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
     gemm_epilogue<P, WM>(pr, pid, m0, n0, M, N, acc, wr, wc, lane);
 }
 
+// Tile of this CTA from the launch's problem table (kernel parameter space: a
+// handful of constant-cache reads instead of a dependent global load at CTA start).
+__device__ __forceinline__ Tile decode_tile(const TileMap& tm, long long NB) {
+    const int b = blockIdx.x;
+    int lo = 0, hi = tm.nprob - 1;  // last entry with first[q] <= b
+    if (tm.first[tm.nprob] == tm.nprob) lo = hi = b;  // one entry per tile
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tm.first[mid] <= b) lo = mid;
+        else hi = mid - 1;
+    }
+    const int info = tm.info[lo], tn = tm.tn[lo], local = b - tm.first[lo];
+    const int lwm = (info >> 16) & 3, halves = ((info >> 18) & 1) + 1;
+    const int per_m = halves * tn;
+    const int mi = local / per_m, rest = local - mi * per_m;
+    const int hl = rest / tn, ni = rest - hl * tn + tm.ni0[lo], h = hl + ((info >> 19) & 1);
+    return Tile{info & 0xffff, (mi + (info >> 20)) * (32 << lwm), (int)(h * NB) + ni * (128 >> lwm), 1 << lwm};
+}
+
 template <class P>
-__global__ void __launch_bounds__(128, P::GEMM_MINB) gemm_dmma_kernel(P pr, const Tile* __restrict__ tiles) {
+__global__ void __launch_bounds__(128, P::GEMM_MINB) gemm_dmma_kernel(P pr, const __grid_constant__ TileMap tm) {
     extern __shared__ __align__(16) double gsm[];
-    const Tile t = tiles[blockIdx.x];
+    const Tile t = decode_tile(tm, pr.g.NB);
     switch (t.pad) {  // warp layout chosen per tile
         case 1: gemm_tile<P, 1>(pr, t, gsm); break;
         case 2: gemm_tile<P, 2>(pr, t, gsm); break;
         default: gemm_tile<P, 4>(pr, t, gsm); break;
-    }
-}
-
-// ------------------------------------------------------------------ warp-specialized grouped GEMM
-// Persistent variant of gemm_dmma_kernel: each CTA is 4 MMA warps (the same
-// (32 WM) x (128 / WM) tiles and fragment code) plus one producer warp that
-// streams the k-chunks of successive tiles through an SGL_WS_ST-deep shared
-// memory ring with cp.async, tracked by mbarriers (full: 32 cp.async arrivals
-// + 1 header arrival; empty: one arrival per MMA warp).  Tiles come from a
-// self-resetting global counter in heaviest-first order, so the producer
-// prefetches the next tile while the MMA warps run the previous epilogue, and
-// the MMA warps never wait at a CTA barrier or issue a load.
-#ifndef SGL_WS_ST
-#define SGL_WS_ST 3
-#endif
-#ifndef SGL_WS_MINB
-#define SGL_WS_MINB 3
-#endif
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
-    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
-        "r"(parity)
-        : "memory");
-}
-// arrive on b once all cp.async issued so far by this thread have landed
-__device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* b) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
-}
-
-template <class P>
-__host__ __device__ constexpr int ws_stage_doubles() {
-    constexpr int s1 = GemmCfg<P, 1>::STAGE, s2 = GemmCfg<P, 2>::STAGE, s4 = GemmCfg<P, 4>::STAGE;
-    constexpr int m = s1 > s2 ? (s1 > s4 ? s1 : s4) : (s2 > s4 ? s2 : s4);
-    return (m + 1) & ~1;  // keep stages 16-byte aligned
-}
-constexpr int kWsMaxPairs = 64;  // column pairs of the widest tile (BN = 128)
-
-template <class P>
-constexpr size_t ws_smem_bytes() {
-    return sizeof(double) * SGL_WS_ST * ws_stage_doubles<P>() + 2 * SGL_WS_ST * sizeof(unsigned long long) +
-           kWsMaxPairs * sizeof(long long) + 16 * sizeof(int);
-}
-
-struct WsRing {
-    double* buf;
-    unsigned long long* full;
-    unsigned long long* empty;
-    long long* coff;  // producer-private: B column offsets of the current tile
-    int* hdr;         // tile index published with the first chunk of a tile (-1: done)
-};
-
-// Producer: rolled transfer loops (compact code -- the MMA warps' straight-line
-// chunks already fill the instruction cache), 16-byte A transfers where the
-// table rows are 16-byte aligned.  Operand rows past M / columns past N are not
-// fetched (they only feed outputs that are never stored); k past K is zero-filled.
-template <class P, int WM>
-__device__ __forceinline__ void ws_produce(const P& pr, const Tile& t, int ti, const WsRing& r, unsigned& it,
-                                           int lane) {
-    using C = GemmCfg<P, WM>;
-    constexpr int BM = C::BM, BN = C::BN, BK = C::BK, ST = SGL_WS_ST, SD = ws_stage_doubles<P>();
-    constexpr int NP = BN / 2;  // column pairs
-    const int pid = t.prob, m0 = t.m0, n0 = t.n0;
-    const int M = pr.M(pid), N = pr.nlim(pid, n0), K = pr.K(pid);
-    const int nch = K > 0 ? (K + BK - 1) / BK : 1;
-    const int rows = min(BM, M - m0), npair = min(NP, (N - n0 + 1) >> 1);
-    const long long bcol0 = P::B_COL_AFFINE ? pr.colB(pid, n0) : 0;
-    // (column offsets may be negative: -m rows of S lie below the m = 0 row)
-    for (int q = lane; q < npair; q += 32) r.coff[q] = P::B_COL_AFFINE ? bcol0 + 2 * q : pr.colB(pid, n0 + 2 * q);
-    __syncwarp();
-    const long long b_step = pr.b_kstep(pid);  // > 0: rowB affine in k
-    const long long b_row0 = b_step > 0 ? pr.rowB(pid, 0) : 0;
-    const long long arow0 = pr.rowA(pid, m0);
-    const double* abase = pr.A + arow0;
-    const long long a_sr = pr.a_sr(pid), a_sk = pr.a_sk(pid);
-    // 16-byte A transfers: pairs along the operand's contiguous dimension
-    const bool avec = P::A_KCONTIG ? ((arow0 | a_sr) & 1) == 0 : ((arow0 | a_sk) & 1) == 0;
-    for (int c = 0; c < nch; ++c, ++it) {
-        const int s = it % ST;
-        mbar_wait(&r.empty[s], ((it / ST) & 1) ^ 1);
-        double* as = r.buf + s * SD;
-        double* bs = as + C::A_STAGE;
-        const int k0 = c * BK, kn = min(BK, K - k0);  // valid k in this chunk
-        if (P::A_KCONTIG) {
-            if (avec) {  // units (row, k pair): BK/2 per row
-                constexpr int UPR = BK / 2;
-#pragma unroll 4
-                for (int e = lane; e < rows * UPR; e += 32) {
-                    const int row = e / UPR, k = 2 * (e % UPR);
-                    const int nb = k < kn ? (k + 1 < kn ? 16 : 8) : 0;
-                    const double* src = nb ? abase + row * a_sr + (k0 + k) : pr.A;
-                    const unsigned d = smem_u32(as + row * C::LDA + k);
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(nb));
-                }
-            } else {
-#pragma unroll 4
-                for (int e = lane; e < rows * BK; e += 32) {
-                    const int row = e / BK, k = e % BK;
-                    const bool ok = k < kn;
-                    cp_async8_zfill(as + row * C::LDA + k, ok ? abase + row * a_sr + (k0 + k) * a_sk : pr.A, ok);
-                }
-            }
-        } else {
-            if (avec) {  // units (row pair, k)
-                constexpr int UPK = BM / 2;
-                const int rp = (rows + 1) >> 1;
-#pragma unroll 4
-                for (int e = lane; e < rp * BK; e += 32) {
-                    const int row = 2 * (e % rp), k = e / rp;
-                    const bool ok = k < kn;
-                    const double* src = ok ? abase + row + (k0 + k) * a_sk : pr.A;
-                    const unsigned d = smem_u32(as + k * C::LDA + row);
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 16 : 0));
-                }
-                (void)UPK;
-            } else {
-#pragma unroll 4
-                for (int e = lane; e < rows * BK; e += 32) {
-                    const int row = e % rows, k = e / rows;
-                    const bool ok = k < kn;
-                    cp_async8_zfill(as + k * C::LDA + row, ok ? abase + row * a_sr + (k0 + k) * a_sk : pr.A, ok);
-                }
-            }
-        }
-        if (P::B_KCONTIG) {  // lanes along k: units (pair, k), BK per pair
-#pragma unroll 4
-            for (int e = lane; e < npair * BK; e += 32) {
-                const int pc = e / BK, k = e % BK;
-                const bool ok = k < kn;
-                const long long ro = b_step > 0 ? b_row0 + (long long)(k0 + k) * b_step : pr.rowB(pid, k0 + k);
-                cp_async16_zfill(bs + k * C::LDB + 2 * pc, ok ? pr.Bm + r.coff[pc] + ro : pr.Bm, ok);
-            }
-        } else {  // lanes along columns: units (k, pair)
-#pragma unroll 4
-            for (int e = lane; e < npair * BK; e += 32) {
-                const int k = e / npair, pc = e - k * npair;
-                const bool ok = k < kn;
-                const long long ro = b_step > 0 ? b_row0 + (long long)(k0 + k) * b_step : pr.rowB(pid, k0 + k);
-                cp_async16_zfill(bs + k * C::LDB + 2 * pc, ok ? pr.Bm + r.coff[pc] + ro : pr.Bm, ok);
-            }
-        }
-        if (c == 0 && lane == 0) r.hdr[s] = ti;
-        cp_async_mbar_arrive(&r.full[s]);
-        if (lane == 0) mbar_arrive(&r.full[s]);
-    }
-}
-
-template <class P, int WM>
-__device__ __forceinline__ void ws_consume(const P& pr, const Tile& t, const WsRing& r, unsigned& it, int warp,
-                                           int lane) {
-    using C = GemmCfg<P, WM>;
-    constexpr int BK = C::BK, ST = SGL_WS_ST, SD = ws_stage_doubles<P>(), FM = C::FM;
-    const int wr = (warp % WM) * 32, wc = (warp / WM) * 32;
-    const int pid = t.prob, m0 = t.m0, n0 = t.n0;
-    const int M = pr.M(pid), N = pr.nlim(pid, n0), K = pr.K(pid);
-    const int nch = K > 0 ? (K + BK - 1) / BK : 1;
-    const int fm_active = max(0, min(FM, (M - m0 - wr + 7) >> 3));
-    const int fn_active = max(0, min(4, (N - n0 - wc + 7) >> 3));
-    double acc[FM][4][2];
-#pragma unroll
-    for (int i = 0; i < FM; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    for (int c = 0; c < nch; ++c, ++it) {
-        const int s = it % ST;
-        mbar_wait(&r.full[s], (it / ST) & 1);
-        const double* as = r.buf + s * SD;
-        const double* bs = as + C::A_STAGE;
-        const int ksteps = min(BK, K - c * BK);
-        if (ksteps == BK) {
-            dispatch_chunk<P, WM, true>(fm_active, fn_active, as, bs, acc, BK, wr, wc, lane);
-        } else {
-            dispatch_chunk<P, WM, false>(fm_active, fn_active, as, bs, acc, ksteps, wr, wc, lane);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&r.empty[s]);
-    }
-    gemm_epilogue<P, WM>(pr, pid, m0, n0, M, N, acc, wr, wc, lane);
-}
-
-template <class P>
-__global__ void __launch_bounds__(160, SGL_WS_MINB)
-    gemm_ws_kernel(P pr, const Tile* __restrict__ tiles, int ntiles, int* sched) {
-    extern __shared__ __align__(16) double gsm[];
-    constexpr int ST = SGL_WS_ST, SD = ws_stage_doubles<P>();
-    WsRing r;
-    r.buf = gsm;
-    r.full = reinterpret_cast<unsigned long long*>(gsm + ST * SD);
-    r.empty = r.full + ST;
-    r.coff = reinterpret_cast<long long*>(r.empty + ST);
-    r.hdr = reinterpret_cast<int*>(r.coff + kWsMaxPairs);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < ST; ++s) {
-            mbar_init(&r.full[s], 33);
-            mbar_init(&r.empty[s], 4);
-        }
-    }
-    __syncthreads();
-    unsigned it = 0;
-    if (warp == 4) {  // producer
-        for (;;) {
-            int ti = 0;
-            if (lane == 0) {
-                ti = atomicAdd(sched, 1);
-                // the last CTA to run out of tiles re-arms the counter for the next launch
-                if (ti >= ntiles && atomicAdd(sched + 1, 1) == (int)gridDim.x - 1) {
-                    atomicExch(sched, 0);
-                    atomicExch(sched + 1, 0);
-                }
-            }
-            ti = __shfl_sync(0xffffffffu, ti, 0);
-            if (ti >= ntiles) {
-                const int s = it % ST;
-                mbar_wait(&r.empty[s], ((it / ST) & 1) ^ 1);
-                if (lane == 0) r.hdr[s] = -1;
-                cp_async_mbar_arrive(&r.full[s]);
-                if (lane == 0) mbar_arrive(&r.full[s]);
-                break;
-            }
-            const Tile t = tiles[ti];
-            switch (t.pad) {
-                case 1: ws_produce<P, 1>(pr, t, ti, r, it, lane); break;
-                case 2: ws_produce<P, 2>(pr, t, ti, r, it, lane); break;
-                default: ws_produce<P, 4>(pr, t, ti, r, it, lane); break;
-            }
-        }
-        cp_async_wait_group<0>();
-    } else {
-        for (;;) {
-            const int s = it % ST;
-            mbar_wait(&r.full[s], (it / ST) & 1);
-            const int ti = r.hdr[s];
-            if (ti < 0) break;
-            const Tile t = tiles[ti];
-            switch (t.pad) {
-                case 1: ws_consume<P, 1>(pr, t, r, it, warp, lane); break;
-                case 2: ws_consume<P, 2>(pr, t, r, it, warp, lane); break;
-                default: ws_consume<P, 4>(pr, t, r, it, warp, lane); break;
-            }
-        }
     }
 }
 
@@ -1480,73 +1248,40 @@ int launch_az_inverse(const Geo& g, const double* G, double* samples, size_t sam
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-// SGL_GEMM_WS=1 selects the warp-specialized persistent kernel.  Its tile
-// scheduler counter is the zeroed int pair stored right after the tile list
-// (tiles_for in sgl_capi.cpp); launches sharing a tile list must be stream-ordered.
-// SGL_GEMM_WS_MASK (bits: 1 LegFwd, 2 LegInv, 4 RadFwd, 8 RadInv) narrows it.
-static bool gemm_ws_enabled(int kind_bit) {
-    static const int mask = [] {
-        const char* e = std::getenv("SGL_GEMM_WS");
-        if (!(e && e[0] == '1')) return 0;
-        const char* m = std::getenv("SGL_GEMM_WS_MASK");
-        return m ? std::atoi(m) : 15;
-    }();
-    return (mask & kind_bit) != 0;
-}
-
 template <class P>
-static int gemm_ws_launch(const P& p, const Tile* tiles, int ntiles, cudaStream_t s) {
-    constexpr size_t smem = ws_smem_bytes<P>();
-    static int per_sm = 0, nsm = 0;
-    if (!per_sm) {
-        cudaFuncSetAttribute(gemm_ws_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_ws_kernel<P>, 160, smem);
-        if (per_sm < 1) per_sm = 1;
-    }
-    const int grid = std::min(ntiles, per_sm * nsm);
-    int* sched = reinterpret_cast<int*>(const_cast<Tile*>(tiles) + ntiles);
-    gemm_ws_kernel<P><<<grid, 160, smem, s>>>(p, tiles, ntiles, sched);
-    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
-}
-
-template <class P>
-static int gemm_launch(const P& p, const Tile* tiles, int ntiles, cudaStream_t s) {
+static int gemm_launch(const P& p, const TileMap* tiles, int ntiles, cudaStream_t s) {
     if (ntiles <= 0) return 0;
-    if (gemm_ws_enabled(P::KIND_BIT)) return gemm_ws_launch<P>(p, tiles, ntiles, s);
     constexpr size_t smem = gemm_smem_bytes<P>();
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(gemm_dmma_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    gemm_dmma_kernel<P><<<ntiles, 128, smem, s>>>(p, tiles);
+    gemm_dmma_kernel<P><<<ntiles, 128, smem, s>>>(p, *tiles);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 int launch_legendre_forward(const Geo& g, const SView& sv, const double* G, double* S, const double* tab,
-                            const long long* tab_off, const Tile* tiles, int ntiles, cudaStream_t s) {
+                            const long long* tab_off, const TileMap* tiles, int ntiles, cudaStream_t s) {
     LegFwd p{g, tab, tab_off, G, S, sv};
     return gemm_launch<LegFwd>(p, tiles, ntiles, s);
 }
 
 int launch_legendre_inverse(const Geo& g, const SView& sv, const double* S, double* G, const double* tab,
-                            const long long* tab_off, const Tile* tiles, int ntiles, cudaStream_t s) {
+                            const long long* tab_off, const TileMap* tiles, int ntiles, cudaStream_t s) {
     LegInv p{g, tab, tab_off, S, G, sv};
     return gemm_launch<LegInv>(p, tiles, ntiles, s);
 }
 
 int launch_radial_forward(const Geo& g, const RadialBlocks& rb, const double* S, double* C,
-                          const double* W, const long long* w_off, const Tile* tiles, int ntiles,
+                          const double* W, const long long* w_off, const TileMap* tiles, int ntiles,
                           cudaStream_t s) {
     RadFwd p{g, W, w_off, S, C, degree_offset(g.B + 1), ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
     return gemm_launch<RadFwd>(p, tiles, ntiles, s);
 }
 
 int launch_radial_inverse(const Geo& g, const RadialBlocks& rb, const double* C, double* S,
-                          const double* V, const long long* v_off, const Tile* tiles, int ntiles,
+                          const double* V, const long long* v_off, const TileMap* tiles, int ntiles,
                           cudaStream_t s) {
     RadInv p{g, V, v_off, C, S, degree_offset(g.B + 1), ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
     return gemm_launch<RadInv>(p, tiles, ntiles, s);

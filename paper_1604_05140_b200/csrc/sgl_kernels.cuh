@@ -15,6 +15,26 @@ struct Tile {
     int prob, m0, n0, pad;
 };
 
+// Tiles of one grouped contraction, passed by value in kernel parameter space.
+// Entry q is a block of tiles of one problem, listed heaviest tile first; it owns
+// tiles [first[q], first[q + 1]), enumerated m-block major (from m-block mi0),
+// then sign half (from h0; Legendre problems with m != 0 split N into the +m / -m
+// halves of NB columns), then n-block (from n-block ni0).  Launches of at most
+// kMaxProblems tiles get one entry per tile (a global heaviest-first order),
+// larger ones one entry per problem (sibling tiles, which share an operand,
+// run back to back).
+#ifndef SGL_MAX_PROBLEMS
+#define SGL_MAX_PROBLEMS 1024
+#endif
+constexpr int kMaxProblems = SGL_MAX_PROBLEMS;
+struct TileMap {
+    int nprob;
+    int first[kMaxProblems + 1];
+    int info[kMaxProblems];  // pid | log2(wm) << 16 | (halves - 1) << 18 | h0 << 19 | mi0 << 20
+    int tn[kMaxProblems];    // n-blocks per half
+    int ni0[kMaxProblems];
+};
+
 // The 4-warp GEMM CTA computes a (32 wm) x (128 / wm) tile, wm in {1, 2, 4}
 // chosen per tile (Tile::pad) by the host.
 constexpr int tile_rows(int wm) { return 32 * wm; }
@@ -74,10 +94,10 @@ struct SView {
 // Polar stage: per (|m|, parity) DMMA contraction against the normalized
 // Legendre table.  tab: rows Pbar_{l,|m|}(cos theta_j'), j' < B.
 int launch_legendre_forward(const Geo& g, const SView& sv, const double* G, double* S, const double* tab,
-                            const long long* tab_off, const Tile* tiles, int ntiles,
+                            const long long* tab_off, const TileMap* tiles, int ntiles,
                             cudaStream_t s);
 int launch_legendre_inverse(const Geo& g, const SView& sv, const double* S, double* G, const double* tab,
-                            const long long* tab_off, const Tile* tiles, int ntiles,
+                            const long long* tab_off, const TileMap* tiles, int ntiles,
                             cudaStream_t s);
 
 // Radial stage: per l DMMA contraction against W_l (forward) / V_l (inverse).
@@ -89,10 +109,10 @@ struct RadialBlocks {
     long long nu0;
 };
 int launch_radial_forward(const Geo& g, const RadialBlocks& rb, const double* S, double* C,
-                          const double* W, const long long* w_off, const Tile* tiles, int ntiles,
+                          const double* W, const long long* w_off, const TileMap* tiles, int ntiles,
                           cudaStream_t s);
 int launch_radial_inverse(const Geo& g, const RadialBlocks& rb, const double* C, double* S,
-                          const double* V, const long long* v_off, const Tile* tiles, int ntiles,
+                          const double* V, const long long* v_off, const TileMap* tiles, int ntiles,
                           cudaStream_t s);
 
 }  // namespace sglk
