@@ -194,9 +194,12 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
         // stay affine inside a tile)
         const long long half = leg ? NB : N;
         const int halves = (int)(N / half);
+        // ties: the widest tile, except for the radial inverse (M = 2B rows of
+        // V_l against a few coefficient columns), where 128 x 32 measured faster
         int lwm = 0;
         long long best = -1;
-        for (int l2 = 0; l2 < 3; ++l2) {
+        for (int c = 0; c < 3; ++c) {
+            const int l2 = kind == kRadInv ? 2 - c : c;
             const long long nt = (long long)((M + (32 << l2) - 1) / (32 << l2)) * ((half + (128 >> l2) - 1) / (128 >> l2));
             if (best < 0 || nt < best) {
                 best = nt;
