@@ -266,15 +266,16 @@ def main():
         cin = torch.from_numpy(complex_normal(rng, (nrot, nb, Om))).cuda()
     grid = torch.empty((nb, Ps), dtype=torch.float64 if args.real else torch.complex128, device="cuda")
     cout = torch.empty((nb, Om), dtype=torch.complex128, device="cuda")
-    # a dedicated (non-default) stream: the library replays CUDA graphs of small,
-    # launch-bound transforms on it
+    # a dedicated (non-default) stream: the library replays CUDA graphs of
+    # transforms up to 2 x 128^3 samples on it
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    # Live per-stage CUDA events need eager launches; small transforms run as
-    # CUDA-graph replays, so for them the stage times come from a second,
-    # profiled pass over the same steps (noted in the output).
-    graphs = (B ** 3) * nb <= 4 * 64 ** 3
-    live_profile = not graphs
+    # The headline pass runs without per-stage events (an event record between
+    # kernels costs ~5 us of GPU time each, ~30 us per B = 128 round trip, and
+    # disables graph replay); the stage times and the roofline come from a second
+    # timed pass over the same steps with CUDA events around every stage launch.
+    graphs = (B ** 3) * nb <= 2 * 128 ** 3
+    live_profile = False
 
     inv = sgl.ifsglft_real_batch if args.real else sgl.ifsglft_batch
     fwd = sgl.fsglft_real_batch if args.real else sgl.fsglft_batch
@@ -391,7 +392,8 @@ def main():
     except (OSError, KeyError, ValueError):
         pass
     roof["timing"] = ("live: CUDA events around each stage launch inside the timed region" if live_profile else
-                      "separate profiled pass (eager launches) after the CUDA-graph timed region")
+                      "live: CUDA events around each stage launch (eager launches) in a second timed pass of "
+                      "the same steps, right after the headline pass")
     whole = 2 * wl.f_fwd(B) * nb / (ms * 1e-3) / 1e12
 
     line = {
