@@ -207,6 +207,9 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
             }
         }
         if (wm_force == 1 || wm_force == 2 || wm_force == 4) lwm = wm_force == 1 ? 0 : wm_force == 2 ? 1 : 2;
+        const int max_wm = kind == kLegFwd ? SGL_MAXWM_LEGFWD : kind == kLegInv ? SGL_MAXWM_LEGINV
+                         : kind == kRadFwd ? SGL_MAXWM_RADFWD : SGL_MAXWM_RADINV;
+        while ((1 << lwm) > max_wm) --lwm;
         const int bm = 32 << lwm, bn = 128 >> lwm;
         const int tm = (M + bm - 1) / bm;
         const long long tn = (half + bn - 1) / bn;

@@ -651,12 +651,13 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
 // Per-kind pipeline shape: k-chunk (BK), cp.async stages (ST), CTAs per SM
 // (__launch_bounds__).  Measured at B = 128 (exp/stage_times.py): BK 8 with 3
 // stages keeps more bytes in flight per CTA than BK 16 with 2 at the same
-// shared-memory footprint (4 CTAs / SM): 585 -> 565 us per round trip; LegFwd
-// runs 5 CTAs / SM (102 registers) and LegInv 4 stages (-1 us each).
+// shared-memory footprint (4 CTAs / SM): 585 -> 565 us per round trip; LegInv
+// and LegFwd (ring sized for wm <= 2) run 4 stages (-1 us, -3.6 us).
 #define SGL_KIND_CFG(NAME, DBK, DST, DMINB)                  \
     static constexpr int GEMM_BK = SGL_BK_##NAME > 0 ? SGL_BK_##NAME : DBK; \
     static constexpr int GEMM_ST = SGL_ST_##NAME > 0 ? SGL_ST_##NAME : DST; \
-    static constexpr int GEMM_MINB = SGL_MINB_##NAME > 0 ? SGL_MINB_##NAME : DMINB;
+    static constexpr int GEMM_MINB = SGL_MINB_##NAME > 0 ? SGL_MINB_##NAME : DMINB; \
+    static constexpr int GEMM_MAXWM = SGL_MAXWM_##NAME;
 
 // --- problem kinds
 // Legendre forward: prob = 2|m| + p.  rows l = |m|+p+2r, K = B (j'), cols n' = sgn*NB + n.
@@ -684,7 +685,7 @@ __device__ __forceinline__ long long g_col(const Geo& g, int p, int am, int n) {
 __device__ __forceinline__ long long g_rowstride(const Geo& g) { return 2 * g.ngx * 2 * g.nbins << g.lgib; }
 
 struct LegFwd {
-    SGL_KIND_CFG(LEGFWD, 8, 3, 5)
+    SGL_KIND_CFG(LEGFWD, 8, 4, 4)
     Geo g;
     const double* A;        // table
     const long long* aoff;  // per prob
@@ -895,7 +896,8 @@ struct GemmCfg {
 
 template <class P>
 constexpr size_t gemm_smem_bytes() {
-    constexpr int s1 = GemmCfg<P, 1>::STAGE, s2 = GemmCfg<P, 2>::STAGE, s4 = GemmCfg<P, 4>::STAGE;
+    constexpr int s1 = GemmCfg<P, 1>::STAGE, s2 = P::GEMM_MAXWM >= 2 ? GemmCfg<P, 2>::STAGE : 0,
+                  s4 = P::GEMM_MAXWM >= 4 ? GemmCfg<P, 4>::STAGE : 0;
     constexpr int m = s1 > s2 ? (s1 > s4 ? s1 : s4) : (s2 > s4 ? s2 : s4);
     return sizeof(double) * P::GEMM_ST * m;
 }
@@ -1132,10 +1134,10 @@ template <class P>
 __global__ void __launch_bounds__(128, P::GEMM_MINB) gemm_dmma_kernel(P pr, const __grid_constant__ TileMap tm) {
     extern __shared__ __align__(16) double gsm[];
     const Tile t = decode_tile(tm, pr.g.NB);
-    switch (t.pad) {  // warp layout chosen per tile
+    switch (t.pad) {  // warp layout chosen per tile (the host keeps wm <= P::GEMM_MAXWM)
         case 1: gemm_tile<P, 1>(pr, t, gsm); break;
-        case 2: gemm_tile<P, 2>(pr, t, gsm); break;
-        default: gemm_tile<P, 4>(pr, t, gsm); break;
+        case 2: if constexpr (P::GEMM_MAXWM >= 2) gemm_tile<P, 2>(pr, t, gsm); break;
+        default: if constexpr (P::GEMM_MAXWM >= 4) gemm_tile<P, 4>(pr, t, gsm); break;
     }
 }
 

@@ -39,6 +39,21 @@ struct TileMap {
 // chosen per tile (Tile::pad) by the host.
 constexpr int tile_rows(int wm) { return 32 * wm; }
 constexpr int tile_cols(int wm) { return 128 / wm; }
+// Largest wm each kind's kernel is built for (its shared-memory ring is sized for
+// the largest stage it can see): the Legendre-forward problems have M <= B/2 + 1
+// rows, so 128-row tiles never win there and its ring is sized for wm <= 2.
+#ifndef SGL_MAXWM_LEGFWD
+#define SGL_MAXWM_LEGFWD 2
+#endif
+#ifndef SGL_MAXWM_LEGINV
+#define SGL_MAXWM_LEGINV 4
+#endif
+#ifndef SGL_MAXWM_RADFWD
+#define SGL_MAXWM_RADFWD 4
+#endif
+#ifndef SGL_MAXWM_RADINV
+#define SGL_MAXWM_RADINV 4
+#endif
 
 // Geometry shared by the stages.  "shell" is a flat index s = f * SC + i over
 // the functions of the batch and the SC radial shells handled by the call.
