@@ -829,7 +829,7 @@ struct RadInv {
     double* C;              // S blocks
     long long omega;
     ShellBlocks sb;
-    static constexpr bool A_KCONTIG = true;
+    static constexpr bool A_KCONTIG = false;  // V_l stored [n][i]: rows i contiguous
     static constexpr bool B_KCONTIG = false;
     __device__ int M(int) const { return 2 * g.B; }
     __device__ int mw(int l) const { return g.real ? l + 1 : 2 * l + 1; }
@@ -837,10 +837,10 @@ struct RadInv {
     __device__ int K(int l) const { return g.B - l; }
     static constexpr bool B_COL_AFFINE = false;
     __device__ int nlim(int l, int) const { return N(l); }
-    __device__ long long rowA(int l, int i) const { return aoff[l] + (long long)i * (g.B - l); }
-    __device__ long long colA(int, int k) const { return k; }
-    __device__ int a_sr(int l) const { return g.B - l; }
-    __device__ int a_sk(int) const { return 1; }
+    __device__ long long rowA(int l, int i) const { return aoff[l] + i; }
+    __device__ long long colA(int, int k) const { return (long long)k * 2 * g.B; }
+    __device__ int a_sr(int) const { return 1; }
+    __device__ int a_sk(int) const { return 2 * g.B; }
     __device__ long long rowB(int l, int k) const { return 2 * degree_offset(l + 1 + k); }
     __device__ long long b_kstep(int) const { return 0; }
     __device__ long long colB(int l, int n) const {
@@ -996,32 +996,38 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
     const int nch = K > 0 ? (K + BK - 1) / BK : 1;
 
     // ---- per-tile load plan: every address this thread will fetch is
-    // base + k0 * step, so a chunk issue is a handful of 64-bit adds
+    // base + k0 * step, so a chunk issue is a handful of 64-bit adds.  A moves in
+    // 2-element units along its contiguous dimension (k for A_KCONTIG, rows
+    // otherwise): one 16-byte cp.async when the tile's rows are 16-byte aligned,
+    // else two 8-byte ones.
+    constexpr int AU = C::AQ / 2;
     const int a_sk = pr.a_sk(pid);
-    const double* a_ptr[C::AQ];
-    int a_so[C::AQ], a_k[C::AQ];
-    unsigned a_ok = 0;
+    const int a_sr = pr.a_sr(pid);
+    const double* a_ptr[AU];
+    int a_so[AU], a_k[AU];
+    unsigned a_ok = 0, a_ok2 = 0;  // first / second element's row inside M
+    bool a_vec;
     {
         const long long abase = pr.rowA(pid, m0);
-        const int a_sr = pr.a_sr(pid);
+        a_vec = P::A_KCONTIG ? a_sk == 1 && ((abase | a_sr) & 1) == 0 : a_sr == 1 && ((abase | a_sk) & 1) == 0;
 #pragma unroll
-        for (int q = 0; q < C::AQ; ++q) {
+        for (int u = 0; u < AU; ++u) {
+            const int e = tid + 128 * u;
             int row, k;
             if (P::A_KCONTIG) {
-                constexpr int KPT = BK / 4;  // 4 threads per row, KPT consecutive k each
-                row = (tid >> 2) + 32 * (q / KPT);
-                k = (tid & 3) * KPT + (q % KPT);
-                a_so[q] = row * C::LDA + k;
+                row = e / (BK / 2);
+                k = 2 * (e % (BK / 2));
+                a_so[u] = row * C::LDA + k;
             } else {
-                const int e = tid + 128 * q;
-                row = e % BM;
-                k = e / BM;
-                a_so[q] = k * C::LDA + row;
+                row = 2 * (e % (BM / 2));
+                k = e / (BM / 2);
+                a_so[u] = k * C::LDA + row;
             }
-            a_k[q] = k;
+            a_k[u] = k;
             const bool ok = m0 + row < M;
-            a_ok |= (ok ? 1u : 0u) << q;
-            a_ptr[q] = ok ? pr.A + abase + (long long)row * a_sr + (long long)k * a_sk : pr.A;
+            a_ok |= (ok ? 1u : 0u) << u;
+            a_ok2 |= ((P::A_KCONTIG ? ok : m0 + row + 1 < M) ? 1u : 0u) << u;
+            a_ptr[u] = ok ? pr.A + abase + (long long)row * a_sr + (long long)k * a_sk : pr.A;
         }
     }
     const long long b_step = pr.b_kstep(pid);  // > 0: rowB is affine in k with this stride
@@ -1060,9 +1066,27 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
         const int k0 = c * BK;
         const long long a_adv = (long long)k0 * a_sk;
 #pragma unroll
-        for (int q = 0; q < C::AQ; ++q) {
-            const bool ok = ((a_ok >> q) & 1u) && k0 + a_k[q] < K;
-            cp_async8_zfill(as + a_so[q], ok ? a_ptr[q] + a_adv : pr.A, ok);
+        for (int u = 0; u < AU; ++u) {
+            const double* src = a_ptr[u] + a_adv;
+            bool ok1, ok2;  // the unit's two elements
+            if (P::A_KCONTIG) {
+                const int kv = K - (k0 + a_k[u]);
+                ok1 = ((a_ok >> u) & 1u) && kv >= 1;
+                ok2 = ((a_ok >> u) & 1u) && kv >= 2;
+            } else {
+                const bool kok = k0 + a_k[u] < K;
+                ok1 = ((a_ok >> u) & 1u) && kok;
+                ok2 = ((a_ok2 >> u) & 1u) && kok;
+            }
+            if (a_vec) {
+                const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(as + a_so[u]));
+                const int nb = ok1 ? (ok2 ? 16 : 8) : 0;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(ok1 ? src : pr.A),
+                             "r"(nb));
+            } else {
+                cp_async8_zfill(as + a_so[u], ok1 ? src : pr.A, ok1);
+                cp_async8_zfill(as + a_so[u] + 1, ok2 ? src + (P::A_KCONTIG ? a_sk : a_sr) : pr.A, ok2);
+            }
         }
         const long long b_adv = (long long)k0 * b_step;
 #pragma unroll

@@ -137,7 +137,7 @@ Tables build_tables(int B, const double* r, const double* a_mod, const double* b
                     cur = next;
                 }
                 t.radial_fwd[t.radial_fwd_off[l] + (long long)q * n2 + i] = (double)(cur * wf);
-                t.radial_inv[t.radial_inv_off[l] + (long long)i * rows + q] = (double)(cur * gi);
+                t.radial_inv[t.radial_inv_off[l] + (long long)q * n2 + i] = (double)(cur * gi);
             }
         }
     });

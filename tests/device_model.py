@@ -91,7 +91,7 @@ class DeviceModel:
         N = 2 * B
         S = np.zeros((B * B, N), dtype=complex)
         for l in range(B):
-            Vl = self.t["V"][self.t["V_off"][l]:self.t["V_off"][l + 1]].reshape(N, B - l)
+            Vl = self.t["V"][self.t["V_off"][l]:self.t["V_off"][l + 1]].reshape(B - l, N).T  # stored [n][i]
             T = np.zeros((B - l, 2 * l + 1), dtype=complex)
             for q in range(B - l):
                 n = l + 1 + q

@@ -119,18 +119,18 @@ def test_device_model_matches_oracle(B):
 
 @pytest.mark.parametrize("B", [4, 8])
 def test_device_radial_tables_match_closed_form(B):
-    """W_l[n][i] = N_nl R_nl(r_i) e^{-r_i^2} a_mod_i and V_l[i][n] = N_nl R_nl(r_i)
+    """W_l[n][i] = N_nl R_nl(r_i) e^{-r_i^2} a_mod_i and V_l[n][i] = N_nl R_nl(r_i)
     (radial_transform.cpp:75-133) against the closed-form Laguerre route
     (special_functions.cpp:110-127)."""
     o = Oracle(B)
     t = host_tables(B, o.r, o.a_mod, o.b_cal)
     for l in range(B):
         W = t["W"][t["W_off"][l]:t["W_off"][l + 1]].reshape(B - l, 2 * B)
-        V = t["V"][t["V_off"][l]:t["V_off"][l + 1]].reshape(2 * B, B - l)
+        V = t["V"][t["V_off"][l]:t["V_off"][l + 1]].reshape(B - l, 2 * B)
         y0 = np.sqrt((2 * l + 1) / (4 * np.pi))
         for q in range(B - l):
             n = l + 1 + q
             rad = np.array([Oracle.sgl_basis(n, l, 0, ri, 0.0, 0.0).real / y0 for ri in o.r])
-            assert np.abs(V[:, q] - rad).max() < 1e-12 * max(1.0, np.abs(rad).max())
+            assert np.abs(V[q] - rad).max() < 1e-12 * max(1.0, np.abs(rad).max())
             w = rad * np.exp(-o.r ** 2) * o.a_mod
             assert np.abs(W[q] - w).max() < 1e-12 * max(1.0, np.abs(w).max())
