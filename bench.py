@@ -44,6 +44,11 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "_fallback": True}
 
 
+def config_id(B, nb):
+    """BASELINE.json config label for a (B, functions per step) workload."""
+    return {(16, 1): "C1", (64, 64): "C2", (128, 1): "C3", (256, 1): "C4"}.get((B, nb), "custom")
+
+
 def env_rank():
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
             int(os.environ.get("LOCAL_RANK", "0")))
@@ -284,11 +289,11 @@ def main():
         inv(plan, cin[s % nrot], out=grid)
         fwd(plan, grid, out=cout)
 
-    for s in range(max(args.warmup, nrot + 2 if graphs else 0)):  # graphs need each input seen twice
+    for s in range(max(args.warmup, 2 * nrot + 2 if graphs else 0)):  # graph capture starts at the second call per input: every input twice
         step(s)
     torch.cuda.synchronize()
     # correctness guard on the warm-up output
-    wl_last = max(args.warmup, nrot + 2 if graphs else 0) - 1
+    wl_last = max(args.warmup, 2 * nrot + 2 if graphs else 0) - 1
     err = float((cout - cin[wl_last % nrot]).abs().max() / cin[wl_last % nrot].abs().max())
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -402,7 +407,8 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: iid complex normal coefficients (numpy PCG64, seed = rank)",
         "config": {"workload": (f"C5: B={B}, {nb} real-valued functions per step per GPU (real fast path)"
-                                if args.real else f"C3: B={B}, {nb} function(s) per step per GPU, ifsglft then fsglft"),
+                                if args.real else f"{config_id(B, nb)}: B={B}, {nb} function(s) per step per GPU, "
+                                                  "ifsglft then fsglft"),
                    "B": B, "batch_per_gpu": nb, "parallelism": f"replicas x{world}" if world > 1 else "single",
                    "l2": f"inputs rotated over {nrot} coefficient buffers ({nrot * 16 * Om * nb / 1e6:.0f} MB) "
                          f"and every step writes/reads a {16 * Ps * nb / 2**20:.0f} MiB grid (> 126 MB L2)"},
