@@ -106,6 +106,12 @@ SglCoefficients fsglft(const SampleGrid& grid, const TransformPlan& plan, unsign
 /// Fast inverse (sgl_transform.hpp:74-76).
 SampleGrid ifsglft(const SglCoefficients& coeffs, const TransformPlan& plan, unsigned threads = 1);
 
+/// Separated transforms (sgl_transform.hpp, dsglft_separated / idsglft_separated;
+/// sgl_transform.cpp:189-272) run on the device as a cross-oracle of the fast
+/// path: closed-form basis values, direct quadratures.  B <= 64.
+SglCoefficients dsglft_separated(const SampleGrid& grid, const TransformPlan& plan, unsigned threads = 1);
+SampleGrid idsglft_separated(const SglCoefficients& coeffs, const TransformPlan& plan, unsigned threads = 1);
+
 /// Batched, host or device memory (see sglgpu.h for mem_kind).
 void fsglft_batch(const TransformPlan& plan, const cplx* samples, cplx* coeffs, std::size_t batch,
                   bool device_pointers = false, void* stream = nullptr);

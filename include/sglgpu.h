@@ -94,6 +94,18 @@ int sglgpu_forward_real(sglgpu_plan* plan, const double* samples, double* coeffs
 int sglgpu_inverse_real(sglgpu_plan* plan, const double* coeffs, double* samples, size_t batch,
                         int mem_kind, void* stream);
 
+/* On-device cross-oracle: the reference's separated transforms
+ * dsglft_separated / idsglft_separated (sgl_transform.cpp:189-272) with
+ * closed-form basis values (assoc_legendre x sph_harm_norm, norm_const x
+ * gen_laguerre x r^l; special_functions.cpp) and direct quadratures -- no FFT,
+ * no fold, no tables, no DMMA -- to check the fast path on the device.  Same
+ * layouts and batching as sglgpu_forward / sglgpu_inverse; B <= 64 (beyond that
+ * the reference's unnormalized Legendre seed is not valid), else SGLGPU_EINVAL. */
+int sglgpu_forward_separated(sglgpu_plan* plan, const double* samples, double* coeffs, size_t batch,
+                             int mem_kind, void* stream);
+int sglgpu_inverse_separated(sglgpu_plan* plan, const double* coeffs, double* samples, size_t batch,
+                             int mem_kind, void* stream);
+
 /* Stage entry points (device memory only, asynchronous on `stream`), used by the
  * multi-GPU shell / (l, m) decomposition.  `shells` is the nu-major intermediate
  * S[nu][f][i] (nu = l(l+1)+m, f < batch, i < shell_count), i.e. the transpose of

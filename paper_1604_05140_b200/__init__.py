@@ -54,7 +54,8 @@ def lib():
         L.sglgpu_plan_table_bytes.argtypes = [_vp]
         L.sglgpu_plan_table_bytes.restype = ctypes.c_size_t
         L.sglgpu_last_launch_count.argtypes = [_vp]
-        for name in ("sglgpu_forward", "sglgpu_inverse", "sglgpu_forward_real", "sglgpu_inverse_real"):
+        for name in ("sglgpu_forward", "sglgpu_inverse", "sglgpu_forward_real", "sglgpu_inverse_real",
+                     "sglgpu_forward_separated", "sglgpu_inverse_separated"):
             getattr(L, name).argtypes = [_vp, _vp, _vp, ctypes.c_size_t, ctypes.c_int, _vp]
         for name in ("sglgpu_spherical_forward", "sglgpu_spherical_inverse"):
             getattr(L, name).argtypes = [_vp, _vp, ctypes.c_size_t, _vp, ctypes.c_int, ctypes.c_int,
@@ -285,6 +286,25 @@ def ifsglft(coeffs: SglCoefficients, plan: TransformPlan, threads: int = 1) -> S
     return SampleGrid(plan.bandlimit, out)
 
 
+def dsglft_separated(grid: SampleGrid, plan: TransformPlan, threads: int = 1) -> SglCoefficients:
+    """Separated forward transform (sgl_transform.cpp:189-229) as an on-device cross-oracle:
+    closed-form basis values and direct quadratures, independent of the fast path. B <= 64."""
+    _check_plan_grid(grid, plan)
+    g = np.ascontiguousarray(grid.values, dtype=np.complex128)
+    out = np.zeros(coefficient_count(plan.bandlimit), dtype=np.complex128)
+    _check(lib().sglgpu_forward_separated(plan.handle, g.ctypes.data, out.ctypes.data, 1, MEM_HOST, None))
+    return SglCoefficients(plan.bandlimit, out)
+
+
+def idsglft_separated(coeffs: SglCoefficients, plan: TransformPlan, threads: int = 1) -> SampleGrid:
+    """Separated inverse transform (sgl_transform.cpp:231-272) as an on-device cross-oracle. B <= 64."""
+    _check_plan_coeffs(coeffs, plan)
+    c = np.ascontiguousarray(coeffs.values, dtype=np.complex128)
+    out = np.zeros(sample_count(plan.bandlimit), dtype=np.complex128)
+    _check(lib().sglgpu_inverse_separated(plan.handle, c.ctypes.data, out.ctypes.data, 1, MEM_HOST, None))
+    return SampleGrid(plan.bandlimit, out)
+
+
 def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
@@ -401,6 +421,7 @@ def roundtrip_error(reference, actual) -> RoundtripError:
 
 __all__ = [
     "SphericalRule", "RadialRule", "TransformPlan", "SglCoefficients", "SampleGrid", "fsglft", "ifsglft",
-    "fsglft_batch", "ifsglft_batch", "fsglft_real_batch", "ifsglft_real_batch", "roundtrip_error", "sphere_rule", "load_radial_rule", "sample_count",
+    "dsglft_separated", "idsglft_separated", "fsglft_batch", "ifsglft_batch", "fsglft_real_batch",
+    "ifsglft_real_batch", "roundtrip_error", "sphere_rule", "load_radial_rule", "sample_count",
     "coefficient_count", "psi_index", "nu_index", "omega_index", "lib",
 ]

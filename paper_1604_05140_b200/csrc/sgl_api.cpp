@@ -281,6 +281,27 @@ SampleGrid ifsglft(const SglCoefficients& coeffs, const TransformPlan& plan, uns
     return out;
 }
 
+SglCoefficients dsglft_separated(const SampleGrid& grid, const TransformPlan& plan, unsigned /*threads*/) {
+    check_plan_grid(grid, plan);
+    SglCoefficients out;
+    out.bandlimit = plan.bandlimit;
+    out.values.assign(coefficient_count(plan.bandlimit), cplx(0.0));
+    throw_status(sglgpu_forward_separated(plan.device_plan(), reinterpret_cast<const double*>(grid.values.data()),
+                                          reinterpret_cast<double*>(out.values.data()), 1, SGLGPU_MEM_HOST, nullptr));
+    return out;
+}
+
+SampleGrid idsglft_separated(const SglCoefficients& coeffs, const TransformPlan& plan, unsigned /*threads*/) {
+    check_plan_coeffs(coeffs, plan);
+    SampleGrid out;
+    out.bandlimit = plan.bandlimit;
+    out.values.assign(sample_count(plan.bandlimit), cplx(0.0));
+    throw_status(sglgpu_inverse_separated(plan.device_plan(), reinterpret_cast<const double*>(coeffs.values.data()),
+                                          reinterpret_cast<double*>(out.values.data()), 1, SGLGPU_MEM_HOST,
+                                          nullptr));
+    return out;
+}
+
 void fsglft_batch(const TransformPlan& plan, const cplx* samples, cplx* coeffs, std::size_t batch,
                   bool device_pointers, void* stream) {
     throw_status(sglgpu_forward(plan.device_plan(), reinterpret_cast<const double*>(samples),

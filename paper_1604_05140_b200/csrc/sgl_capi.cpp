@@ -103,6 +103,8 @@ struct sglgpu_plan {
     long long* d_W_off = nullptr;
     double* d_V = nullptr;
     long long* d_V_off = nullptr;
+    double* d_r = nullptr;     // radial rule (separated cross-oracle only)
+    double* d_amod = nullptr;
     DevBuf G, S, in, out;
     std::map<std::tuple<int, int, int, int, int>, std::pair<sglk::TileMap*, int>> tiles;
     std::mutex mu;
@@ -701,6 +703,50 @@ int run_real(sglgpu_plan* p, const double* in, double* out, size_t batch, int me
     });
 }
 
+// dsglft_separated / idsglft_separated (sgl_transform.cpp:189-272) on the device:
+// the cross-oracle rung of SURVEY.md 8(f).  Synchronous w.r.t. host memory.
+int run_separated(sglgpu_plan* p, const double* in, double* out, size_t batch, int mem_kind, void* stream,
+                  bool forward) {
+    return guarded([&] {
+        check_plan(p);
+        if (mem_kind != SGLGPU_MEM_HOST && mem_kind != SGLGPU_MEM_DEVICE)
+            fail(SGLGPU_EINVAL, "sglgpu: unknown mem_kind");
+        if (batch == 0) return;
+        if (!in || !out) fail(SGLGPU_EINVAL, "sglgpu: null data pointer");
+        const int B = p->B;
+        if (B > 64) fail(SGLGPU_EINVAL, "sglgpu separated transform: bandlimit must be <= 64 (reference validity)");
+        std::lock_guard<std::mutex> lock(p->mu);
+        set_device(p);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const size_t psi = 2 * (size_t)sample_count(B), om = 2 * (size_t)coefficient_count(B);
+        const size_t in_len = forward ? psi : om, out_len = forward ? om : psi;
+        const size_t chunk = std::max<size_t>(1, std::min<size_t>(batch, 64));
+        p->S.ensure((size_t)4 * B * B * B * chunk);
+        int launches = 0;
+        for (size_t b0 = 0; b0 < batch; b0 += chunk) {
+            const int nb = (int)std::min(chunk, batch - b0);
+            const double* src = in + b0 * in_len;
+            double* dst = out + b0 * out_len;
+            if (mem_kind == SGLGPU_MEM_HOST) {
+                p->in.ensure(in_len * chunk);
+                p->out.ensure(out_len * chunk);
+                ck(cudaMemcpyAsync(p->in.p, src, nb * in_len * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+                src = p->in.p;
+            }
+            double* d_dst = mem_kind == SGLGPU_MEM_HOST ? p->out.p : dst;
+            const int k = forward ? sglk::launch_separated_forward(B, nb, src, d_dst, p->S.p, p->d_r, p->d_amod,
+                                                                   p->d_bcal, st)
+                                  : sglk::launch_separated_inverse(B, nb, src, d_dst, p->S.p, p->d_r, st);
+            ck_launch(k, forward ? "separated_forward" : "separated_inverse");
+            launches += k;
+            if (mem_kind == SGLGPU_MEM_HOST)
+                ck(cudaMemcpyAsync(dst, p->out.p, nb * out_len * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+        }
+        if (mem_kind == SGLGPU_MEM_HOST) ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        p->last_launches = launches;
+    });
+}
+
 int run(sglgpu_plan* p, const double* in, double* out, size_t batch, int mem_kind, void* stream,
         bool forward) {
     return guarded([&] {
@@ -829,6 +875,8 @@ int sglgpu_plan_create(const sglgpu_plan_desc* desc, sglgpu_plan** out) {
             p->d_W_off = dev_upload(t.radial_fwd_off);
             p->d_V = dev_upload(t.radial_inv);
             p->d_V_off = dev_upload(t.radial_inv_off);
+            p->d_r = dev_upload(std::vector<double>(desc->r, desc->r + 2 * B));
+            p->d_amod = dev_upload(std::vector<double>(desc->a_mod, desc->a_mod + 2 * B));
         } catch (...) {
             sglgpu_plan_destroy(p);
             throw;
@@ -846,7 +894,7 @@ int sglgpu_plan_destroy(sglgpu_plan* p) {
     cudaSetDevice(p->device);
     cudaDeviceSynchronize();
     for (void* q : {(void*)p->d_tw, (void*)p->d_bcal, (void*)p->d_leg, (void*)p->d_leg_off, (void*)p->d_W,
-                    (void*)p->d_W_off, (void*)p->d_V, (void*)p->d_V_off})
+                    (void*)p->d_W_off, (void*)p->d_V, (void*)p->d_V_off, (void*)p->d_r, (void*)p->d_amod})
         if (q) cudaFree(q);
     for (auto& kv : p->tiles) delete kv.second.first;
     for (auto& [stage, a, b] : p->prof) {
@@ -911,6 +959,16 @@ int sglgpu_forward(sglgpu_plan* plan, const double* samples, double* coeffs, siz
 int sglgpu_inverse(sglgpu_plan* plan, const double* coeffs, double* samples, size_t batch, int mem_kind,
                    void* stream) {
     return run(plan, coeffs, samples, batch, mem_kind, stream, false);
+}
+
+int sglgpu_forward_separated(sglgpu_plan* plan, const double* samples, double* coeffs, size_t batch, int mem_kind,
+                             void* stream) {
+    return run_separated(plan, samples, coeffs, batch, mem_kind, stream, true);
+}
+
+int sglgpu_inverse_separated(sglgpu_plan* plan, const double* coeffs, double* samples, size_t batch, int mem_kind,
+                             void* stream) {
+    return run_separated(plan, coeffs, samples, batch, mem_kind, stream, false);
 }
 
 int sglgpu_forward_real(sglgpu_plan* plan, const double* samples, double* coeffs, size_t batch, int mem_kind,

@@ -130,4 +130,12 @@ int launch_radial_inverse(const Geo& g, const RadialBlocks& rb, const double* C,
                           const double* V, const long long* v_off, const TileMap* tiles, int ntiles,
                           cudaStream_t s);
 
+// On-device cross-oracle (sgl_separated.cu): the reference's separated transforms
+// with closed-form basis values, direct quadratures, no tables.  shells: scratch
+// of batch * 2B * B^2 complex.  r, a_mod: the radial rule (2B each).
+int launch_separated_forward(int B, int batch, const double* samples, double* coeffs, double* shells,
+                             const double* r, const double* a_mod, const double* bcal, cudaStream_t s);
+int launch_separated_inverse(int B, int batch, const double* coeffs, double* samples, double* shells,
+                             const double* r, cudaStream_t s);
+
 }  // namespace sglk

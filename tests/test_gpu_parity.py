@@ -415,3 +415,42 @@ def test_full_size_properties_b128():
     assert float((lin - ref).abs().max() / ref.abs().max()) < 1e-13
     z = sgl.fsglft_batch(plan, torch.zeros((1, sgl.sample_count(B)), dtype=torch.complex128, device="cuda"))
     assert not bool(z.abs().max())
+
+
+# ---------------------------------------------------------------- on-device cross-oracle
+@pytest.mark.parametrize("B", [1, 2, 3, 5, 8, 16, 32])
+def test_separated_cross_oracle_matches_fast_path_and_oracle(B):
+    """dsglft_separated / idsglft_separated on the GPU (closed-form basis values, direct
+    quadratures: sgl_transform.cpp:189-272) agree with the fast GPU path and the CPU oracle."""
+    plan, orc = plan_for(B)
+    rng = np.random.default_rng(4000 + B)
+    c = complex_normal(rng, coefficient_count(B))
+    g_sep = sgl.idsglft_separated(sgl.SglCoefficients(B, c), plan).values
+    g_fast = sgl.ifsglft(sgl.SglCoefficients(B, c), plan).values
+    assert np.isfinite(g_sep).all()
+    assert per_shell(g_sep, g_fast, B) <= TOL
+    assert per_shell(g_sep, orc.inverse(c), B) <= TOL
+    g = complex_normal(rng, sample_count(B))  # not bandlimited: every term of the quadrature counts
+    f_sep = sgl.dsglft_separated(sgl.SampleGrid(B, g), plan).values
+    assert normwise(f_sep, sgl.fsglft(sgl.SampleGrid(B, g), plan).values) <= TOL
+    assert normwise(f_sep, orc.forward(g)) <= TOL
+
+
+@pytest.mark.parametrize("B", [2, 4, 8, 16])
+def test_separated_cross_oracle_on_reference_golden(B):
+    """The reference's own round trip (tests/golden, made by oracle/_ref) through the separated rung."""
+    import os
+
+    golden = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    load = lambda n: np.fromfile(os.path.join(golden, n), dtype="<f8").view(np.complex128)
+    plan, _ = plan_for(B)
+    g_ref, back_ref = load(f"rt_B{B}_grid.bin"), load(f"rt_B{B}_back.bin")
+    assert normwise(sgl.dsglft_separated(sgl.SampleGrid(B, g_ref), plan).values, back_ref) <= 1e-13
+    assert per_shell(sgl.idsglft_separated(sgl.SglCoefficients(B, load(f"rt_B{B}_coeffs.bin")), plan).values,
+                     g_ref, B) <= 1e-13
+
+
+def test_separated_cross_oracle_rejects_large_bandlimit():
+    plan, _ = plan_for(128)
+    with pytest.raises(ValueError, match="<= 64"):
+        sgl.dsglft_separated(sgl.SampleGrid(128, np.zeros(sample_count(128), complex)), plan)
