@@ -124,6 +124,18 @@ int main() {
         }
         report(ok && ok2, "shape errors", "");
     }
+    // fast == separated (the oracle chain, :148-174; here the separated rung runs on the device)
+    {
+        const auto plan = TransformPlan::compute(8);
+        SampleGrid g{8, random_complex(sample_count(8), 88)};
+        const auto f = fsglft(g, plan), s = dsglft_separated(g, plan);
+        double num = 0.0, den = 0.0;
+        for (std::size_t w = 0; w < f.values.size(); ++w) {
+            num = std::max(num, std::abs(f.values[w] - s.values[w]));
+            den = std::max(den, std::abs(s.values[w]));
+        }
+        report(num / den < 1e-12, "fast == separated (device)", std::to_string(num / den));
+    }
     // B = 128: valid where the reference's M_lm underflows
     {
         const auto plan = TransformPlan::compute(128);
