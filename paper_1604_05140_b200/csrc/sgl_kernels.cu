@@ -131,6 +131,16 @@ struct FFTShape {
     static constexpr int R0 = 1 << (LOGN % 4 == 0 ? (N < 16 ? LOGN : 4) : LOGN % 4);  // first radix
     static constexpr int IG = (T * 2 <= 256) ? (ELEMS / 16) / T : 1;  // shell pairs per CTA
     static constexpr int THREADS = 2 * IG * T;
+    // twiddle table: N plain entries, then 15 Ns entries per pass after the first
+    // (sgl_tables.cpp); HEAD: a leading small-radix pass
+    static constexpr bool HEAD = (R0 != RMAX || N < 16);
+    static constexpr int NPASS = (HEAD ? 1 : 0) + ((N >= 16) ? (LOGN - (HEAD ? ilog2c(R0) : 0)) / 4 : 0);
+    static constexpr int tw_count() {
+        int n = N, ns = HEAD ? R0 : 16;
+        for (int p = 1; p < NPASS; ++p, ns *= 16) n += 15 * ns;
+        return n;
+    }
+    static constexpr int TWN = tw_count();
 };
 
 // Synchronizes the threads that share a ring pair (j', 2B-1-j'): one warp when
@@ -145,13 +155,16 @@ __device__ __forceinline__ void pair_sync() {
 }
 
 // One Stockham pass of radix R on a ring of length N held by T threads.
-// Ns = product of the radices already applied.  tw[x] = e^{-2 pi i x / N}.
+// Ns = product of the radices already applied.  twp: this pass's twiddles,
+// twp[(r - 1) Ns + k] = e^{-2 pi i r k / (R Ns)} (PT; consecutive threads read
+// consecutive entries), or the plain table e^{-2 pi i x / N} (!PT).  Unused
+// when Ns = 1.
 // Inputs come from ld(x), outputs go to st(x, v): the first pass of the forward
 // FFT reads global memory directly into registers and the last pass of the
 // inverse writes global memory directly, so only the middle exchanges touch
 // shared memory.  When IN_PLACE, all reads complete (pair_sync) before any write.
-template <int N, int R, int SIGN, bool IN_PLACE, class Ld, class St>
-__device__ __forceinline__ void stockham_pass(int Ns, int t, const double2* tw, Ld&& ld, St&& st) {
+template <int N, int R, int SIGN, bool IN_PLACE, bool PT = true, class Ld, class St>
+__device__ __forceinline__ void stockham_pass(int Ns, int t, const double2* twp, Ld&& ld, St&& st) {
     constexpr int T = FFTShape<N>::T;
     constexpr int NBF = N / R;          // butterflies in this pass
     constexpr int PER = NBF / T;        // butterflies per thread
@@ -167,10 +180,10 @@ __device__ __forceinline__ void stockham_pass(int Ns, int t, const double2* tw, 
         const int j = t + b * T;
         const int k = j & (Ns - 1);
         if (Ns > 1) {
-            const int step = k * (N / (Ns * R));
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                double2 w = tw[(r * step) & (N - 1)];
+                // PT: this pass's table; else twp is the plain table tw[x] = e^{-2 pi i x / N}
+                double2 w = PT ? twp[(r - 1) * Ns + k] : twp[(r * k * (N / (Ns * R))) & (N - 1)];
                 if (SIGN > 0) w.y = -w.y;
                 v[b][r] = cmul(v[b][r], w);
             }
@@ -190,7 +203,7 @@ __device__ __forceinline__ void stockham_pass(int Ns, int t, const double2* tw, 
 
 // Full FFT of one ring: first pass reads ld, last pass writes st, middle
 // passes run in place on `ring` (padded).  Ends without a trailing sync.
-template <int N, int SIGN, bool FIRST_IN_PLACE, class Ld, class St>
+template <int N, int SIGN, bool FIRST_IN_PLACE, bool PT = true, class Ld, class St>
 __device__ __forceinline__ void ring_fft_io(double2* ring, int t, const double2* tw, Ld&& ld, St&& st) {
     using S = FFTShape<N>;
     auto rd = [&](int x) { return ring[phys(x)]; };
@@ -211,13 +224,15 @@ __device__ __forceinline__ void ring_fft_io(double2* ring, int t, const double2*
             Ns *= 16;
         }
         pair_sync<N>();
+        const double2* twp = PT ? tw + N : tw;  // per-pass tables follow the N plain twiddles
 #pragma unroll 1
         for (int p = 1; p < NPASS - 1; ++p) {
-            stockham_pass<N, 16, SIGN, true>(Ns, t, tw, rd, wr);
+            stockham_pass<N, 16, SIGN, true, PT>(Ns, t, twp, rd, wr);
+            if (PT) twp += 15 * Ns;
             Ns *= 16;
             pair_sync<N>();
         }
-        stockham_pass<N, 16, SIGN, true>(Ns, t, tw, rd, st);
+        stockham_pass<N, 16, SIGN, true, PT>(Ns, t, twp, rd, st);
     }
 }
 
@@ -299,6 +314,9 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
     using S = FFTShape<N, SGL_AZI_ELEMS>;
     constexpr int B = N / 2;
     extern __shared__ double2 smem[];
+    // the plain twiddle table staged in shared memory under the prologue barrier
+    // (measured: 118 us; the forward kernel's per-pass tables from global 120 us,
+    // per-pass tables in shared memory 125 us)
     double2* tw = smem;
     double2* rings = smem + N;
     const int tid = threadIdx.x;
@@ -338,7 +356,7 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
             const int f = s / g.SC, i = s - f * g.SC;
             dst = X + (size_t)f * fstride + ((size_t)i * N + j) * N;
         }
-        ring_fft_io<N, +1, true>(
+        ring_fft_io<N, +1, true, false>(
             ring, tt, tw,
             [&](int x) {
                 const double2 e = e_buf[phys(x)], o = o_buf[phys(x)];
@@ -366,12 +384,12 @@ az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, doub
     constexpr int IGR = 2 * S::IG;
     extern __shared__ double2 smem[];
     double2* tw = smem;
-    double2* rings = smem + N;
+    double2* rings = smem + S::TWN;
     const int tid = threadIdx.x;
     const int jp = blockIdx.y;
     const int s0 = blockIdx.x * IGR;
     const int nshell = g.batch * g.SC;
-    for (int x = tid; x < N; x += S::THREADS) tw[x] = __ldg(twg + x);
+    for (int x = tid; x < S::TWN; x += S::THREADS) tw[x] = __ldg(twg + x);
     __syncthreads();
     {
         const int q = tid / S::T, tt = tid - q * S::T;
@@ -417,7 +435,7 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
     constexpr int EOS = N + 1;  // per shell: E[0..B) then O[0..B), padded
     extern __shared__ double2 smem[];
     double2* tw = smem;
-    double2* rings = smem + N;
+    double2* rings = smem + S::TWN;
     double2* eo = rings + IGR * S::STRIDE;
     const int tid = threadIdx.x;
     const int jp = blockIdx.y;
@@ -436,7 +454,7 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
             *dst = make_double2(0.0, 0.0);
         }
     }
-    for (int x = tid; x < N; x += S::THREADS) tw[x] = __ldg(twg + x);
+    for (int x = tid; x < S::TWN; x += S::THREADS) tw[x] = __ldg(twg + x);
     cp_async_wait_all();
     __syncthreads();
     {
@@ -477,7 +495,7 @@ static int az_fwd_real_launch(const Geo& g, const double* X, size_t fstride, dou
                               const double* tw, cudaStream_t s) {
     using S = FFTShape<N>;
     constexpr int IGR = 2 * S::IG;
-    const size_t smem = sizeof(double2) * (N + IGR * S::STRIDE);
+    const size_t smem = sizeof(double2) * (S::TWN + IGR * S::STRIDE);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(az_forward_real_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -495,7 +513,7 @@ static int az_inv_real_launch(const Geo& g, const double* G, double* X, size_t f
                               cudaStream_t s) {
     using S = FFTShape<N>;
     constexpr int IGR = 2 * S::IG;
-    const size_t smem = sizeof(double2) * (N + IGR * S::STRIDE + IGR * (N + 1));
+    const size_t smem = sizeof(double2) * (S::TWN + IGR * S::STRIDE + IGR * (N + 1));
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(az_inverse_real_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -49,6 +49,26 @@ Tables build_tables(int B, const double* r, const double* a_mod, const double* b
         t.twiddle[2 * x] = (double)cosl(ang);
         t.twiddle[2 * x + 1] = (double)sinl(ang);
     }
+    // Per-pass twiddle tables of the radix-16 Stockham FFT (sgl_kernels.cu,
+    // ring_fft_io / FFTShape): for every pass after the first, radix 16 with Ns
+    // outputs already combined, entries w[(r - 1) Ns + k] = tw[r k N / (16 Ns)],
+    // r = 1..15, k < Ns -- consecutive threads read consecutive entries.
+    if ((n2 & (n2 - 1)) == 0 && n2 >= 32) {
+        int logn = 0;
+        while ((1 << logn) < n2) ++logn;
+        const int r0 = logn % 4 == 0 ? 16 : 1 << (logn % 4);
+        const bool head = r0 != 16;
+        const int npass = (head ? 1 : 0) + (logn - (head ? logn % 4 : 0)) / 4;
+        int ns = head ? r0 : 16;
+        for (int pass = 1; pass < npass; ++pass, ns *= 16)
+            for (int rr = 1; rr < 16; ++rr)
+                for (int k = 0; k < ns; ++k) {
+                    const long long x = ((long long)rr * k * (n2 / (ns * 16))) % n2;
+                    const long double ang = -2.0L * kPiL * x / n2;
+                    t.twiddle.push_back((double)cosl(ang));
+                    t.twiddle.push_back((double)sinl(ang));
+                }
+    }
     t.bcal.assign(bcal, bcal + n2);
 
     // ---- normalized Legendre table, rows grouped by (|m|, parity)
