@@ -118,9 +118,6 @@ __device__ __forceinline__ int phys(int x) { return x + (x >> 4); }
 #ifndef SGL_AZI_MINB
 #define SGL_AZI_MINB SGL_AZ_MINB
 #endif
-#ifndef SGL_AZI_ASYNC
-#define SGL_AZI_ASYNC 0  // inverse prologue: cp.async (1) or register loads (0); measured: 0 is faster
-#endif
 
 template <int N, int ELEMS = SGL_AZ_ELEMS>
 struct FFTShape {
@@ -323,23 +320,29 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
     const int jp = blockIdx.y;
     const int s0 = blockIdx.x * S::IG;
     const int nshell = g.batch * g.SC;
-#pragma unroll 4
-    for (int idx = tid; idx < 2 * N * S::IG; idx += S::THREADS) {
+    // prologue: all of this thread's G loads in flight before the first shared
+    // store (a partially unrolled load -> store loop kept only 4 in flight)
+    constexpr int PER = 2 * N * S::IG / S::THREADS;
+    static_assert(PER * S::THREADS == 2 * N * S::IG, "prologue must divide evenly");
+    double2 pv[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int idx = tid + q * S::THREADS;
         const int sl = idx % S::IG;
         const int rowi = idx / S::IG;  // p * N + bin
         const int p = rowi / N, bin = rowi - p * N;
         const int s = s0 + sl;
-        double2* dst = rings + (2 * sl + p) * S::STRIDE + phys(bin);
-        if (bin != B && s < nshell) {
-            const double2* src = G + g_index(g, p, bin, jp, s);
-            if (SGL_AZI_ASYNC) cp_async16(dst, src);
-            else *dst = __ldcs(src);
-        } else {
-            *dst = make_double2(0.0, 0.0);
-        }
+        pv[q] = (bin != B && s < nshell) ? __ldcs(G + g_index(g, p, bin, jp, s)) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int idx = tid + q * S::THREADS;
+        const int sl = idx % S::IG;
+        const int rowi = idx / S::IG;
+        const int p = rowi / N, bin = rowi - p * N;
+        rings[(2 * sl + p) * S::STRIDE + phys(bin)] = pv[q];
     }
     for (int x = tid; x < N; x += S::THREADS) tw[x] = __ldg(twg + x);
-    if (SGL_AZI_ASYNC) cp_async_wait_all();
     __syncthreads();
     {
         const int q = tid / S::T, tt = tid - q * S::T;
