@@ -111,6 +111,9 @@ __device__ __forceinline__ int phys(int x) { return x + (x >> 4); }
 #ifndef SGL_AZ_MINB
 #define SGL_AZ_MINB 4
 #endif
+#ifndef SGL_AZI_TW
+#define SGL_AZI_TW 1  // inverse twiddles: 0 plain table in shared memory, 1 per-pass tables from global (93 vs 104 us)
+#endif
 
 #ifndef SGL_AZI_ELEMS
 #define SGL_AZI_ELEMS SGL_AZ_ELEMS  // inverse kernel tile size
@@ -314,8 +317,13 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
     // the plain twiddle table staged in shared memory under the prologue barrier
     // (measured: 118 us; the forward kernel's per-pass tables from global 120 us,
     // per-pass tables in shared memory 125 us)
+#if SGL_AZI_TW == 1
+    const double2* tw = twg;  // per-pass tables from global
+    double2* rings = smem;
+#else
     double2* tw = smem;
     double2* rings = smem + N;
+#endif
     const int tid = threadIdx.x;
     const int jp = blockIdx.y;
     const int s0 = blockIdx.x * S::IG;
@@ -342,7 +350,9 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
         const int p = rowi / N, bin = rowi - p * N;
         rings[(2 * sl + p) * S::STRIDE + phys(bin)] = pv[q];
     }
+#if SGL_AZI_TW != 1
     for (int x = tid; x < N; x += S::THREADS) tw[x] = __ldg(twg + x);
+#endif
     __syncthreads();
     {
         const int q = tid / S::T, tt = tid - q * S::T;
@@ -359,7 +369,7 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
             const int f = s / g.SC, i = s - f * g.SC;
             dst = X + (size_t)f * fstride + ((size_t)i * N + j) * N;
         }
-        ring_fft_io<N, +1, true, false>(
+        ring_fft_io<N, +1, true, SGL_AZI_TW == 1>(
             ring, tt, tw,
             [&](int x) {
                 const double2 e = e_buf[phys(x)], o = o_buf[phys(x)];
@@ -1237,7 +1247,7 @@ static int az_inv_launch(const Geo& g, const double* G, double* X, size_t fstrid
                          cudaStream_t s) {
     using S = FFTShape<N, SGL_AZI_ELEMS>;
     static_assert(S::IG == FFTShape<N>::IG, "forward and inverse azimuthal tiles must match the G blocking");
-    const size_t smem = sizeof(double2) * (N + 2 * S::IG * S::STRIDE);
+    const size_t smem = sizeof(double2) * ((SGL_AZI_TW == 1 ? 0 : N) + 2 * S::IG * S::STRIDE);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(az_inverse_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
