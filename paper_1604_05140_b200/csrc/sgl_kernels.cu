@@ -396,14 +396,11 @@ az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, doub
     constexpr int B = N / 2;
     constexpr int IGR = 2 * S::IG;
     extern __shared__ double2 smem[];
-    double2* tw = smem;
-    double2* rings = smem + S::TWN;
+    double2* rings = smem;  // twiddles: per-pass tables from global (as in az_forward_kernel)
     const int tid = threadIdx.x;
     const int jp = blockIdx.y;
     const int s0 = blockIdx.x * IGR;
     const int nshell = g.batch * g.SC;
-    for (int x = tid; x < S::TWN; x += S::THREADS) tw[x] = __ldg(twg + x);
-    __syncthreads();
     {
         const int q = tid / S::T, tt = tid - q * S::T;
         const int s = s0 + q;
@@ -417,7 +414,7 @@ az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, doub
         }
         double2* ring = rings + q * S::STRIDE;
         ring_fft_io<N, -1, false>(
-            ring, tt, tw, [&](int x) { return ok ? make_double2(__ldcs(src1 + x), __ldcs(src2 + x)) : make_double2(0.0, 0.0); },
+            ring, tt, twg, [&](int x) { return ok ? make_double2(__ldcs(src1 + x), __ldcs(src2 + x)) : make_double2(0.0, 0.0); },
             [&](int x, double2 v) { ring[phys(x)] = v; });
     }
     __syncthreads();
@@ -447,8 +444,7 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
     constexpr int IGR = 2 * S::IG;
     constexpr int EOS = N + 1;  // per shell: E[0..B) then O[0..B), padded
     extern __shared__ double2 smem[];
-    double2* tw = smem;
-    double2* rings = smem + S::TWN;
+    double2* rings = smem;  // twiddles: per-pass tables from global
     double2* eo = rings + IGR * S::STRIDE;
     const int tid = threadIdx.x;
     const int jp = blockIdx.y;
@@ -467,7 +463,6 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
             *dst = make_double2(0.0, 0.0);
         }
     }
-    for (int x = tid; x < S::TWN; x += S::THREADS) tw[x] = __ldg(twg + x);
     cp_async_wait_all();
     __syncthreads();
     {
@@ -484,7 +479,7 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
         }
         double2* ring = rings + q * S::STRIDE;
         ring_fft_io<N, +1, false>(
-            ring, tt, tw,
+            ring, tt, twg,
             [&](int bin) {
                 if (bin == B) return make_double2(0.0, 0.0);
                 const int m = bin < B ? bin : N - bin;
@@ -508,7 +503,7 @@ static int az_fwd_real_launch(const Geo& g, const double* X, size_t fstride, dou
                               const double* tw, cudaStream_t s) {
     using S = FFTShape<N>;
     constexpr int IGR = 2 * S::IG;
-    const size_t smem = sizeof(double2) * (S::TWN + IGR * S::STRIDE);
+    const size_t smem = sizeof(double2) * (IGR * S::STRIDE);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(az_forward_real_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -526,7 +521,7 @@ static int az_inv_real_launch(const Geo& g, const double* G, double* X, size_t f
                               cudaStream_t s) {
     using S = FFTShape<N>;
     constexpr int IGR = 2 * S::IG;
-    const size_t smem = sizeof(double2) * (S::TWN + IGR * S::STRIDE + IGR * (N + 1));
+    const size_t smem = sizeof(double2) * (IGR * S::STRIDE + IGR * (N + 1));
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(az_inverse_real_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
