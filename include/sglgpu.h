@@ -132,6 +132,33 @@ int sglgpu_spherical_inverse(sglgpu_plan* plan, const double* shells, double* sa
                              size_t sample_stride, int shell_begin, int shell_count,
                              size_t batch, void* stream);
 
+/* Multi-GPU exchange fused into the stage epilogues (NVLink peer stores instead
+ * of the all-to-all between the stages).  Device memory only.
+ *
+ * spherical_forward_to: like sglgpu_spherical_forward, but the Legendre
+ *   epilogue stores the S rows of degree l in [l_bounds[q], l_bounds[q+1]) at
+ *   dst[q] + (nu - l_bounds[q]^2) * NB (NB = 2 * batch * shell_count reals per
+ *   nu row): dst[q] is this rank's shell block inside rank q's receive buffer,
+ *   i.e. exactly what sglgpu_radial_forward reads there (shells_per_block =
+ *   shell_count).  ndst <= 8.
+ * radial_inverse_to: like sglgpu_radial_inverse, but shell block b
+ *   ([b * spb, (b+1) * spb)) is stored in rank b's full-nu S buffer dst[b]
+ *   ([nu][f][i_local], NB = 2 * batch * spb), which sglgpu_spherical_inverse
+ *   then reads; ndst = 2B / spb <= 8.
+ * The caller orders the peers' kernels (e.g. an NCCL barrier on the stream)
+ * before the receive buffers are read. */
+int sglgpu_spherical_forward_to(sglgpu_plan* plan, const double* samples, size_t sample_stride, int shell_begin,
+                                int shell_count, size_t batch, int ndst, double* const* dst, const int* l_bounds,
+                                void* stream);
+int sglgpu_radial_inverse_to(sglgpu_plan* plan, const double* coeffs, int l_begin, int l_end, int shells_per_block,
+                             size_t batch, int ndst, double* const* dst, void* stream);
+/* Peer-mappable device buffers (cudaMalloc + CUDA IPC, 64-byte handles). */
+int sglgpu_device_alloc(size_t bytes, void** ptr);
+int sglgpu_device_free(void* ptr);
+int sglgpu_ipc_export(void* ptr, void* handle64);
+int sglgpu_ipc_open(const void* handle64, void** ptr);
+int sglgpu_ipc_close(void* ptr);
+
 /* Number of kernels the most recent forward/inverse call on this plan launched
  * (for the bench's gpu_launches count). */
 int sglgpu_last_launch_count(const sglgpu_plan* plan);

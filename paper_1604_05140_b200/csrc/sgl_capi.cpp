@@ -1075,4 +1075,108 @@ int sglgpu_radial_inverse(sglgpu_plan* p, const double* coeffs, double* shells, 
     });
 }
 
+// ---------------------------------------------------------------- fused exchange (NVLink peer stores)
+int sglgpu_spherical_forward_to(sglgpu_plan* p, const double* samples, size_t sample_stride, int shell_begin,
+                                int shell_count, size_t batch, int ndst, double* const* dst, const int* l_bounds,
+                                void* stream) {
+    return guarded([&] {
+        check_plan(p);
+        const int B = p->B;
+        if (shell_begin < 0 || shell_count < 1 || shell_begin + shell_count > 2 * B)
+            fail(SGLGPU_EINVAL, "sglgpu_spherical_forward_to: shell range out of bounds");
+        if (ndst < 1 || ndst > sglk::kMaxPeers || !dst || !l_bounds)
+            fail(SGLGPU_EINVAL, "sglgpu_spherical_forward_to: 1..8 destinations with pointers and bounds required");
+        if (l_bounds[0] != 0 || l_bounds[ndst] != B)
+            fail(SGLGPU_EINVAL, "sglgpu_spherical_forward_to: degree bounds must span [0, B)");
+        for (int q = 0; q < ndst; ++q)
+            if (l_bounds[q + 1] < l_bounds[q]) fail(SGLGPU_EINVAL, "sglgpu_spherical_forward_to: bounds must increase");
+        if (batch == 0) return;
+        std::lock_guard<std::mutex> lock(p->mu);
+        set_device(p);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int nb = (int)batch;
+        sglk::Geo g{B, shell_count, nb, 2LL * nb * shell_count};
+        p->G.ensure(2 * (size_t)sglk::g_layout(g));
+        int n = sglk::launch_az_forward(g, samples, 2 * sample_stride, p->G.p, p->d_bcal, p->d_tw, st);
+        ck_launch(n, "az_forward");
+        sglk::PeerDest pd;
+        pd.n = ndst;
+        for (int q = 0; q < ndst; ++q) {
+            pd.bound[q] = l_bounds[q];
+            // rows nu of rank q's degrees land at dst[q] + (nu - nu0_q) * NB
+            pd.base[q] = dst[q] - (long long)l_bounds[q] * l_bounds[q] * g.NB;
+        }
+        pd.bound[ndst] = l_bounds[ndst];
+        auto lt = tiles_for(p, kLegFwd, nb, shell_count, 0, 2 * B);
+        const sglk::SView sv{g.NB, shell_count, 0};
+        int k = sglk::launch_legendre_forward_peers(g, sv, p->G.p, pd, p->d_leg, p->d_leg_off, lt.first, lt.second,
+                                                    st);
+        ck_launch(k, "legendre_forward");
+        p->last_launches = n + k;
+    });
+}
+
+int sglgpu_radial_inverse_to(sglgpu_plan* p, const double* coeffs, int l_begin, int l_end, int shells_per_block,
+                             size_t batch, int ndst, double* const* dst, void* stream) {
+    return guarded([&] {
+        check_plan(p);
+        const int B = p->B;
+        if (l_begin < 0 || l_end > B || l_begin > l_end) fail(SGLGPU_EINVAL, "sglgpu_radial_inverse_to: bad l range");
+        if (shells_per_block < 1 || (2 * B) % shells_per_block != 0)
+            fail(SGLGPU_EINVAL, "sglgpu_radial_inverse_to: shells_per_block must divide 2B");
+        if (ndst != 2 * B / shells_per_block || ndst > sglk::kMaxPeers || !dst)
+            fail(SGLGPU_EINVAL, "sglgpu_radial_inverse_to: one destination per shell block (at most 8) required");
+        if (batch == 0 || l_begin == l_end) return;
+        std::lock_guard<std::mutex> lock(p->mu);
+        set_device(p);
+        const int nb = (int)batch, sc = shells_per_block;
+        sglk::Geo g{B, sc, nb, 2LL * nb * sc};
+        const long long nu0 = (long long)l_begin * l_begin;
+        sglk::PeerDest pd;
+        pd.n = ndst;
+        // rank b's S is [nu][f][i_local] over all nu; the kernel's column offset is relative to nu0
+        for (int b = 0; b < ndst; ++b) pd.base[b] = dst[b] + nu0 * g.NB;
+        auto rt = tiles_for(p, kRadInv, nb, sc, l_begin, l_end);
+        int k = sglk::launch_radial_inverse_peers(g, sglk::RadialBlocks{sc, 0, nu0}, coeffs, pd, p->d_V, p->d_V_off,
+                                                  rt.first, rt.second, static_cast<cudaStream_t>(stream));
+        ck_launch(k, "radial_inverse");
+        p->last_launches = k;
+    });
+}
+
+// Device buffers that peers can map (CUDA IPC), for the fused exchange.
+int sglgpu_device_alloc(size_t bytes, void** ptr) {
+    return guarded([&] {
+        if (!ptr) fail(SGLGPU_EINVAL, "sglgpu_device_alloc: null output");
+        ck(cudaMalloc(ptr, std::max<size_t>(bytes, 16)), "cudaMalloc(peer buffer)");
+    });
+}
+
+int sglgpu_device_free(void* ptr) {
+    return guarded([&] { ck(cudaFree(ptr), "cudaFree(peer buffer)"); });
+}
+
+int sglgpu_ipc_export(void* ptr, void* handle64) {
+    return guarded([&] {
+        if (!ptr || !handle64) fail(SGLGPU_EINVAL, "sglgpu_ipc_export: null argument");
+        cudaIpcMemHandle_t h;
+        ck(cudaIpcGetMemHandle(&h, ptr), "cudaIpcGetMemHandle");
+        static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+        std::memcpy(handle64, &h, sizeof(h));
+    });
+}
+
+int sglgpu_ipc_open(const void* handle64, void** ptr) {
+    return guarded([&] {
+        if (!ptr || !handle64) fail(SGLGPU_EINVAL, "sglgpu_ipc_open: null argument");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle64, sizeof(h));
+        ck(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    });
+}
+
+int sglgpu_ipc_close(void* ptr) {
+    return guarded([&] { ck(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle"); });
+}
+
 }  // extern "C"

@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
+#include <utility>
 
 namespace sglk {
 
@@ -903,6 +904,35 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem_dst, const void* gme
 // predication; shared-memory tiles keep the operand's contiguous dimension
 // innermost (padded) so fills and fragment loads are bank-conflict free.
 // 8-row fragments past M, 8-col fragments past N and k-steps past K are skipped.
+// Multi-GPU variants whose epilogue stores go straight to the peers that own
+// the output rows (NVLink peer stores; the fused exchange of distributed.py).
+struct LegFwdPeers : LegFwd {
+    PeerDest pd;  // rows of degree l go to the owner of l
+    __device__ double* out_row(int pid, int r) const {
+        const int l = am(pid) + (pid & 1) + 2 * r;
+        int q = 0;
+        while (q + 1 < pd.n && l >= pd.bound[q + 1]) ++q;
+        return pd.base[q] + rowC(pid, r);
+    }
+};
+struct RadInvPeers : RadInv {
+    PeerDest pd;  // shell block b goes to its owner (base[b])
+    __device__ double* out_row(int l, int i) const {
+        const int b = i / sb.sc_blk;
+        return pd.base[b] + 2LL * (i - b * sb.sc_blk);
+    }
+};
+
+template <class P, class = void>
+struct has_peers : std::false_type {};
+template <class P>
+struct has_peers<P, std::void_t<decltype(std::declval<const P&>().pd)>> : std::true_type {};
+
+template <class P, class = void>
+struct has_out_row : std::false_type {};
+template <class P>
+struct has_out_row<P, std::void_t<decltype(std::declval<const P&>().out_row(0, 0))>> : std::true_type {};
+
 template <class P, class = void>
 struct has_mirror : std::false_type {};
 template <class P>
@@ -993,7 +1023,9 @@ __device__ __forceinline__ void gemm_epilogue(const P& pr, int pid, int m0, int 
     for (int fm = 0; fm < FM; ++fm) {
         const int row = m0 + wr + fm * 8 + (lane >> 2);
         if (row >= M) continue;
-        double* out = pr.C + pr.rowC(pid, row);
+        double* out;
+        if constexpr (has_out_row<P>::value) out = pr.out_row(pid, row);
+        else out = pr.C + pr.rowC(pid, row);
 #pragma unroll
         for (int fn = 0; fn < 4; ++fn) {
             const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
@@ -1009,6 +1041,10 @@ __device__ __forceinline__ void gemm_epilogue(const P& pr, int pid, int m0, int 
                         make_double2(flip(acc[fm][fn][0], ms), flip(acc[fm][fn][1], ms ^ 0x8000000000000000ULL));
             }
         }
+    }
+    if constexpr (has_peers<P>::value) {
+        // peer (NVLink) stores are made visible system-wide before the kernel retires
+        __threadfence_system();
     }
 }
 
@@ -1320,6 +1356,15 @@ int launch_legendre_forward(const Geo& g, const SView& sv, const double* G, doub
     return gemm_launch<LegFwd>(p, tiles, ntiles, s);
 }
 
+int launch_legendre_forward_peers(const Geo& g, const SView& sv, const double* G, const PeerDest& pd,
+                                  const double* tab, const long long* tab_off, const TileMap* tiles, int ntiles,
+                                  cudaStream_t s) {
+    LegFwdPeers p;
+    static_cast<LegFwd&>(p) = LegFwd{g, tab, tab_off, G, nullptr, sv};
+    p.pd = pd;
+    return gemm_launch<LegFwdPeers>(p, tiles, ntiles, s);
+}
+
 int launch_legendre_inverse(const Geo& g, const SView& sv, const double* S, double* G, const double* tab,
                             const long long* tab_off, const TileMap* tiles, int ntiles, cudaStream_t s) {
     LegInv p{g, tab, tab_off, S, G, sv};
@@ -1338,6 +1383,16 @@ int launch_radial_inverse(const Geo& g, const RadialBlocks& rb, const double* C,
                           cudaStream_t s) {
     RadInv p{g, V, v_off, C, S, degree_offset(g.B + 1), ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
     return gemm_launch<RadInv>(p, tiles, ntiles, s);
+}
+
+int launch_radial_inverse_peers(const Geo& g, const RadialBlocks& rb, const double* C, const PeerDest& pd,
+                                const double* V, const long long* v_off, const TileMap* tiles, int ntiles,
+                                cudaStream_t s) {
+    RadInvPeers p;
+    static_cast<RadInv&>(p) = RadInv{g, V, v_off, C, nullptr, degree_offset(g.B + 1),
+                                     ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
+    p.pd = pd;
+    return gemm_launch<RadInvPeers>(p, tiles, ntiles, s);
 }
 
 }  // namespace sglk

@@ -123,6 +123,26 @@ struct RadialBlocks {
     long long blk_stride;
     long long nu0;
 };
+// Peer destinations for the multi-GPU exchange fused into a stage's epilogue
+// (NVLink peer stores instead of an all-to-all): output row r goes to base[q]
+// for the q with bound[q] <= key(r) < bound[q + 1] (key: l for the Legendre
+// forward, the shell for the radial inverse).  n = 0: the plain output pointer.
+constexpr int kMaxPeers = 8;
+struct PeerDest {
+    int n = 0;
+    int bound[kMaxPeers + 1] = {};
+    double* base[kMaxPeers] = {};
+};
+
+// Legendre forward whose S rows go straight to their owners' shell blocks.
+int launch_legendre_forward_peers(const Geo& g, const SView& sv, const double* G, const PeerDest& pd,
+                                  const double* tab, const long long* tab_off, const TileMap* tiles, int ntiles,
+                                  cudaStream_t s);
+// Radial inverse whose shell blocks go straight to the shells' owners.
+int launch_radial_inverse_peers(const Geo& g, const RadialBlocks& rb, const double* C, const PeerDest& pd,
+                                const double* V, const long long* v_off, const TileMap* tiles, int ntiles,
+                                cudaStream_t s);
+
 int launch_radial_forward(const Geo& g, const RadialBlocks& rb, const double* S, double* C,
                           const double* W, const long long* w_off, const TileMap* tiles, int ntiles,
                           cudaStream_t s);

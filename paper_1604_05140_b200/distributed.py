@@ -20,6 +20,12 @@ inverse
   2. all_to_all back: rank r receives [nu][f][i_local] for its shells
   3. spherical inverse on its shells -> its psi-order slice of the samples
 
+The fused variant (`fsglft_distributed_fused` / `ifsglft_distributed_fused`)
+replaces the all-to-all by NVLink peer stores from the producing kernel's
+epilogue into the consumers' receive buffers (mapped with CUDA IPC,
+`PeerBuffers`), so the exchange overlaps the Legendre / radial-inverse GEMM
+tile by tile; a one-element all_reduce on the stream orders the stores.
+
 Degree ranges are balanced by the radial work (2l+1)(B-l) per degree.
 Batched transforms need none of this: shard whole functions across ranks.
 
@@ -114,6 +120,197 @@ class CudaStages:
             self.plan.handle, shells_local.data_ptr(), out.data_ptr(), 4 * B * B * shell_count, shell_begin,
             shell_count, batch, self._stream(out)))
         return out
+
+
+# ---------------------------------------------------------------- fused exchange over NVLink
+class PeerBuffers:
+    """Receive buffers of the fused exchange and every rank's view of them.
+
+    fwd[q]: rank q's forward receive buffer, W shell blocks [src][nu - nu0_q][f][i_local]
+            (what sglgpu_radial_forward reads in place);
+    inv[b]: rank b's inverse buffer S[nu][f][i_local] over all nu (what
+            sglgpu_spherical_inverse reads).
+    On a node the peers' buffers are mapped with CUDA IPC (`exchange`); `local`
+    builds the same structure for W virtual ranks on one device (tests)."""
+
+    def __init__(self, part: "Partition", batch: int, fwd_ptrs, inv_ptrs, owned, opened):
+        self.part, self.batch = part, batch
+        self.fwd, self.inv = fwd_ptrs, inv_ptrs
+        self._owned, self._opened = owned, opened
+
+    @staticmethod
+    def sizes(part: "Partition", batch: int, q: int):
+        row = batch * part.shells_per_rank  # complex per nu row of a shell block
+        nu0, nu1 = part.nu_range(q)
+        return part.world * (nu1 - nu0) * row * 16, part.B * part.B * row * 16
+
+    @staticmethod
+    def _alloc(L, nbytes):
+        import ctypes
+
+        import paper_1604_05140_b200 as sgl
+
+        p = ctypes.c_void_p()
+        sgl._check(L.sglgpu_device_alloc(nbytes, ctypes.byref(p)))
+        return p.value
+
+    @classmethod
+    def local(cls, part: "Partition", batch: int):
+        import paper_1604_05140_b200 as sgl
+
+        L = sgl.lib()
+        fwd, inv = [], []
+        for q in range(part.world):
+            fb, ib = cls.sizes(part, batch, q)
+            fwd.append(cls._alloc(L, fb))
+            inv.append(cls._alloc(L, ib))
+        return cls(part, batch, fwd, inv, fwd + inv, [])
+
+    @classmethod
+    def exchange(cls, part: "Partition", batch: int, dist, group=None):
+        """Allocates this rank's buffers, all-gathers their IPC handles and maps the peers'."""
+        import ctypes
+
+        import paper_1604_05140_b200 as sgl
+
+        L = sgl.lib()
+        r, W = dist.get_rank(group), part.world
+        fb, ib = cls.sizes(part, batch, r)
+        mine = [cls._alloc(L, fb), cls._alloc(L, ib)]
+        handles = []
+        for p in mine:
+            h = ctypes.create_string_buffer(64)
+            sgl._check(L.sglgpu_ipc_export(p, h))
+            handles.append(h.raw)
+        allh = [None] * W
+        dist.all_gather_object(allh, handles, group=group)
+        fwd, inv, opened = [], [], []
+        for q in range(W):
+            if q == r:
+                fwd.append(mine[0])
+                inv.append(mine[1])
+                continue
+            ptrs = []
+            for h in allh[q]:
+                p = ctypes.c_void_p()
+                sgl._check(L.sglgpu_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)))
+                ptrs.append(p.value)
+                opened.append(p.value)
+            fwd.append(ptrs[0])
+            inv.append(ptrs[1])
+        return cls(part, batch, fwd, inv, mine, opened)
+
+    def close(self):
+        import paper_1604_05140_b200 as sgl
+
+        L = sgl.lib()
+        for p in self._opened:
+            L.sglgpu_ipc_close(p)
+        for p in self._owned:
+            L.sglgpu_device_free(p)
+        self._opened, self._owned = [], []
+
+    def fwd_dst(self, r: int):
+        """Where rank r's shell block starts in every rank's forward receive buffer."""
+        import ctypes
+
+        part, row = self.part, self.batch * self.part.shells_per_rank
+        out = []
+        for q in range(part.world):
+            nu0, nu1 = part.nu_range(q)
+            out.append(self.fwd[q] + r * (nu1 - nu0) * row * 16)
+        return (ctypes.c_void_p * part.world)(*out)
+
+    def inv_dst(self):
+        import ctypes
+
+        return (ctypes.c_void_p * self.part.world)(*self.inv)
+
+
+def _stream_of(t):
+    import torch
+
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def fused_forward_spherical(samples_local, part: "Partition", stages: "CudaStages", peers: PeerBuffers, rank: int,
+                            batch: int = 1):
+    """Step 1 of the fused forward: rank `rank`'s spherical stage, its S rows stored
+    straight into their owners' receive buffers (sglgpu_spherical_forward_to)."""
+    import ctypes
+
+    B, W, sc = part.B, part.world, part.shells_per_rank
+    s0, _ = part.shell_range(rank)
+    bounds = (ctypes.c_int * (W + 1))(*([lr[0] for lr in part.l_ranges] + [B]))
+    stages.sgl._check(stages.L.sglgpu_spherical_forward_to(
+        stages.plan.handle, samples_local.data_ptr(), 4 * B * B * sc, s0, sc, batch, W, peers.fwd_dst(rank), bounds,
+        _stream_of(samples_local)))
+
+
+def fused_forward_radial(part: "Partition", stages: "CudaStages", peers: PeerBuffers, rank: int, coeffs):
+    """Step 2: the radial stage of rank `rank` on its receive buffer (in place) -> its
+    degrees of `coeffs` ([batch, Omega], other entries untouched)."""
+    l0, l1 = part.l_ranges[rank]
+    if l1 > l0:
+        stages.sgl._check(stages.L.sglgpu_radial_forward(
+            stages.plan.handle, peers.fwd[rank], coeffs.data_ptr(), l0, l1, part.shells_per_rank, peers.batch,
+            _stream_of(coeffs)))
+
+
+def fused_inverse_radial(coeffs, part: "Partition", stages: "CudaStages", peers: PeerBuffers, rank: int):
+    """Step 1 of the fused inverse: rank `rank`'s radial stage, each shell block
+    stored straight into the shell owner's S buffer (sglgpu_radial_inverse_to)."""
+    l0, l1 = part.l_ranges[rank]
+    if l1 > l0:
+        stages.sgl._check(stages.L.sglgpu_radial_inverse_to(
+            stages.plan.handle, coeffs.data_ptr(), l0, l1, part.shells_per_rank, peers.batch, part.world,
+            peers.inv_dst(), _stream_of(coeffs)))
+
+
+def fused_inverse_spherical(part: "Partition", stages: "CudaStages", peers: PeerBuffers, rank: int, device):
+    """Step 2: the spherical inverse of rank `rank`'s shells from its S buffer."""
+    import torch
+
+    B, sc = part.B, part.shells_per_rank
+    out = torch.empty(peers.batch * 4 * B * B * sc, dtype=torch.complex128, device=device)
+    stages.sgl._check(stages.L.sglgpu_spherical_inverse(
+        stages.plan.handle, peers.inv[rank], out.data_ptr(), 4 * B * B * sc, part.shell_range(rank)[0], sc,
+        peers.batch, _stream_of(out)))
+    return out
+
+
+def _stream_barrier(dist, group, device):
+    """Orders every rank's peer stores before any rank reads its receive buffer:
+    a one-element all_reduce is stream-ordered on each rank (NCCL)."""
+    import torch
+
+    t = torch.zeros(1, device=device)
+    dist.all_reduce(t, group=group)
+
+
+def fsglft_distributed_fused(samples_local, part: "Partition", stages: "CudaStages", peers: PeerBuffers, dist,
+                             group=None, batch: int = 1):
+    """fsglft_distributed with the all-to-all fused into the Legendre epilogue
+    (NVLink peer stores into the owners' receive buffers; see PeerBuffers)."""
+    import torch
+
+    r = dist.get_rank(group)
+    fused_forward_spherical(samples_local, part, stages, peers, r, batch)
+    _stream_barrier(dist, group, samples_local.device)
+    omega = part.B * (part.B + 1) * (2 * part.B + 1) // 6
+    coeffs = torch.zeros((batch, omega), dtype=torch.complex128, device=samples_local.device)
+    fused_forward_radial(part, stages, peers, r, coeffs)
+    dist.all_reduce(torch.view_as_real(coeffs), group=group)
+    return coeffs
+
+
+def ifsglft_distributed_fused(coeffs, part: "Partition", stages: "CudaStages", peers: PeerBuffers, dist,
+                              group=None, batch: int = 1):
+    """ifsglft_distributed with the all-to-all fused into the radial-inverse epilogue."""
+    r = dist.get_rank(group)
+    fused_inverse_radial(coeffs, part, stages, peers, r)
+    _stream_barrier(dist, group, coeffs.device)
+    return fused_inverse_spherical(part, stages, peers, r, coeffs.device)
 
 
 def _a2a(dist, group, send, send_counts, recv_counts):

@@ -272,10 +272,12 @@ def normwise(a: np.ndarray, ref: np.ndarray) -> float:
     return float(np.abs(a - ref).max() / den) if den > 0 else float(np.abs(a).max())
 
 
-def per_shell(a: np.ndarray, ref: np.ndarray, B: int) -> float:
-    """max over radial shells of the shell-wise normwise error (grids)."""
-    a = a.reshape(-1, 2 * B, 4 * B * B)
-    ref = ref.reshape(-1, 2 * B, 4 * B * B)
+def per_shell(a: np.ndarray, ref: np.ndarray, B: int, shells: int = 0) -> float:
+    """max over radial shells of the shell-wise normwise error (grids; `shells`
+    shells per function, default all 2B)."""
+    sh = shells or 2 * B
+    a = a.reshape(-1, sh, 4 * B * B)
+    ref = ref.reshape(-1, sh, 4 * B * B)
     d = np.abs(a - ref).max(axis=2)
     s = np.abs(ref).max(axis=2)
     s = np.where(s > 0, s, 1.0)

@@ -454,3 +454,65 @@ def test_separated_cross_oracle_rejects_large_bandlimit():
     plan, _ = plan_for(128)
     with pytest.raises(ValueError, match="<= 64"):
         sgl.dsglft_separated(sgl.SampleGrid(128, np.zeros(sample_count(128), complex)), plan)
+
+
+# ---------------------------------------------------------------- fused exchange (peer stores instead of all-to-all)
+@pytest.mark.parametrize("B,W,nb", [(8, 2, 1), (16, 4, 2), (32, 8, 1)])
+def test_fused_exchange_emulated_ranks(B, W, nb):
+    """The peer-store epilogues with W virtual ranks on one device (receive buffers
+    as local allocations): every rank's spherical stage writes its S rows into the
+    owners' buffers, every rank's radial stage reads its own in place -- and the
+    mirror for the inverse.  Ranks run one after another; nothing waits on a peer."""
+    import torch
+
+    from paper_1604_05140_b200.distributed import (CudaStages, Partition, PeerBuffers, fused_forward_radial,
+                                                   fused_forward_spherical, fused_inverse_radial,
+                                                   fused_inverse_spherical)
+
+    plan, orc = plan_for(B)
+    part = Partition.make(B, W)
+    st = CudaStages(plan)
+    peers = PeerBuffers.local(part, nb)
+    try:
+        rng = np.random.default_rng(77 + B)
+        n = coefficient_count(B)
+        c = complex_normal(rng, nb * n).reshape(nb, n)
+        dc = torch.from_numpy(c).cuda()
+        for r in range(W):
+            fused_inverse_radial(dc, part, st, peers, r)
+        torch.cuda.synchronize()
+        sc, nsh = part.shells_per_rank, 4 * B * B
+        slices = [fused_inverse_spherical(part, st, peers, r, dc.device).view(nb, -1) for r in range(W)]
+        torch.cuda.synchronize()
+        for r in range(W):
+            for f in range(nb):
+                g_ref = orc.inverse(c[f])[r * sc * nsh:(r + 1) * sc * nsh]
+                assert per_shell(slices[r][f].cpu().numpy(), g_ref, B, shells=sc) <= TOL
+        for r in range(W):
+            fused_forward_spherical(slices[r].contiguous(), part, st, peers, r, nb)
+        torch.cuda.synchronize()
+        coeffs = torch.zeros((nb, n), dtype=torch.complex128, device="cuda")
+        for r in range(W):
+            fused_forward_radial(part, st, peers, r, coeffs)
+        back = coeffs.cpu().numpy()
+        for f in range(nb):
+            assert normwise(back[f], c[f]) <= TOL
+    finally:
+        peers.close()
+
+
+def test_fused_exchange_ipc_two_processes():
+    """CUDA IPC mapping of the receive buffers + peer-store epilogues across two
+    processes (both on this box's GPU; CPU barriers between the steps)."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, SGL_FUSED_DEVICE="0")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29563",
+                          os.path.join(here, "dist_fused_check.py"), "16", "2"],
+                         capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "fused exchange OK" in out.stdout
