@@ -226,6 +226,8 @@ def main():
                     help="N>1: split one transform by shells / (l, m) (strong scaling, default) "
                          "or run independent replicas (weak scaling)")
     ap.add_argument("--force-split", action="store_true", help="run the split path even at N=1 (testing)")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="split mode: stage exchange fused into the kernels (NVLink peer stores) or NCCL all-to-all")
     ap.add_argument("--real", action="store_true",
                     help="real-valued functions through the real fast path (config C5: f_{nl,-m} = (-1)^m conj f_nlm, "
                          "|f_nlm| ~ exp(-n/8))")
@@ -444,7 +446,9 @@ def split_arm(args, rank, world, local):
 
     import paper_1604_05140_b200 as sgl
     from paper_1604_05140_b200 import workload as wl
-    from paper_1604_05140_b200.distributed import CudaStages, Partition, fsglft_distributed, ifsglft_distributed
+    from paper_1604_05140_b200.distributed import (CudaStages, Partition, PeerBuffers, fsglft_distributed,
+                                                   fsglft_distributed_fused, ifsglft_distributed,
+                                                   ifsglft_distributed_fused)
 
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -458,9 +462,26 @@ def split_arm(args, rank, world, local):
     cin = torch.from_numpy(complex_normal(rng, (nrot, nb, Om))).cuda()
     stream = torch.cuda.current_stream()
 
+    # the exchange: fused into the stage epilogues (peer stores into CUDA-IPC-mapped
+    # receive buffers) unless --exchange nccl or the peers cannot be mapped
+    exchange, why = args.exchange, ""
+    peers = None
+    if exchange == "fused":
+        try:
+            peers = PeerBuffers.exchange(part, nb, dist)
+        except Exception as e:  # noqa: BLE001 -- e.g. IPC not permitted: fall back to the NCCL all-to-all
+            exchange, why = "nccl", f"fused exchange unavailable: {e}"
+        flag = torch.tensor([0.0 if exchange == "fused" else 1.0], device="cuda")
+        dist.all_reduce(flag)  # every rank must take the same path
+        if flag.item() > 0 and exchange == "fused":
+            exchange, why = "nccl", "fused exchange unavailable on a peer"
+    inv_d = (lambda c: ifsglft_distributed_fused(c, part, st, peers, dist, batch=nb)) if exchange == "fused" else \
+        (lambda c: ifsglft_distributed(c, part, st, dist, batch=nb))
+    fwd_d = (lambda x: fsglft_distributed_fused(x, part, st, peers, dist, batch=nb)) if exchange == "fused" else \
+        (lambda x: fsglft_distributed(x, part, st, dist, batch=nb))
+
     def step(s):
-        loc = ifsglft_distributed(cin[s % nrot], part, st, dist, batch=nb)
-        return fsglft_distributed(loc, part, st, dist, batch=nb)
+        return fwd_d(inv_d(cin[s % nrot]).view(nb, -1))
 
     for s in range(args.warmup):
         out = step(s)
@@ -492,9 +513,9 @@ def split_arm(args, rank, world, local):
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(ke):
-        loc = ifsglft_distributed(hc.cuda(non_blocking=True), part, st, dist, batch=nb)
+        loc = inv_d(hc.cuda(non_blocking=True))
         hloc.copy_(loc.view(nb, -1), non_blocking=True)
-        c2 = fsglft_distributed(hloc.cuda(non_blocking=True), part, st, dist, batch=nb)
+        c2 = fwd_d(hloc.cuda(non_blocking=True))
         hout.copy_(c2, non_blocking=True)
         torch.cuda.synchronize()
     e2e_ms = 1000.0 * (time.perf_counter() - t0) / ke
@@ -508,13 +529,16 @@ def split_arm(args, rank, world, local):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: iid complex normal coefficients (numpy PCG64, seed 0)",
         "config": {"workload": f"C3: B={B}, {nb} function(s) per step split over {world} GPUs "
-                               "(shells / degree ranges, NCCL all-to-all)",
+                               "(shells / degree ranges, " + ("exchange fused into the stage epilogues: NVLink "
+                               "peer stores" if exchange == "fused" else "NCCL all-to-all") + ")",
+                   "exchange": exchange + (f" ({why})" if why else ""),
                    "B": B, "batch": nb, "parallelism": f"shell/(l,m) split x{world}",
                    "l2": f"inputs rotated over {nrot} buffers; per-step grid {16 * Ps * nb / 2**20:.0f} MiB > L2"},
         "e2e": {"value": nb / (e2e_ms / 1000.0), "unit": "transforms/s",
                 "h2d_bytes_per_step": 16 * (Om + sc * 4 * B * B) * nb,
                 "d2h_bytes_per_step": 16 * (sc * 4 * B * B + Om) * nb, "ms_per_step": e2e_ms,
-                "api": "paper_1604_05140_b200.distributed.{ifsglft,fsglft}_distributed"},
+                "api": "paper_1604_05140_b200.distributed.{ifsglft,fsglft}_distributed" +
+                       ("_fused" if exchange == "fused" else "")},
         "gpu_launches": 6 * args.steps,
         "transform_fp64_tflops": whole,
         "transform_roofline_frac": whole / FP64_PEAK_TFLOPS,
@@ -525,6 +549,10 @@ def split_arm(args, rank, world, local):
         raise SystemExit(f"bench: distributed round trip failed (normwise error {err:.3e})")
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if peers is not None:
+        torch.cuda.synchronize()
+        dist.barrier()
+        peers.close()
     dist.destroy_process_group()
 
 
