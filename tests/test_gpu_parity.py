@@ -516,3 +516,35 @@ def test_fused_exchange_ipc_two_processes():
                          capture_output=True, text=True, timeout=300, env=env)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "fused exchange OK" in out.stdout
+
+
+def test_large_batch_crosses_workspace_chunks():
+    """B = 32, 1200 functions: more than one ~6 GiB workspace chunk (batch_chunk in
+    sgl_capi.cpp) and several 1 GiB function slices inside each -- every function
+    must still match its own single-function transform."""
+    import torch
+
+    B, nb = 32, 1200
+    plan, orc = plan_for(B)
+    rng = np.random.default_rng(1200)
+    n = coefficient_count(B)
+    c = torch.from_numpy(complex_normal(rng, nb * n).reshape(nb, n)).cuda()
+    g = sgl.ifsglft_batch(plan, c)
+    back = sgl.fsglft_batch(plan, g)
+    torch.cuda.synchronize()
+    assert float((back - c).abs().max() / c.abs().max()) <= TOL
+    for f in (0, 599, 1143, 1144, 1145, nb - 1):
+        gf = sgl.ifsglft_batch(plan, c[f:f + 1].contiguous())
+        assert float((g[f] - gf[0]).abs().max() / gf.abs().max()) <= 1e-14
+    assert per_shell(g[nb - 1].cpu().numpy(), orc.inverse(c[nb - 1].cpu().numpy()), B) <= TOL
+
+
+def test_empty_batch_and_zero_bandlimit_errors():
+    """batch = 0 is a no-op; malformed calls fail with the reference's exception type."""
+    plan, _ = plan_for(4)
+    out = np.zeros((0, coefficient_count(4)), dtype=np.complex128)
+    assert sgl.fsglft_batch(plan, np.zeros((0, sample_count(4)), dtype=np.complex128), out=out).shape[0] == 0
+    with pytest.raises(ValueError):
+        sgl.fsglft(sgl.SampleGrid(4, np.zeros(10, complex)), plan)
+    with pytest.raises(ValueError):
+        sgl.ifsglft(sgl.SglCoefficients(5, np.zeros(coefficient_count(5), complex)), plan)
