@@ -112,9 +112,6 @@ __device__ __forceinline__ int phys(int x) { return x + (x >> 4); }
 #ifndef SGL_AZ_MINB
 #define SGL_AZ_MINB 4
 #endif
-#ifndef SGL_AZI_TW
-#define SGL_AZI_TW 1  // inverse twiddles: 0 plain table in shared memory, 1 per-pass tables from global (93 vs 104 us)
-#endif
 
 #ifndef SGL_AZI_ELEMS
 #define SGL_AZI_ELEMS SGL_AZ_ELEMS  // inverse kernel tile size
@@ -157,14 +154,14 @@ __device__ __forceinline__ void pair_sync() {
 
 // One Stockham pass of radix R on a ring of length N held by T threads.
 // Ns = product of the radices already applied.  twp: this pass's twiddles,
-// twp[(r - 1) Ns + k] = e^{-2 pi i r k / (R Ns)} (PT; consecutive threads read
-// consecutive entries), or the plain table e^{-2 pi i x / N} (!PT).  Unused
-// when Ns = 1.
+// twp[(r - 1) Ns + k] = e^{-2 pi i r k / (R Ns)} (consecutive threads read
+// consecutive entries; a plain e^{-2 pi i x / N} table read at r k N / (R Ns)
+// scatters the reads and cost the forward kernel 10 us).  Unused when Ns = 1.
 // Inputs come from ld(x), outputs go to st(x, v): the first pass of the forward
 // FFT reads global memory directly into registers and the last pass of the
 // inverse writes global memory directly, so only the middle exchanges touch
 // shared memory.  When IN_PLACE, all reads complete (pair_sync) before any write.
-template <int N, int R, int SIGN, bool IN_PLACE, bool PT = true, class Ld, class St>
+template <int N, int R, int SIGN, bool IN_PLACE, class Ld, class St>
 __device__ __forceinline__ void stockham_pass(int Ns, int t, const double2* twp, Ld&& ld, St&& st) {
     constexpr int T = FFTShape<N>::T;
     constexpr int NBF = N / R;          // butterflies in this pass
@@ -183,8 +180,7 @@ __device__ __forceinline__ void stockham_pass(int Ns, int t, const double2* twp,
         if (Ns > 1) {
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                // PT: this pass's table; else twp is the plain table tw[x] = e^{-2 pi i x / N}
-                double2 w = PT ? twp[(r - 1) * Ns + k] : twp[(r * k * (N / (Ns * R))) & (N - 1)];
+                double2 w = twp[(r - 1) * Ns + k];
                 if (SIGN > 0) w.y = -w.y;
                 v[b][r] = cmul(v[b][r], w);
             }
@@ -204,7 +200,7 @@ __device__ __forceinline__ void stockham_pass(int Ns, int t, const double2* twp,
 
 // Full FFT of one ring: first pass reads ld, last pass writes st, middle
 // passes run in place on `ring` (padded).  Ends without a trailing sync.
-template <int N, int SIGN, bool FIRST_IN_PLACE, bool PT = true, class Ld, class St>
+template <int N, int SIGN, bool FIRST_IN_PLACE, class Ld, class St>
 __device__ __forceinline__ void ring_fft_io(double2* ring, int t, const double2* tw, Ld&& ld, St&& st) {
     using S = FFTShape<N>;
     auto rd = [&](int x) { return ring[phys(x)]; };
@@ -225,15 +221,15 @@ __device__ __forceinline__ void ring_fft_io(double2* ring, int t, const double2*
             Ns *= 16;
         }
         pair_sync<N>();
-        const double2* twp = PT ? tw + N : tw;  // per-pass tables follow the N plain twiddles
+        const double2* twp = tw + N;  // per-pass tables follow the N plain twiddles
 #pragma unroll 1
         for (int p = 1; p < NPASS - 1; ++p) {
-            stockham_pass<N, 16, SIGN, true, PT>(Ns, t, twp, rd, wr);
-            if (PT) twp += 15 * Ns;
+            stockham_pass<N, 16, SIGN, true>(Ns, t, twp, rd, wr);
+            twp += 15 * Ns;
             Ns *= 16;
             pair_sync<N>();
         }
-        stockham_pass<N, 16, SIGN, true, PT>(Ns, t, twp, rd, st);
+        stockham_pass<N, 16, SIGN, true>(Ns, t, twp, rd, st);
     }
 }
 
@@ -318,13 +314,7 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
     // the plain twiddle table staged in shared memory under the prologue barrier
     // (measured: 118 us; the forward kernel's per-pass tables from global 120 us,
     // per-pass tables in shared memory 125 us)
-#if SGL_AZI_TW == 1
-    const double2* tw = twg;  // per-pass tables from global
-    double2* rings = smem;
-#else
-    double2* tw = smem;
-    double2* rings = smem + N;
-#endif
+    double2* rings = smem;  // twiddles: per-pass tables from global (93 us; a shared-memory copy 104 us)
     const int tid = threadIdx.x;
     const int jp = blockIdx.y;
     const int s0 = blockIdx.x * S::IG;
@@ -351,9 +341,6 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
         const int p = rowi / N, bin = rowi - p * N;
         rings[(2 * sl + p) * S::STRIDE + phys(bin)] = pv[q];
     }
-#if SGL_AZI_TW != 1
-    for (int x = tid; x < N; x += S::THREADS) tw[x] = __ldg(twg + x);
-#endif
     __syncthreads();
     {
         const int q = tid / S::T, tt = tid - q * S::T;
@@ -370,8 +357,8 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
             const int f = s / g.SC, i = s - f * g.SC;
             dst = X + (size_t)f * fstride + ((size_t)i * N + j) * N;
         }
-        ring_fft_io<N, +1, true, SGL_AZI_TW == 1>(
-            ring, tt, tw,
+        ring_fft_io<N, +1, true>(
+            ring, tt, twg,
             [&](int x) {
                 const double2 e = e_buf[phys(x)], o = o_buf[phys(x)];
                 return mirror ? csub(e, o) : cadd(e, o);
@@ -1278,7 +1265,7 @@ static int az_inv_launch(const Geo& g, const double* G, double* X, size_t fstrid
                          cudaStream_t s) {
     using S = FFTShape<N, SGL_AZI_ELEMS>;
     static_assert(S::IG == FFTShape<N>::IG, "forward and inverse azimuthal tiles must match the G blocking");
-    const size_t smem = sizeof(double2) * ((SGL_AZI_TW == 1 ? 0 : N) + 2 * S::IG * S::STRIDE);
+    const size_t smem = sizeof(double2) * (2 * S::IG * S::STRIDE);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(az_inverse_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
