@@ -113,9 +113,6 @@ struct sglgpu_plan {
     bool profiling = false;
     std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> prof;
     std::vector<cudaEvent_t> ev_pool;
-    // slice pipeline: two internal streams and ordering events (no timing)
-    cudaStream_t aux[2] = {nullptr, nullptr};
-    std::vector<cudaEvent_t> sync_ev;
     // CUDA graphs of whole device-memory transforms, keyed by
     // (direction, batch, in, out, stream); replayed with one launch
     struct GraphEntry {
@@ -287,27 +284,6 @@ int staged(sglgpu_plan* p, int stage, cudaStream_t st, F&& launch) {
     return k;
 }
 
-cudaEvent_t sync_event(sglgpu_plan* p, size_t i) {
-    while (p->sync_ev.size() <= i) {
-        cudaEvent_t e;
-        ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-        p->sync_ev.push_back(e);
-    }
-    return p->sync_ev[i];
-}
-
-void ensure_aux(sglgpu_plan* p) {
-    for (auto& a : p->aux)
-        if (!a) ck(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "cudaStreamCreate");
-}
-
-// Opt-in (SGL_PIPELINE=1): measured slower on B200 at B = 128 (0.92 ms vs 0.63 ms
-// per round trip with 32 MiB slices) -- the per-slice grids are too small and the
-// concurrent kernels compete for the same SMs.  Kept for experiments.
-bool pipelined_slices() {
-    const char* e = std::getenv("SGL_PIPELINE");
-    return e && e[0] == '1';
-}
 
 // Second call with the same graph key?  (The table is bounded: callers that
 // pass fresh buffers every call never reach the graph path.)
@@ -347,7 +323,7 @@ Slices plan_slices(int B, int nb) {
     // Measured on B200 (B = 128, one function): shell slices of 16-64 MiB cost more
     // in per-launch tails than the L2 reuse saves, so a single function runs
     // unsliced; batches are sliced to bound the workspace.
-    double mb = nb == 1 ? (pipelined_slices() ? 32.0 : 0.0) : 1024.0;
+    double mb = nb == 1 ? 0.0 : 1024.0;
     if (const char* e = std::getenv("SGL_G_CHUNK_MB")) mb = std::atof(e);
     const double per_shell = 64.0 * B * B;  // bytes of G per (shell, function)
     const long long cap = std::max(1LL, (long long)(mb * 1048576.0 / per_shell));
@@ -375,60 +351,6 @@ int forward_device(sglgpu_plan* p, const double* X, double* C, int nb, cudaStrea
     const Slices sl = plan_slices(B, nb);
     p->S.ensure((size_t)4 * B * B * B * nb);
     int n = 0, k;
-    if (nb == 1 && sl.count > 1 && pipelined_slices()) {
-        // Two-stream slice pipeline: the azimuthal FFT of slice c+1 (HBM-bound)
-        // runs while the Legendre GEMM of slice c (DMMA-bound) consumes slice c's
-        // G from L2; G is double-buffered (2 x ~32 MiB), so it never streams
-        // through HBM.
-        ensure_aux(p);
-        const int SC = sl.shells;
-        sglk::Geo gc{B, SC, 1, 2LL * SC};
-        const size_t gslice = 2 * (size_t)sglk::g_layout(gc);
-        p->G.ensure(2 * gslice);
-        const sglk::SView sv{2LL * 2 * B, 2 * B, 0};
-        auto lt = tiles_for(p, kLegFwd, 1, SC, 0, 2 * B);
-        cudaStream_t sa = p->aux[0], sb = p->aux[1];
-        size_t ev = 0;
-        cudaEvent_t start = sync_event(p, ev++);
-        ck(cudaEventRecord(start, st), "record");
-        ck(cudaStreamWaitEvent(sa, start, 0), "wait");
-        ck(cudaStreamWaitEvent(sb, start, 0), "wait");
-        std::vector<cudaEvent_t> leg_done(sl.count);
-        for (int c = 0; c < sl.count; ++c) {
-            const int i0 = c * SC;
-            double* gbuf = p->G.p + (c & 1) * gslice;
-            if (c >= 2) ck(cudaStreamWaitEvent(sa, leg_done[c - 2], 0), "wait");
-            k = staged(p, 0, sa, [&] {
-                return sglk::launch_az_forward(gc, X + (size_t)i0 * 2 * 4 * B * B, psi2, gbuf, p->d_bcal, p->d_tw, sa);
-            });
-            ck_launch(k, "az_forward");
-            n += k;
-            cudaEvent_t az_done = sync_event(p, ev++);
-            ck(cudaEventRecord(az_done, sa), "record");
-            ck(cudaStreamWaitEvent(sb, az_done, 0), "wait");
-            sglk::SView v = sv;
-            v.i0 = i0;
-            k = staged(p, 1, sb, [&] {
-                return sglk::launch_legendre_forward(gc, v, gbuf, p->S.p, p->d_leg, p->d_leg_off, lt.first, lt.second, sb);
-            });
-            ck_launch(k, "legendre_forward");
-            n += k;
-            leg_done[c] = sync_event(p, ev++);
-            ck(cudaEventRecord(leg_done[c], sb), "record");
-        }
-        sglk::Geo g{B, 2 * B, 1, 2LL * 2 * B};
-        auto rt = tiles_for(p, kRadFwd, 1, 2 * B, 0, B);
-        k = staged(p, 2, sb, [&] {
-            return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, p->S.p, C, p->d_W, p->d_W_off,
-                                               rt.first, rt.second, sb);
-        });
-        ck_launch(k, "radial_forward");
-        cudaEvent_t end = sync_event(p, ev++);
-        ck(cudaEventRecord(end, sb), "record");
-        ck(cudaStreamWaitEvent(sa, end, 0), "wait");  // keep aux streams ordered with the caller
-        ck(cudaStreamWaitEvent(st, end, 0), "wait");
-        return n + k;
-    }
     if (nb == 1) {
         // shell slices: az + Legendre per slice into the full S, then radial once
         const int SC = sl.shells;
@@ -494,57 +416,6 @@ int inverse_device(sglgpu_plan* p, const double* C, double* X, int nb, cudaStrea
     const Slices sl = plan_slices(B, nb);
     p->S.ensure((size_t)4 * B * B * B * nb);
     int n = 0, k;
-    if (nb == 1 && sl.count > 1 && pipelined_slices()) {
-        // mirror of the forward pipeline: Legendre inverse of slice c+1 (DMMA)
-        // overlaps the inverse FFT of slice c (HBM); G double-buffered in L2
-        ensure_aux(p);
-        cudaStream_t sa = p->aux[0], sb = p->aux[1];
-        size_t ev = 0;
-        cudaEvent_t start = sync_event(p, ev++);
-        ck(cudaEventRecord(start, st), "record");
-        ck(cudaStreamWaitEvent(sa, start, 0), "wait");
-        ck(cudaStreamWaitEvent(sb, start, 0), "wait");
-        sglk::Geo g{B, 2 * B, 1, 2LL * 2 * B};
-        auto rt = tiles_for(p, kRadInv, 1, 2 * B, 0, B);
-        k = staged(p, 3, sb, [&] {
-            return sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, 0}, C, p->S.p, p->d_V, p->d_V_off,
-                                               rt.first, rt.second, sb);
-        });
-        ck_launch(k, "radial_inverse");
-        n += k;
-        const int SC = sl.shells;
-        sglk::Geo gc{B, SC, 1, 2LL * SC};
-        const size_t gslice = 2 * (size_t)sglk::g_layout(gc);
-        p->G.ensure(2 * gslice);
-        auto lt = tiles_for(p, kLegInv, 1, SC, 0, 2 * B);
-        std::vector<cudaEvent_t> az_done(sl.count);
-        for (int c = 0; c < sl.count; ++c) {
-            const int i0 = c * SC;
-            double* gbuf = p->G.p + (c & 1) * gslice;
-            if (c >= 2) ck(cudaStreamWaitEvent(sb, az_done[c - 2], 0), "wait");
-            const sglk::SView v{2LL * 2 * B, 2 * B, i0};
-            k = staged(p, 4, sb, [&] {
-                return sglk::launch_legendre_inverse(gc, v, p->S.p, gbuf, p->d_leg, p->d_leg_off, lt.first, lt.second, sb);
-            });
-            ck_launch(k, "legendre_inverse");
-            n += k;
-            cudaEvent_t leg_done = sync_event(p, ev++);
-            ck(cudaEventRecord(leg_done, sb), "record");
-            ck(cudaStreamWaitEvent(sa, leg_done, 0), "wait");
-            k = staged(p, 5, sa, [&] {
-                return sglk::launch_az_inverse(gc, gbuf, X + (size_t)i0 * 2 * 4 * B * B, psi2, p->d_tw, sa);
-            });
-            ck_launch(k, "az_inverse");
-            n += k;
-            az_done[c] = sync_event(p, ev++);
-            ck(cudaEventRecord(az_done[c], sa), "record");
-        }
-        cudaEvent_t end = sync_event(p, ev++);
-        ck(cudaEventRecord(end, sa), "record");
-        ck(cudaStreamWaitEvent(sb, end, 0), "wait");
-        ck(cudaStreamWaitEvent(st, end, 0), "wait");
-        return n;
-    }
     if (nb == 1) {
         sglk::Geo g{B, 2 * B, 1, 2LL * 2 * B};
         auto rt = tiles_for(p, kRadInv, 1, 2 * B, 0, B);
@@ -902,10 +773,7 @@ int sglgpu_plan_destroy(sglgpu_plan* p) {
         cudaEventDestroy(b);
     }
     for (auto e : p->ev_pool) cudaEventDestroy(e);
-    for (auto e : p->sync_ev) cudaEventDestroy(e);
     for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second.exec);
-    for (auto a : p->aux)
-        if (a) cudaStreamDestroy(a);
     p->G.release();
     p->S.release();
     p->in.release();
