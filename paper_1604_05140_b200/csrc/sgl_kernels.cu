@@ -264,10 +264,10 @@ az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2*
     const int s0 = blockIdx.x * S::IG;
     const int nshell = g.batch * g.SC;
     {
-        // twiddles are read straight from the (L1-resident) global table: no
-        // staging barrier in front of the ring loads (108 -> 106 us at B = 128;
-        // the inverse keeps its shared-memory copy, staged under its prologue
-        // barrier -- global twiddles there measured 118 -> 129 us)
+        // twiddles come straight from the (L1-resident) per-pass global tables;
+        // the ring loads go straight to registers (staging small-N rings through
+        // shared memory for longer coalesced runs measured slower: B = 32 7.8 ->
+        // 9.3 ms, B = 64 0.81 -> 0.97 ms for the C5 / C2 batches)
         const int q = tid / S::T, tt = tid - q * S::T;
         const int s = s0 + (q >> 1);
         const int j = (q & 1) ? (N - 1 - jp) : jp;
