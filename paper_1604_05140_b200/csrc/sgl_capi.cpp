@@ -218,7 +218,18 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
                         (std::min(bm, M) + 7) / 8 * 8 * ((std::min<long long>(bn, half) + 7) / 8 * 8) * kk});
         ntiles += (long long)tm * halves * tn;
     }
-    if (ntiles <= sglk::kMaxProblems) {  // one entry per tile, exact per-tile work
+    // n-blocks per CTA for kinds built with sequences: short-K problems amortize
+    // the CTA prologue and overlap each tile's epilogue with the next tile's
+    // loads (LegInv, B = 128: 114.5 -> 112.6 us with 2; B = 64 x 64: 652 -> 588 us
+    // and B = 32 x 4096: 4378 -> 3672 us with 4)
+    int seq = 1;
+    if (kind == kLegInv) {
+        const int kmax = (B + 1) / 2;  // the Legendre inverse's K (degrees of one parity)
+        // measured: B = 32, 64: 4; B = 128: 2; B = 256: the one-tile kernel (seq 2: +4%)
+        seq = kmax <= 32 ? 4 : kmax <= 64 ? 2 : 1;
+        if (const char* e = std::getenv("SGL_SEQ")) seq = std::max(1, std::min(8, std::atoi(e)));
+    }
+    if (seq == 1 && ntiles <= sglk::kMaxProblems) {  // one entry per tile, exact per-tile work
         std::vector<Entry> per;
         for (const Entry& e : ents) {
             int M, N, K;
@@ -239,13 +250,14 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
     auto* tm = new sglk::TileMap{};
     long long n = 0;
     tm->nprob = (int)ents.size();
+    tm->seq = seq;
     for (size_t q = 0; q < ents.size(); ++q) {
         const Entry& e = ents[q];
         tm->first[q] = (int)n;
-        tm->info[q] = e.pid | e.lwm << 16 | (e.halves - 1) << 18 | e.h0 << 19 | e.mi0 << 20;
+        tm->info[q] = e.pid | e.lwm << 16 | (e.halves - 1) << 18 | e.h0 << 19 | e.mi0 << 20 | (seq - 1) << 26;
         tm->tn[q] = e.tn;
         tm->ni0[q] = e.ni0;
-        n += (long long)e.tm * e.halves * e.tn;
+        n += (long long)e.tm * e.halves * ((e.tn + seq - 1) / seq);
     }
     if (n >= (1LL << 31) - 1) fail(SGLGPU_EINVAL, "tile table: too many tiles");
     tm->first[ents.size()] = (int)n;

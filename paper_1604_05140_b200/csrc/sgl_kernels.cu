@@ -672,7 +672,8 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
     static constexpr int GEMM_BK = SGL_BK_##NAME > 0 ? SGL_BK_##NAME : DBK; \
     static constexpr int GEMM_ST = SGL_ST_##NAME > 0 ? SGL_ST_##NAME : DST; \
     static constexpr int GEMM_MINB = SGL_MINB_##NAME > 0 ? SGL_MINB_##NAME : DMINB; \
-    static constexpr int GEMM_MAXWM = SGL_MAXWM_##NAME;
+    static constexpr int GEMM_MAXWM = SGL_MAXWM_##NAME; \
+    static constexpr bool GEMM_SEQ = false;
 
 // --- problem kinds
 // Legendre forward: prob = 2|m| + p.  rows l = |m|+p+2r, K = B (j'), cols n' = sgn*NB + n.
@@ -902,6 +903,9 @@ struct LegFwdPeers : LegFwd {
         return pd.base[q] + rowC(pid, r);
     }
 };
+struct LegInvSeq : LegInv {  // CTAs run TileMap::seq consecutive n-blocks
+    static constexpr bool GEMM_SEQ = true;
+};
 struct RadInvPeers : RadInv {
     PeerDest pd;  // shell block b goes to its owner (base[b])
     __device__ double* out_row(int l, int i) const {
@@ -1084,6 +1088,9 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
     const double* b_ptr[C::BQ];
     int b_k[C::BQ], b_so[C::BQ];
     unsigned b_ok = 0;
+    constexpr bool SEQ = P::GEMM_SEQ;
+    static_assert(!SEQ || P::B_COL_AFFINE, "n-block sequences shift affine B columns");
+    int b_bc[SEQ ? C::BQ : 1];
     {
         const long long bcol0 = P::B_COL_AFFINE ? pr.colB(pid, n0) : 0;
 #pragma unroll
@@ -1099,6 +1106,7 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
                 b_k[q] = e / (BN / 2);
             }
             b_so[q] = b_k[q] * C::LDB + bc;
+            if constexpr (SEQ) b_bc[q] = bc;
             const bool ok = n0 + bc < N;
             b_ok |= (ok ? 1u : 0u) << q;
             const long long col = !ok ? 0 : (P::B_COL_AFFINE ? bcol0 + bc : pr.colB(pid, n0 + bc));
@@ -1107,11 +1115,18 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
         }
     }
 
-    auto issue = [&](int c) {
+    // SEQ: the CTA runs t.nseq consecutive n-blocks of the problem as one
+    // pipelined sequence of chunks v = tile * nch + c (A is the same for all of
+    // them; B columns shift by BN per tile), so each tile's epilogue overlaps the
+    // next tile's loads and the CTA prologue is paid once per sequence.
+    auto issue = [&](int v) {
+        const int tv = SEQ ? v / nch : 0;
+        const int c = v - tv * nch;
+        const int cs = tv * BN;  // column shift of tile tv
 #ifdef SGL_GEMM_NOLOAD  // experiment: compute-only timing (wrong results)
-        if (c > 0) { cp_async_commit(); return; }
+        if (v > 0) { cp_async_commit(); return; }
 #endif
-        double* as = smem + (c % ST) * C::STAGE;
+        double* as = smem + (v % ST) * C::STAGE;
         double* bs = as + C::A_STAGE;
         const int k0 = c * BK;
         const long long a_adv = (long long)k0 * a_sk;
@@ -1142,8 +1157,10 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
 #pragma unroll
         for (int q = 0; q < C::BQ; ++q) {
             const int k = k0 + b_k[q];
-            const bool ok = ((b_ok >> q) & 1u) && k < K;
-            const double* src = b_step > 0 ? b_ptr[q] + b_adv : b_ptr[q] + pr.rowB(pid, k);
+            bool ok;
+            if constexpr (SEQ) ok = n0 + cs + b_bc[q] < N && k < K;
+            else ok = ((b_ok >> q) & 1u) && k < K;
+            const double* src = (b_step > 0 ? b_ptr[q] + b_adv : b_ptr[q] + pr.rowB(pid, k)) + cs;
             cp_async16_zfill(bs + b_so[q], ok ? src : pr.Bm, ok);
         }
         cp_async_commit();
@@ -1157,6 +1174,42 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+    if constexpr (SEQ) {
+        const int nv = t.nseq * nch;
+        int fna = fn_active;
+#pragma unroll
+        for (int v = 0; v < ST - 1; ++v) {
+            if (v < nv) issue(v);
+            else cp_async_commit();
+        }
+        int c = 0, tv = 0;
+        for (int v = 0; v < nv; ++v) {
+            cp_async_wait_group<ST - 2>();
+            __syncthreads();
+            if (v + ST - 1 < nv) issue(v + ST - 1);
+            else cp_async_commit();
+            const double* as = smem + (v % ST) * C::STAGE;
+            const double* bs = as + C::A_STAGE;
+            const int ksteps = min(BK, K - c * BK);
+            if (ksteps == BK) {
+                dispatch_chunk<P, WM, true>(fm_active, fna, as, bs, acc, BK, wr, wc, lane);
+            } else {
+                dispatch_chunk<P, WM, false>(fm_active, fna, as, bs, acc, ksteps, wr, wc, lane);
+            }
+            if (++c == nch) {  // tile tv complete: write it, reset for tile tv + 1
+                gemm_epilogue<P, WM>(pr, pid, m0, n0 + tv * BN, M, N, acc, wr, wc, lane);
+#pragma unroll
+                for (int i = 0; i < FM; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+                c = 0;
+                ++tv;
+                fna = max(0, min(4, (N - (n0 + tv * BN) - wc + 7) >> 3));
+            }
+        }
+        cp_async_wait_group<0>();
+        return;
+    }
 #pragma unroll
     for (int c = 0; c < ST - 1; ++c) {
         if (c < nch) issue(c);
@@ -1187,6 +1240,7 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
 
 // Tile of this CTA from the launch's problem table (kernel parameter space: a
 // handful of constant-cache reads instead of a dependent global load at CTA start).
+template <int SEQ>
 __device__ __forceinline__ Tile decode_tile(const TileMap& tm, long long NB) {
     const int b = blockIdx.x;
     int lo = 0, hi = tm.nprob - 1;  // last entry with first[q] <= b
@@ -1198,16 +1252,26 @@ __device__ __forceinline__ Tile decode_tile(const TileMap& tm, long long NB) {
     }
     const int info = tm.info[lo], tn = tm.tn[lo], local = b - tm.first[lo];
     const int lwm = (info >> 16) & 3, halves = ((info >> 18) & 1) + 1;
+    if constexpr (SEQ) {  // CTAs run groups of `seq` consecutive n-blocks (seq chosen per launch)
+        const int seq = ((info >> 26) & 7) + 1;
+        const int tg = (tn + seq - 1) / seq;
+        const int per_m = halves * tg;
+        const int mi = local / per_m, rest = local - mi * per_m;
+        const int hl = rest / tg, gi = rest - hl * tg, h = hl + ((info >> 19) & 1);
+        const int ni = gi * seq + tm.ni0[lo];
+        return Tile{info & 0xffff, (mi + ((info >> 20) & 63)) * (32 << lwm), (int)(h * NB) + ni * (128 >> lwm),
+                    1 << lwm, min(seq, tn - gi * seq)};
+    }
     const int per_m = halves * tn;
     const int mi = local / per_m, rest = local - mi * per_m;
     const int hl = rest / tn, ni = rest - hl * tn + tm.ni0[lo], h = hl + ((info >> 19) & 1);
-    return Tile{info & 0xffff, (mi + (info >> 20)) * (32 << lwm), (int)(h * NB) + ni * (128 >> lwm), 1 << lwm};
+    return Tile{info & 0xffff, (mi + (info >> 20)) * (32 << lwm), (int)(h * NB) + ni * (128 >> lwm), 1 << lwm, 1};
 }
 
 template <class P>
 __global__ void __launch_bounds__(128, P::GEMM_MINB) gemm_dmma_kernel(P pr, const __grid_constant__ TileMap tm) {
     extern __shared__ __align__(16) double gsm[];
-    const Tile t = decode_tile(tm, pr.g.NB);
+    const Tile t = decode_tile<P::GEMM_SEQ>(tm, pr.g.NB);
     switch (t.pad) {  // warp layout chosen per tile (the host keeps wm <= P::GEMM_MAXWM)
         case 1: gemm_tile<P, 1>(pr, t, gsm); break;
         case 2: if constexpr (P::GEMM_MAXWM >= 2) gemm_tile<P, 2>(pr, t, gsm); break;
@@ -1355,6 +1419,11 @@ int launch_legendre_forward_peers(const Geo& g, const SView& sv, const double* G
 int launch_legendre_inverse(const Geo& g, const SView& sv, const double* S, double* G, const double* tab,
                             const long long* tab_off, const TileMap* tiles, int ntiles, cudaStream_t s) {
     LegInv p{g, tab, tab_off, S, G, sv};
+    if (ntiles > 0 && tiles->seq > 1) {
+        LegInvSeq q;
+        static_cast<LegInv&>(q) = p;
+        return gemm_launch<LegInvSeq>(q, tiles, ntiles, s);
+    }
     return gemm_launch<LegInv>(p, tiles, ntiles, s);
 }
 

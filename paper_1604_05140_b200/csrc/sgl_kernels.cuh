@@ -13,6 +13,7 @@ namespace sglk {
 // Tile descriptor for the grouped DMMA contraction: {problem, m0, n0, warp layout wm}.
 struct Tile {
     int prob, m0, n0, pad;
+    int nseq;  // consecutive n-blocks this CTA runs (kinds with GEMM_SEQ > 1)
 };
 
 // Tiles of one grouped contraction, passed by value in kernel parameter space.
@@ -29,6 +30,7 @@ struct Tile {
 constexpr int kMaxProblems = SGL_MAX_PROBLEMS;
 struct TileMap {
     int nprob;
+    int seq;  // n-blocks per CTA (1: one tile per CTA)
     int first[kMaxProblems + 1];
     int info[kMaxProblems];  // pid | log2(wm) << 16 | (halves - 1) << 18 | h0 << 19 | mi0 << 20
     int tn[kMaxProblems];    // n-blocks per half
@@ -42,6 +44,9 @@ constexpr int tile_cols(int wm) { return 128 / wm; }
 // Largest wm each kind's kernel is built for (its shared-memory ring is sized for
 // the largest stage it can see): the Legendre-forward problems have M <= B/2 + 1
 // rows, so 128-row tiles never win there and its ring is sized for wm <= 2.
+// The Legendre inverse (B columns affine in n) has a second kernel whose CTAs run
+// several consecutive n-blocks of a problem as one pipelined chunk sequence; the
+// count is chosen per launch (TileMap::seq) and seq > 1 selects that kernel.
 #ifndef SGL_MAXWM_LEGFWD
 #define SGL_MAXWM_LEGFWD 2
 #endif
