@@ -390,10 +390,12 @@ def main():
     try:
         with open(os.path.join(REPO, "profiles", "r01_traffic.json")) as f:
             tr = json.load(f)["bytes"]
-        kname = {0: f"void az_forward_kernel<{2 * B}>", 1: "void gemm_dmma_kernel<LegFwd>",
-                 2: "void gemm_dmma_kernel<RadFwd>", 3: "void gemm_dmma_kernel<RadInv>",
-                 4: "void gemm_dmma_kernel<LegInv>", 5: f"void az_inverse_kernel<{2 * B}>"}[dom]
-        if B == 128 and nb == 1 and kname in tr:
+        knames = {0: [f"void az_forward_kernel<{2 * B}>"], 1: ["void gemm_dmma_kernel<LegFwd>"],
+                  2: ["void gemm_dmma_kernel<RadFwd>"], 3: ["void gemm_dmma_kernel<RadInv>"],
+                  4: ["void gemm_dmma_kernel<LegInvSeq>", "void gemm_dmma_kernel<LegInv>"],
+                  5: [f"void az_inverse_kernel<{2 * B}>"]}[dom]
+        kname = next((k for k in knames if k in tr), None)
+        if B == 128 and nb == 1 and kname is not None:
             roof["traffic"] = tr[kname]
             roof["traffic_source"] = "profiles/r01_ncu_full.txt (dram__bytes_read.sum + dram__bytes_write.sum)"
     except (OSError, KeyError, ValueError):
