@@ -332,10 +332,12 @@ struct Slices {
 };
 
 Slices plan_slices(int B, int nb) {
-    // Measured on B200 (B = 128, one function): shell slices of 16-64 MiB cost more
-    // in per-launch tails than the L2 reuse saves, so a single function runs
-    // unsliced; batches are sliced to bound the workspace.
-    double mb = nb == 1 ? 0.0 : 1024.0;
+    // Measured on B200: slices cost more in per-launch tails than the L2 reuse
+    // saves -- B = 128, one function: 16-64 MiB shell slices, 1800 -> 1374
+    // transforms/s; B = 64 x 64 and B = 32 x 4096: 1 GiB function slices 2%
+    // slower than none -- so transforms run unsliced (the workspace is bounded
+    // by batch_chunk).  SGL_G_CHUNK_MB sets a slice size for experiments.
+    double mb = 0.0;
     if (const char* e = std::getenv("SGL_G_CHUNK_MB")) mb = std::atof(e);
     const double per_shell = 64.0 * B * B;  // bytes of G per (shell, function)
     const long long cap = std::max(1LL, (long long)(mb * 1048576.0 / per_shell));
