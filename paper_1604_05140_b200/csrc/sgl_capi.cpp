@@ -313,10 +313,15 @@ bool use_graphs(int B, size_t batch) {
     return (double)B * B * B * (double)batch <= 128.0 * 128 * 128 * 2;
 }
 
-// Largest batch chunk whose G + S workspaces stay under ~6 GiB.
+// Largest batch chunk whose G + S workspaces stay under the budget
+// (SGL_WORKSPACE_GB, default 6 GiB).
 size_t batch_chunk(int B, size_t batch) {
     const size_t per = (size_t)(16 + 4) * B * B * B * sizeof(double);  // G + S per function
-    const size_t budget = (size_t)6 << 30;
+    static const size_t budget = [] {
+        const char* e = std::getenv("SGL_WORKSPACE_GB");
+        const double gb = e ? std::atof(e) : 6.0;
+        return (size_t)(std::max(0.25, gb) * (double)(1ULL << 30));
+    }();
     return std::max<size_t>(1, std::min(batch, budget / per));
 }
 
