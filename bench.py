@@ -366,10 +366,14 @@ def main():
     for s in range(6):
         if stage_n[s]:
             t_ms = stage_ms[s] / args.steps  # per step (a stage may be split into several launches)
+            tf = work[s][0] * nb / (t_ms * 1e-3) / 1e12
+            gb = work[s][1] * nb / (t_ms * 1e-3) / 1e9
+            hbm = s in (0, 5)  # the azimuthal kernels are HBM-bound, the contractions FP64-bound
             stage_info[wl.STAGE_NAMES[s]] = {
                 "ms": round(t_ms, 5), "launches_per_step": int(stage_n[s]) // args.steps,
-                "tflops": round(work[s][0] * nb / (t_ms * 1e-3) / 1e12, 3),
-                "gbs": round(work[s][1] * nb / (t_ms * 1e-3) / 1e9, 1),
+                "tflops": round(tf, 3), "gbs": round(gb, 1),
+                "bound": "hbm" if hbm else "tensor",
+                "roofline_frac": round(gb / peaks["hbm_gbs"] if hbm else tf / FP64_PEAK_TFLOPS, 3),
                 "share": round(stage_ms[s] / stage_ms.sum(), 4),
             }
     if dom in (0, 5):
