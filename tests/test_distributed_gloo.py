@@ -74,3 +74,25 @@ def test_partition_balances_radial_work():
         assert p.shells_per_rank * W == 2 * B
     with pytest.raises(ValueError):
         Partition.make(3, 4)
+
+
+def test_peer_buffer_layout_matches_radial_blocks():
+    """The fused exchange's destinations (PeerBuffers.fwd_dst) place source rank r's
+    shell block where sglgpu_radial_forward reads block r of the owner's receive
+    buffer: [src][nu - nu0_q][f][i_local], blk_stride = (nu1 - nu0) * row."""
+    from paper_1604_05140_b200.distributed import PeerBuffers
+
+    B, W, batch = 16, 4, 3
+    part = Partition.make(B, W)
+    row = batch * part.shells_per_rank
+    fwd = [(1 << 40) + (q << 32) for q in range(W)]  # fake device addresses
+    peers = PeerBuffers(part, batch, fwd, [0] * W, [], [])
+    for r in range(W):
+        dst = list(peers.fwd_dst(r))
+        for q in range(W):
+            nu0, nu1 = part.nu_range(q)
+            assert dst[q] == fwd[q] + r * (nu1 - nu0) * row * 16
+    for q in range(W):
+        fb, ib = PeerBuffers.sizes(part, batch, q)
+        nu0, nu1 = part.nu_range(q)
+        assert fb == W * (nu1 - nu0) * row * 16 and ib == B * B * row * 16
