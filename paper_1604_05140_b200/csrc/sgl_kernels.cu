@@ -710,6 +710,7 @@ struct LegFwd {
     SView sv;
     static constexpr bool A_KCONTIG = true;
     static constexpr bool B_KCONTIG = false;
+    static constexpr int B_ROW_TABLE = 0;  // rowB affine in k: pointer increments
     __device__ int am(int pid) const { return pid >> 1; }
     __device__ int M(int pid) const { const int r = g.B - am(pid) - (pid & 1); return r > 0 ? (r + 1) / 2 : 0; }
     __device__ int N(int pid) const { return am(pid) == 0 || g.real ? (int)g.NB : 2 * (int)g.NB; }
@@ -746,6 +747,7 @@ struct LegInv {
     SView sv;
     static constexpr bool A_KCONTIG = false;
     static constexpr bool B_KCONTIG = false;
+    static constexpr int B_ROW_TABLE = 128;  // K <= (B + 1) / 2 rows, B <= 256
     __device__ int am(int pid) const { return pid >> 1; }
     __device__ int M(int) const { return g.B; }
     __device__ int N(int pid) const { return am(pid) == 0 || g.real ? (int)g.NB : 2 * (int)g.NB; }
@@ -798,6 +800,7 @@ struct RadFwd {
     ShellBlocks sb;
     static constexpr bool A_KCONTIG = true;
     static constexpr bool B_KCONTIG = true;
+    static constexpr int B_ROW_TABLE = 512;  // K = 2B rows (shell blocks: not affine under the split)
     __device__ int M(int l) const { return g.B - l; }
     __device__ int mw(int l) const { return g.real ? l + 1 : 2 * l + 1; }  // orders per (l, f)
     __device__ int N(int l) const { return mw(l) * g.batch * 2; }
@@ -847,6 +850,7 @@ struct RadInv {
     ShellBlocks sb;
     static constexpr bool A_KCONTIG = false;  // V_l stored [n][i]: rows i contiguous
     static constexpr bool B_KCONTIG = false;
+    static constexpr int B_ROW_TABLE = 256;  // K = B - l rows
     __device__ int M(int) const { return 2 * g.B; }
     __device__ int mw(int l) const { return g.real ? l + 1 : 2 * l + 1; }
     __device__ int N(int l) const { return mw(l) * g.batch * 2; }
@@ -947,7 +951,7 @@ constexpr size_t gemm_smem_bytes() {
     constexpr int s1 = GemmCfg<P, 1>::STAGE, s2 = P::GEMM_MAXWM >= 2 ? GemmCfg<P, 2>::STAGE : 0,
                   s4 = P::GEMM_MAXWM >= 4 ? GemmCfg<P, 4>::STAGE : 0;
     constexpr int m = s1 > s2 ? (s1 > s4 ? s1 : s4) : (s2 > s4 ? s2 : s4);
-    return sizeof(double) * P::GEMM_ST * m;
+    return sizeof(double) * (P::GEMM_ST * m + P::B_ROW_TABLE);  // + the B row-offset table
 }
 
 // One k-chunk of MMAs for a warp with FA x NA active 8 x 8 fragments.
@@ -976,6 +980,10 @@ __device__ __forceinline__ void mma_chunk(const double* as, const double* bs, do
 template <class P, int WM, bool FULL>
 __device__ __forceinline__ void dispatch_chunk(int fa, int na, const double* as, const double* bs,
                                                double (&acc)[4][4][2], int ksteps, int wr, int wc, int lane) {
+    if (fa == 4 && na == 4) {  // the common full-fragment case first
+        mma_chunk<P, WM, 4, 4, FULL>(as, bs, acc, ksteps, wr, wc, lane);
+        return;
+    }
 #define SGL_MMA_CASE(A_, N_) \
     case A_ * 8 + N_: mma_chunk<P, WM, A_, N_, FULL>(as, bs, acc, ksteps, wr, wc, lane); break;
     switch (fa * 8 + na) {
@@ -1084,7 +1092,19 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
             a_ptr[u] = ok ? pr.A + abase + (long long)row * a_sr + (long long)k * a_sk : pr.A;
         }
     }
-    const long long b_step = pr.b_kstep(pid);  // > 0: rowB is affine in k with this stride
+    // B rows: affine kinds (B_ROW_TABLE == 0) advance their pointers by a fixed
+    // stride per chunk; the others read row k's offset from a per-tile table in
+    // shared memory (rowB(pid, k) for k < K, 0 past K), built once here, so a
+    // chunk issue is one LDS + one 64-bit add per transfer instead of the row map
+    // (quadratic / cubic in k for the Legendre-inverse / radial-inverse rows).
+    constexpr bool TAB = P::B_ROW_TABLE > 0;
+    const long long b_step = TAB ? 0 : pr.b_kstep(pid);
+    long long* ktab = reinterpret_cast<long long*>(smem + ST * C::STAGE);
+    if constexpr (TAB) {
+        const int kr = nch * BK;  // <= P::B_ROW_TABLE (K <= the kind's maximum)
+        for (int k = tid; k < kr; k += 128) ktab[k] = k < K ? pr.rowB(pid, k) : 0;
+        __syncthreads();
+    }
     const double* b_ptr[C::BQ];
     int b_k[C::BQ], b_so[C::BQ];
     unsigned b_ok = 0;
@@ -1110,9 +1130,17 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
             const bool ok = n0 + bc < N;
             b_ok |= (ok ? 1u : 0u) << q;
             const long long col = !ok ? 0 : (P::B_COL_AFFINE ? bcol0 + bc : pr.colB(pid, n0 + bc));
-            // with an affine row map the k = b_k[q] row offset is folded in here
-            b_ptr[q] = pr.Bm + col + (b_step > 0 ? pr.rowB(pid, 0) + (long long)b_k[q] * b_step : 0);
+            // affine rows: the k = b_k[q] row offset is folded in here
+            b_ptr[q] = pr.Bm + col + (TAB ? 0 : pr.rowB(pid, 0) + (long long)b_k[q] * b_step);
         }
+    }
+    // A is affine in k for every kind: per-chunk advance k0 * a_sk.  Byte counts
+    // of the 16-byte units for chunks entirely inside K (no k check needed).
+    int a_nb[AU];
+#pragma unroll
+    for (int u = 0; u < AU; ++u) {
+        const bool o1 = (a_ok >> u) & 1u, o2 = P::A_KCONTIG ? o1 : ((a_ok2 >> u) & 1u);
+        a_nb[u] = o1 ? (o2 ? 16 : 8) : 0;
     }
 
     // SEQ: the CTA runs t.nseq consecutive n-blocks of the problem as one
@@ -1129,12 +1157,16 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
         double* as = smem + (v % ST) * C::STAGE;
         double* bs = as + C::A_STAGE;
         const int k0 = c * BK;
+        const bool kfull = k0 + BK <= K;
         const long long a_adv = (long long)k0 * a_sk;
 #pragma unroll
         for (int u = 0; u < AU; ++u) {
             const double* src = a_ptr[u] + a_adv;
             bool ok1, ok2;  // the unit's two elements
-            if (P::A_KCONTIG) {
+            if (kfull) {
+                ok1 = a_nb[u] >= 8;
+                ok2 = a_nb[u] == 16;
+            } else if (P::A_KCONTIG) {
                 const int kv = K - (k0 + a_k[u]);
                 ok1 = ((a_ok >> u) & 1u) && kv >= 1;
                 ok2 = ((a_ok >> u) & 1u) && kv >= 2;
@@ -1158,9 +1190,9 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
         for (int q = 0; q < C::BQ; ++q) {
             const int k = k0 + b_k[q];
             bool ok;
-            if constexpr (SEQ) ok = n0 + cs + b_bc[q] < N && k < K;
-            else ok = ((b_ok >> q) & 1u) && k < K;
-            const double* src = (b_step > 0 ? b_ptr[q] + b_adv : b_ptr[q] + pr.rowB(pid, k)) + cs;
+            if constexpr (SEQ) ok = n0 + cs + b_bc[q] < N && (kfull || k < K);
+            else ok = ((b_ok >> q) & 1u) && (kfull || k < K);
+            const double* src = (TAB ? b_ptr[q] + ktab[k] : b_ptr[q] + b_adv) + cs;
             cp_async16_zfill(bs + b_so[q], ok ? src : pr.Bm, ok);
         }
         cp_async_commit();
