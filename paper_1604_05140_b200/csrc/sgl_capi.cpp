@@ -322,7 +322,16 @@ size_t batch_chunk(int B, size_t batch) {
         const double gb = e ? std::atof(e) : 6.0;
         return (size_t)(std::max(0.25, gb) * (double)(1ULL << 30));
     }();
-    return std::max<size_t>(1, std::min(batch, budget / per));
+    // the GEMM kernels index G, S and the coefficients of one call in 32 bits
+    const size_t idx_cap = ((size_t)1 << 31) / ((size_t)16 * B * B * B);  // G: 16 B^3 doubles per function
+    return std::max<size_t>(1, std::min({batch, budget / per, idx_cap}));
+}
+
+// Stage entry points run one launch per stage over the caller's whole batch: the
+// GEMM kernels' 32-bit indexing bounds it (G: 16 B^3 doubles per function).
+void check_stage_batch(int B, size_t batch, const char* who) {
+    if ((double)batch * 16.0 * B * B * B >= 2147483648.0)
+        fail(SGLGPU_EINVAL, std::string(who) + ": batch too large for one stage call (split it)");
 }
 
 // L2 residency of the azimuthal -> polar intermediate G: the spherical stage
@@ -873,6 +882,7 @@ int sglgpu_spherical_forward(sglgpu_plan* p, const double* samples, size_t sampl
     return guarded([&] {
         check_plan(p);
         const int B = p->B;
+        check_stage_batch(B, batch, "sglgpu_spherical_forward");
         if (shell_begin < 0 || shell_count < 1 || shell_begin + shell_count > 2 * B)
             fail(SGLGPU_EINVAL, "sglgpu_spherical_forward: shell range out of bounds");
         if (batch == 0) return;
@@ -897,6 +907,7 @@ int sglgpu_spherical_inverse(sglgpu_plan* p, const double* shells, double* sampl
     return guarded([&] {
         check_plan(p);
         const int B = p->B;
+        check_stage_batch(B, batch, "sglgpu_spherical_inverse");
         if (shell_begin < 0 || shell_count < 1 || shell_begin + shell_count > 2 * B)
             fail(SGLGPU_EINVAL, "sglgpu_spherical_inverse: shell range out of bounds");
         if (batch == 0) return;
@@ -921,6 +932,7 @@ int sglgpu_radial_forward(sglgpu_plan* p, const double* shells, double* coeffs, 
     return guarded([&] {
         check_plan(p);
         const int B = p->B;
+        check_stage_batch(B, batch, "sglgpu_radial_forward");
         if (l_begin < 0 || l_end > B || l_begin > l_end) fail(SGLGPU_EINVAL, "sglgpu_radial_forward: bad l range");
         if (shells_per_block < 1 || (2 * B) % shells_per_block != 0)
             fail(SGLGPU_EINVAL, "sglgpu_radial_forward: shells_per_block must divide 2B");
@@ -944,6 +956,7 @@ int sglgpu_radial_inverse(sglgpu_plan* p, const double* coeffs, double* shells, 
     return guarded([&] {
         check_plan(p);
         const int B = p->B;
+        check_stage_batch(B, batch, "sglgpu_radial_inverse");
         if (l_begin < 0 || l_end > B || l_begin > l_end) fail(SGLGPU_EINVAL, "sglgpu_radial_inverse: bad l range");
         if (shells_per_block < 1 || (2 * B) % shells_per_block != 0)
             fail(SGLGPU_EINVAL, "sglgpu_radial_inverse: shells_per_block must divide 2B");
@@ -969,6 +982,7 @@ int sglgpu_spherical_forward_to(sglgpu_plan* p, const double* samples, size_t sa
     return guarded([&] {
         check_plan(p);
         const int B = p->B;
+        check_stage_batch(B, batch, "sglgpu_spherical_forward_to");
         if (shell_begin < 0 || shell_count < 1 || shell_begin + shell_count > 2 * B)
             fail(SGLGPU_EINVAL, "sglgpu_spherical_forward_to: shell range out of bounds");
         if (ndst < 1 || ndst > sglk::kMaxPeers || !dst || !l_bounds)
@@ -1008,6 +1022,7 @@ int sglgpu_radial_inverse_to(sglgpu_plan* p, const double* coeffs, int l_begin, 
     return guarded([&] {
         check_plan(p);
         const int B = p->B;
+        check_stage_batch(B, batch, "sglgpu_radial_inverse_to");
         if (l_begin < 0 || l_end > B || l_begin > l_end) fail(SGLGPU_EINVAL, "sglgpu_radial_inverse_to: bad l range");
         if (shells_per_block < 1 || (2 * B) % shells_per_block != 0)
             fail(SGLGPU_EINVAL, "sglgpu_radial_inverse_to: shells_per_block must divide 2B");

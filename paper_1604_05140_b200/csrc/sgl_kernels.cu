@@ -680,25 +680,29 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
 // Column n of a Legendre problem is (sgn, f, i_local, c) over the G chunk
 // (g.SC shells per function); it lands in S at (nu, f, sv.i0 + i_local, c)
 // of an S with sv.sc shells per function and sv.NB reals per nu row.
-__device__ __forceinline__ long long s_col(const Geo& g, const SView& sv, int am, int n) {
-    const int sgn = n >= g.NB;
-    const int nn = n - (sgn ? (int)g.NB : 0);
+// Index math inside one call's G, S and coefficient arrays is 32-bit: the host
+// keeps every array a GEMM touches below 2^31 doubles (batch_chunk).
+__device__ __forceinline__ int s_col(const Geo& g, const SView& sv, int am, int n) {
+    const int NB = (int)g.NB;
+    const int sgn = n >= NB;
+    const int nn = n - (sgn ? NB : 0);
     const int f = nn / (2 * g.SC), rem = nn - f * 2 * g.SC;
-    return (sgn ? -am : am) * sv.NB + (long long)f * 2 * sv.sc + 2LL * sv.i0 + rem;
+    return (sgn ? -am : am) * (int)sv.NB + f * 2 * sv.sc + 2 * sv.i0 + rem;
 }
 
 // Real offset of column n of a Legendre problem inside the blocked G (the row
 // part, j' * row stride, is separate): n = (sgn, flat shell s, re/im).
-__device__ __forceinline__ long long g_col(const Geo& g, int p, int am, int n) {
-    const int sgn = n >= g.NB;
-    const int nn = n - (sgn ? (int)g.NB : 0);
+__device__ __forceinline__ int g_col(const Geo& g, int p, int am, int n) {
+    const int NB = (int)g.NB;
+    const int sgn = n >= NB;
+    const int nn = n - (sgn ? NB : 0);
     const int s = nn >> 1;
     const int bin = sgn ? 2 * g.B - am : am;
-    const long long gx = s >> g.lgib;
+    const int gx = s >> g.lgib;
     const int sl = s & ((1 << g.lgib) - 1);
     return 2 * ((((gx * 2 + p) * g.nbins + bin) << g.lgib) + sl) + (nn & 1);
 }
-__device__ __forceinline__ long long g_rowstride(const Geo& g) { return 2 * g.ngx * 2 * g.nbins << g.lgib; }
+__device__ __forceinline__ int g_rowstride(const Geo& g) { return (2 * (int)g.ngx * 2 * g.nbins) << g.lgib; }
 
 struct LegFwd {
     SGL_KIND_CFG(LEGFWD, 8, 4, 4)
@@ -718,16 +722,16 @@ struct LegFwd {
     static constexpr bool B_COL_AFFINE = false;  // blocked G: per-column offsets
     // end (exclusive) of the sign half that column n0 lies in
     __device__ int nlim(int pid, int n0) const { return n0 < g.NB ? (int)g.NB : N(pid); }
-    __device__ long long rowA(int pid, int r) const { return aoff[pid] + (long long)r * g.B; }
+    __device__ long long rowA(int pid, int r) const { return aoff[pid] + r * g.B; }
     __device__ long long colA(int, int k) const { return k; }
     __device__ int a_sr(int) const { return g.B; }
     __device__ int a_sk(int) const { return 1; }
-    __device__ long long rowB(int, int k) const { return (long long)k * g_rowstride(g); }
+    __device__ long long rowB(int, int k) const { return k * g_rowstride(g); }
     __device__ long long b_kstep(int) const { return g_rowstride(g); }
     __device__ long long colB(int pid, int n) const { return g_col(g, pid & 1, am(pid), n); }
     __device__ long long rowC(int pid, int r) const {
-        const long long l = am(pid) + (pid & 1) + 2 * r;
-        return l * (l + 1) * sv.NB;
+        const int l = am(pid) + (pid & 1) + 2 * r;
+        return l * (l + 1) * (int)sv.NB;
     }
     __device__ long long colC(int pid, int n) const { return s_col(g, sv, am(pid), n); }
     __device__ bool negC(int pid, int n) const { return n >= g.NB && (am(pid) & 1); }
@@ -755,22 +759,23 @@ struct LegInv {
     static constexpr bool B_COL_AFFINE = true;
     __device__ int nlim(int pid, int n0) const { return n0 < g.NB ? (int)g.NB : N(pid); }
     __device__ long long rowA(int pid, int j) const { return aoff[pid] + j; }
-    __device__ long long colA(int, int k) const { return (long long)k * g.B; }
+    __device__ long long colA(int, int k) const { return k * g.B; }
     __device__ int a_sr(int) const { return 1; }
     __device__ int a_sk(int) const { return g.B; }
     __device__ long long rowB(int pid, int k) const {
-        const long long l = am(pid) + (pid & 1) + 2 * k;
-        return l * (l + 1) * sv.NB;
+        const int l = am(pid) + (pid & 1) + 2 * k;
+        return l * (l + 1) * (int)sv.NB;
     }
     __device__ long long b_kstep(int) const { return 0; }
     __device__ long long colB(int pid, int n) const { return s_col(g, sv, am(pid), n); }
-    __device__ long long rowC(int, int j) const { return (long long)j * g_rowstride(g); }
+    __device__ long long rowC(int, int j) const { return j * g_rowstride(g); }
     __device__ long long colC(int pid, int n) const { return g_col(g, pid & 1, am(pid), n); }
     __device__ bool negC(int pid, int n) const { return n >= g.NB && (am(pid) & 1); }
     __device__ bool c_affine(int, int, int) const { return false; }  // blocked G: per-column offsets
 };
 
 __host__ __device__ inline long long degree_offset(long long n) { return (n - 1) * n * (2 * n - 1) / 6; }
+__device__ __forceinline__ int degree_offset32(int n) { return (n - 1) * n * (2 * n - 1) / 6; }  // n <= 257
 
 // Shell-block view of the nu-major intermediate S for the radial stage.  On one
 // GPU S is a single block S[nu][f][i] (i < 2B).  Under the multi-GPU shell / (l, m)
@@ -783,7 +788,7 @@ struct ShellBlocks {
     long long nu0;         // first nu held
     __device__ long long row(int i) const {
         const int b = i / sc_blk;
-        return b * blk_stride + 2LL * (i - b * sc_blk);
+        return b * (int)blk_stride + 2 * (i - b * sc_blk);
     }
 };
 
@@ -807,7 +812,7 @@ struct RadFwd {
     __device__ int K(int) const { return 2 * g.B; }
     static constexpr bool B_COL_AFFINE = false;
     __device__ int nlim(int l, int) const { return N(l); }
-    __device__ long long rowA(int l, int r) const { return aoff[l] + (long long)r * 2 * g.B; }
+    __device__ long long rowA(int l, int r) const { return aoff[l] + r * 2 * g.B; }
     __device__ long long colA(int, int k) const { return k; }
     __device__ int a_sr(int) const { return 2 * g.B; }
     __device__ int a_sk(int) const { return 1; }
@@ -816,13 +821,13 @@ struct RadFwd {
     __device__ long long colB(int l, int n) const {
         const int mf = n >> 1, w = mw(l);
         const int f = mf / w, mm = mf - f * w + (g.real ? l : 0);  // mm = m + l
-        return ((long long)l * l + mm - sb.nu0) * g.NB + (long long)f * 2 * g.SC + (n & 1);
+        return (l * l + mm - (int)sb.nu0) * (int)g.NB + f * 2 * g.SC + (n & 1);
     }
-    __device__ long long rowC(int l, int r) const { return 2 * degree_offset(l + 1 + r); }
+    __device__ long long rowC(int l, int r) const { return 2 * degree_offset32(l + 1 + r); }
     __device__ long long colC(int l, int n) const {
         const int mf = n >> 1, w = mw(l);
         const int f = mf / w, mm = mf - f * w + (g.real ? l : 0);
-        return (long long)f * 2 * omega + 2LL * ((long long)l * l + mm) + (n & 1);
+        return f * 2 * (int)omega + 2 * (l * l + mm) + (n & 1);
     }
     __device__ bool negC(int, int) const { return false; }
     __device__ bool c_affine(int, int, int) const { return false; }
@@ -834,7 +839,7 @@ struct RadFwd {
         const int f = mf / w, m = mf - f * w;
         if (m == 0) return -1;
         neg = m & 1;
-        return (long long)f * 2 * omega + 2LL * ((long long)l * l + l - m) + (n & 1);
+        return f * 2 * (int)omega + 2 * (l * l + l - m) + (n & 1);
     }
 };
 
@@ -858,21 +863,21 @@ struct RadInv {
     static constexpr bool B_COL_AFFINE = false;
     __device__ int nlim(int l, int) const { return N(l); }
     __device__ long long rowA(int l, int i) const { return aoff[l] + i; }
-    __device__ long long colA(int, int k) const { return (long long)k * 2 * g.B; }
+    __device__ long long colA(int, int k) const { return k * 2 * g.B; }
     __device__ int a_sr(int) const { return 1; }
     __device__ int a_sk(int) const { return 2 * g.B; }
-    __device__ long long rowB(int l, int k) const { return 2 * degree_offset(l + 1 + k); }
+    __device__ long long rowB(int l, int k) const { return 2 * degree_offset32(l + 1 + k); }
     __device__ long long b_kstep(int) const { return 0; }
     __device__ long long colB(int l, int n) const {
         const int mf = n >> 1, w = mw(l);
         const int f = mf / w, mm = mf - f * w + (g.real ? l : 0);
-        return (long long)f * 2 * omega + 2LL * ((long long)l * l + mm) + (n & 1);
+        return f * 2 * (int)omega + 2 * (l * l + mm) + (n & 1);
     }
     __device__ long long rowC(int, int i) const { return sb.row(i); }
     __device__ long long colC(int l, int n) const {
         const int mf = n >> 1, w = mw(l);
         const int f = mf / w, mm = mf - f * w + (g.real ? l : 0);
-        return ((long long)l * l + mm - sb.nu0) * g.NB + (long long)f * 2 * g.SC + (n & 1);
+        return (l * l + mm - (int)sb.nu0) * (int)g.NB + f * 2 * g.SC + (n & 1);
     }
     __device__ bool negC(int, int) const { return false; }
     __device__ bool c_affine(int, int, int) const { return false; }
@@ -1006,15 +1011,15 @@ __device__ __forceinline__ void gemm_epilogue(const P& pr, int pid, int m0, int 
     constexpr int BN = C::BN, FM = C::FM;
     // signs are applied as sign-bit flips (a DMUL would compete with the DMMAs
     // for the FP64 pipe)
-    long long cofs[4];
+    int cofs[4];
     unsigned long long csg[4];
     const bool caff = pr.c_affine(pid, n0, BN);
-    const long long cbase = caff ? pr.colC(pid, n0) : 0;
+    const int cbase = caff ? (int)pr.colC(pid, n0) : 0;
 #pragma unroll
     for (int fn = 0; fn < 4; ++fn) {
         const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
         const bool ok = col < N;
-        cofs[fn] = ok ? (caff ? cbase + (col - n0) : pr.colC(pid, col)) : 0;
+        cofs[fn] = ok ? (caff ? cbase + (col - n0) : (int)pr.colC(pid, col)) : 0;
         csg[fn] = ok && pr.negC(pid, col) ? 0x8000000000000000ULL : 0ULL;
     }
     auto flip = [](double v, unsigned long long m) { return __longlong_as_double(__double_as_longlong(v) ^ m); };
@@ -1024,7 +1029,7 @@ __device__ __forceinline__ void gemm_epilogue(const P& pr, int pid, int m0, int 
         if (row >= M) continue;
         double* out;
         if constexpr (has_out_row<P>::value) out = pr.out_row(pid, row);
-        else out = pr.C + pr.rowC(pid, row);
+        else out = pr.C + (int)pr.rowC(pid, row);
 #pragma unroll
         for (int fn = 0; fn < 4; ++fn) {
             const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
@@ -1089,7 +1094,7 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
             const bool ok = m0 + row < M;
             a_ok |= (ok ? 1u : 0u) << u;
             a_ok2 |= ((P::A_KCONTIG ? ok : m0 + row + 1 < M) ? 1u : 0u) << u;
-            a_ptr[u] = ok ? pr.A + abase + (long long)row * a_sr + (long long)k * a_sk : pr.A;
+            a_ptr[u] = ok ? pr.A + abase + (row * a_sr + k * a_sk) : pr.A;
         }
     }
     // B rows: affine kinds (B_ROW_TABLE == 0) advance their pointers by a fixed
@@ -1099,10 +1104,10 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
     // (quadratic / cubic in k for the Legendre-inverse / radial-inverse rows).
     constexpr bool TAB = P::B_ROW_TABLE > 0;
     const long long b_step = TAB ? 0 : pr.b_kstep(pid);
-    long long* ktab = reinterpret_cast<long long*>(smem + ST * C::STAGE);
+    int* ktab = reinterpret_cast<int*>(smem + ST * C::STAGE);
     if constexpr (TAB) {
         const int kr = nch * BK;  // <= P::B_ROW_TABLE (K <= the kind's maximum)
-        for (int k = tid; k < kr; k += 128) ktab[k] = k < K ? pr.rowB(pid, k) : 0;
+        for (int k = tid; k < kr; k += 128) ktab[k] = k < K ? (int)pr.rowB(pid, k) : 0;
         __syncthreads();
     }
     const double* b_ptr[C::BQ];
@@ -1131,7 +1136,7 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
             b_ok |= (ok ? 1u : 0u) << q;
             const long long col = !ok ? 0 : (P::B_COL_AFFINE ? bcol0 + bc : pr.colB(pid, n0 + bc));
             // affine rows: the k = b_k[q] row offset is folded in here
-            b_ptr[q] = pr.Bm + col + (TAB ? 0 : pr.rowB(pid, 0) + (long long)b_k[q] * b_step);
+            b_ptr[q] = pr.Bm + col + (TAB ? 0 : (int)pr.rowB(pid, 0) + b_k[q] * (int)b_step);
         }
     }
     // A is affine in k for every kind: per-chunk advance k0 * a_sk.  Byte counts
@@ -1158,7 +1163,7 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
         double* bs = as + C::A_STAGE;
         const int k0 = c * BK;
         const bool kfull = k0 + BK <= K;
-        const long long a_adv = (long long)k0 * a_sk;
+        const int a_adv = k0 * a_sk;
 #pragma unroll
         for (int u = 0; u < AU; ++u) {
             const double* src = a_ptr[u] + a_adv;
@@ -1185,7 +1190,7 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
                 cp_async8_zfill(as + a_so[u] + 1, ok2 ? src + (P::A_KCONTIG ? a_sk : a_sr) : pr.A, ok2);
             }
         }
-        const long long b_adv = (long long)k0 * b_step;
+        const int b_adv = k0 * (int)b_step;
 #pragma unroll
         for (int q = 0; q < C::BQ; ++q) {
             const int k = k0 + b_k[q];
