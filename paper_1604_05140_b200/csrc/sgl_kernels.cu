@@ -663,12 +663,27 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
 #ifndef SGL_BK_LEGFWD
 #define SGL_BK_LEGFWD 0
 #endif
+#ifndef SGL_ISSUE_LEGFWD
+#define SGL_ISSUE_LEGFWD -1
+#endif
+#ifndef SGL_ISSUE_LEGINV
+#define SGL_ISSUE_LEGINV -1
+#endif
+#ifndef SGL_ISSUE_RADFWD
+#define SGL_ISSUE_RADFWD -1
+#endif
+#ifndef SGL_ISSUE_RADINV
+#define SGL_ISSUE_RADINV -1
+#endif
 // Per-kind pipeline shape: k-chunk (BK), cp.async stages (ST), CTAs per SM
-// (__launch_bounds__).  Measured at B = 128 (exp/stage_times.py): BK 8 with 3
-// stages keeps more bytes in flight per CTA than BK 16 with 2 at the same
+// (__launch_bounds__), where the next chunk's loads are issued (GEMM_ISSUE:
+// measured at B = 128 -- after the MMAs: legendre_inverse 110 -> 108.7 us,
+// radial_forward 53.1 -> 51.2 us; before them: radial_inverse 45.9 vs 50.6 us).
+// Measured at B = 128 (exp/stage_times.py): BK 8 with 3 stages keeps more bytes in flight per CTA than BK 16 with 2 at the same
 // shared-memory footprint (4 CTAs / SM): 585 -> 565 us per round trip; LegInv
 // and LegFwd (ring sized for wm <= 2) run 4 stages (-1 us, -3.6 us).
-#define SGL_KIND_CFG(NAME, DBK, DST, DMINB)                  \
+#define SGL_KIND_CFG(NAME, DBK, DST, DMINB, DISSUE)          \
+    static constexpr int GEMM_ISSUE = SGL_ISSUE_##NAME >= 0 ? SGL_ISSUE_##NAME : DISSUE; \
     static constexpr int GEMM_BK = SGL_BK_##NAME > 0 ? SGL_BK_##NAME : DBK; \
     static constexpr int GEMM_ST = SGL_ST_##NAME > 0 ? SGL_ST_##NAME : DST; \
     static constexpr int GEMM_MINB = SGL_MINB_##NAME > 0 ? SGL_MINB_##NAME : DMINB; \
@@ -705,7 +720,7 @@ __device__ __forceinline__ int g_col(const Geo& g, int p, int am, int n) {
 __device__ __forceinline__ int g_rowstride(const Geo& g) { return (2 * (int)g.ngx * 2 * g.nbins) << g.lgib; }
 
 struct LegFwd {
-    SGL_KIND_CFG(LEGFWD, 8, 4, 4)
+    SGL_KIND_CFG(LEGFWD, 8, 4, 4, 0)
     Geo g;
     const double* A;        // table
     const long long* aoff;  // per prob
@@ -742,7 +757,7 @@ struct LegFwd {
 
 // Legendre inverse: prob = 2|m| + p.  rows j' (M = B), K = #l of parity p, cols n'.
 struct LegInv {
-    SGL_KIND_CFG(LEGINV, 8, 4, 4)
+    SGL_KIND_CFG(LEGINV, 8, 4, 4, 2)
     Geo g;
     const double* A;
     const long long* aoff;
@@ -795,7 +810,7 @@ struct ShellBlocks {
 // Radial forward: prob = l.  rows n = l+1+r (M = B-l), K = 2B (i), cols (mf, c),
 // mf = f * (2l+1) + (m + l).  g.SC = sc_blk, g.NB = batch * sc_blk * 2.
 struct RadFwd {
-    SGL_KIND_CFG(RADFWD, 8, 3, 4)
+    SGL_KIND_CFG(RADFWD, 8, 3, 4, 2)
     Geo g;
     const double* A;        // W
     const long long* aoff;
@@ -845,7 +860,7 @@ struct RadFwd {
 
 // Radial inverse: prob = l.  rows i (M = 2B), K = B-l (n), cols (mf, c).
 struct RadInv {
-    SGL_KIND_CFG(RADINV, 8, 3, 4)
+    SGL_KIND_CFG(RADINV, 8, 3, 4, 0)
     Geo g;
     const double* A;        // V
     const long long* aoff;
@@ -959,10 +974,12 @@ constexpr size_t gemm_smem_bytes() {
     return sizeof(double) * (P::GEMM_ST * m + P::B_ROW_TABLE);  // + the B row-offset table
 }
 
-// One k-chunk of MMAs for a warp with FA x NA active 8 x 8 fragments.
-template <class P, int WM, int FA, int NA, bool FULL>
+// One k-chunk of MMAs for a warp with FA x NA active 8 x 8 fragments.  mid()
+// (the next chunk's cp.async issue) runs once, where the kind's GEMM_ISSUE puts
+// it: 0 before the MMAs, 1 after the first k-step, 2 after the chunk.
+template <class P, int WM, int FA, int NA, bool FULL, class Mid>
 __device__ __forceinline__ void mma_chunk(const double* as, const double* bs, double (&acc)[4][4][2], int ksteps,
-                                          int wr, int wc, int lane) {
+                                          int wr, int wc, int lane, Mid&& mid) {
     using C = GemmCfg<P, WM>;
 #pragma unroll
     for (int kk = 0; kk < C::BK; kk += 4) {
@@ -979,24 +996,31 @@ __device__ __forceinline__ void mma_chunk(const double* as, const double* bs, do
         for (int fm = 0; fm < FA; ++fm)
 #pragma unroll
             for (int fn = 0; fn < NA; ++fn) dmma884(acc[fm][fn], af[fm], bf[fn]);
+        if (P::GEMM_ISSUE == 1 && kk == 0) mid();
     }
+    if (P::GEMM_ISSUE == 2) mid();
 }
 
-template <class P, int WM, bool FULL>
+template <class P, int WM, bool FULL, class Mid>
 __device__ __forceinline__ void dispatch_chunk(int fa, int na, const double* as, const double* bs,
-                                               double (&acc)[4][4][2], int ksteps, int wr, int wc, int lane) {
+                                               double (&acc)[4][4][2], int ksteps, int wr, int wc, int lane,
+                                               Mid&& mid) {
+    if (P::GEMM_ISSUE == 0) mid();
+    auto mid2 = [&] {
+        if (P::GEMM_ISSUE != 0) mid();
+    };
     if (fa == 4 && na == 4) {  // the common full-fragment case first
-        mma_chunk<P, WM, 4, 4, FULL>(as, bs, acc, ksteps, wr, wc, lane);
+        mma_chunk<P, WM, 4, 4, FULL>(as, bs, acc, ksteps, wr, wc, lane, mid2);
         return;
     }
 #define SGL_MMA_CASE(A_, N_) \
-    case A_ * 8 + N_: mma_chunk<P, WM, A_, N_, FULL>(as, bs, acc, ksteps, wr, wc, lane); break;
+    case A_ * 8 + N_: mma_chunk<P, WM, A_, N_, FULL>(as, bs, acc, ksteps, wr, wc, lane, mid2); break;
     switch (fa * 8 + na) {
         SGL_MMA_CASE(4, 4) SGL_MMA_CASE(4, 3) SGL_MMA_CASE(4, 2) SGL_MMA_CASE(4, 1)
         SGL_MMA_CASE(3, 4) SGL_MMA_CASE(3, 3) SGL_MMA_CASE(3, 2) SGL_MMA_CASE(3, 1)
         SGL_MMA_CASE(2, 4) SGL_MMA_CASE(2, 3) SGL_MMA_CASE(2, 2) SGL_MMA_CASE(2, 1)
         SGL_MMA_CASE(1, 4) SGL_MMA_CASE(1, 3) SGL_MMA_CASE(1, 2) SGL_MMA_CASE(1, 1)
-        default: break;  // a warp with no active fragment only helps with the loads
+        default: mid2(); break;  // a warp with no active fragment only helps with the loads
     }
 #undef SGL_MMA_CASE
 }
@@ -1223,15 +1247,17 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
         for (int v = 0; v < nv; ++v) {
             cp_async_wait_group<ST - 2>();
             __syncthreads();
-            if (v + ST - 1 < nv) issue(v + ST - 1);
-            else cp_async_commit();
+            auto mid = [&] {
+                if (v + ST - 1 < nv) issue(v + ST - 1);
+                else cp_async_commit();
+            };
             const double* as = smem + (v % ST) * C::STAGE;
             const double* bs = as + C::A_STAGE;
             const int ksteps = min(BK, K - c * BK);
             if (ksteps == BK) {
-                dispatch_chunk<P, WM, true>(fm_active, fna, as, bs, acc, BK, wr, wc, lane);
+                dispatch_chunk<P, WM, true>(fm_active, fna, as, bs, acc, BK, wr, wc, lane, mid);
             } else {
-                dispatch_chunk<P, WM, false>(fm_active, fna, as, bs, acc, ksteps, wr, wc, lane);
+                dispatch_chunk<P, WM, false>(fm_active, fna, as, bs, acc, ksteps, wr, wc, lane, mid);
             }
             if (++c == nch) {  // tile tv complete: write it, reset for tile tv + 1
                 gemm_epilogue<P, WM>(pr, pid, m0, n0 + tv * BN, M, N, acc, wr, wc, lane);
@@ -1255,20 +1281,19 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
     for (int c = 0; c < nch; ++c) {
         cp_async_wait_group<ST - 2>();
         __syncthreads();
-        if (c + ST - 1 < nch) issue(c + ST - 1);
-        else cp_async_commit();
+        auto mid = [&] {
+            if (c + ST - 1 < nch) issue(c + ST - 1);
+            else cp_async_commit();
+        };
         const double* as = smem + (c % ST) * C::STAGE;
         const double* bs = as + C::A_STAGE;
         const int ksteps = min(BK, K - c * BK);  // k-steps past K carry zeros: skip them
         // warp-uniform dispatch to straight-line MMA code: no per-MMA guards
         // (a guarded mma.sync costs ISETP + WARPSYNC + NOP per DMMA)
-#ifdef SGL_GEMM_NOMMA  // experiment: load-only timing (wrong results)
-        if (ksteps > 0) continue;
-#endif
         if (ksteps == BK) {
-            dispatch_chunk<P, WM, true>(fm_active, fn_active, as, bs, acc, BK, wr, wc, lane);
+            dispatch_chunk<P, WM, true>(fm_active, fn_active, as, bs, acc, BK, wr, wc, lane, mid);
         } else {
-            dispatch_chunk<P, WM, false>(fm_active, fn_active, as, bs, acc, ksteps, wr, wc, lane);
+            dispatch_chunk<P, WM, false>(fm_active, fn_active, as, bs, acc, ksteps, wr, wc, lane, mid);
         }
     }
     cp_async_wait_group<0>();
