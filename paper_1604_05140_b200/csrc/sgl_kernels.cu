@@ -1176,9 +1176,18 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
     // pipelined sequence of chunks v = tile * nch + c (A is the same for all of
     // them; B columns shift by BN per tile), so each tile's epilogue overlaps the
     // next tile's loads and the CTA prologue is paid once per sequence.
+    // issue() is called for v = 0, 1, 2, ... in order: (tile, chunk) of the next
+    // issue are counters (no division by nch per chunk)
+    int is_tile = 0, is_chunk = 0;
     auto issue = [&](int v) {
-        const int tv = SEQ ? v / nch : 0;
-        const int c = v - tv * nch;
+        const int tv = SEQ ? is_tile : 0;
+        const int c = SEQ ? is_chunk : v;
+        if constexpr (SEQ) {
+            if (++is_chunk == nch) {
+                is_chunk = 0;
+                ++is_tile;
+            }
+        }
         const int cs = tv * BN;  // column shift of tile tv
 #ifdef SGL_GEMM_NOLOAD  // experiment: compute-only timing (wrong results)
         if (v > 0) { cp_async_commit(); return; }
