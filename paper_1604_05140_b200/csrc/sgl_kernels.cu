@@ -701,7 +701,7 @@ __device__ __forceinline__ int s_col(const Geo& g, const SView& sv, int am, int 
     const int NB = (int)g.NB;
     const int sgn = n >= NB;
     const int nn = n - (sgn ? NB : 0);
-    const int f = nn / (2 * g.SC), rem = nn - f * 2 * g.SC;
+    const int f = g.batch == 1 ? 0 : nn / (2 * g.SC), rem = nn - f * 2 * g.SC;  // no division for one function
     return (sgn ? -am : am) * (int)sv.NB + f * 2 * sv.sc + 2 * sv.i0 + rem;
 }
 
@@ -737,10 +737,11 @@ struct LegFwd {
     static constexpr bool B_COL_AFFINE = false;  // blocked G: per-column offsets
     // end (exclusive) of the sign half that column n0 lies in
     __device__ int nlim(int pid, int n0) const { return n0 < g.NB ? (int)g.NB : N(pid); }
-    __device__ long long rowA(int pid, int r) const { return aoff[pid] + r * g.B; }
+    __device__ long long rowA(int pid, int r) const { return aoff[pid] + r * lstride(); }
     __device__ long long colA(int, int k) const { return k; }
-    __device__ int a_sr(int) const { return g.B; }
+    __device__ int a_sr(int) const { return lstride(); }
     __device__ int a_sk(int) const { return 1; }
+    __device__ int lstride() const { return g.B + (g.B & 1); }  // legendre_stride (sgl_tables.hpp)
     __device__ long long rowB(int, int k) const { return k * g_rowstride(g); }
     __device__ long long b_kstep(int) const { return g_rowstride(g); }
     __device__ long long colB(int pid, int n) const { return g_col(g, pid & 1, am(pid), n); }
@@ -774,9 +775,10 @@ struct LegInv {
     static constexpr bool B_COL_AFFINE = true;
     __device__ int nlim(int pid, int n0) const { return n0 < g.NB ? (int)g.NB : N(pid); }
     __device__ long long rowA(int pid, int j) const { return aoff[pid] + j; }
-    __device__ long long colA(int, int k) const { return k * g.B; }
+    __device__ long long colA(int, int k) const { return k * lstride(); }
     __device__ int a_sr(int) const { return 1; }
-    __device__ int a_sk(int) const { return g.B; }
+    __device__ int a_sk(int) const { return lstride(); }
+    __device__ int lstride() const { return g.B + (g.B & 1); }  // legendre_stride (sgl_tables.hpp)
     __device__ long long rowB(int pid, int k) const {
         const int l = am(pid) + (pid & 1) + 2 * k;
         return l * (l + 1) * (int)sv.NB;
@@ -802,6 +804,7 @@ struct ShellBlocks {
     long long blk_stride;  // reals between blocks
     long long nu0;         // first nu held
     __device__ long long row(int i) const {
+        if (blk_stride == 0) return 2 * i;  // one block (single GPU)
         const int b = i / sc_blk;
         return b * (int)blk_stride + 2 * (i - b * sc_blk);
     }
@@ -835,13 +838,13 @@ struct RadFwd {
     __device__ long long b_kstep(int) const { return sb.sc_blk == 2 * g.B ? 2 : 0; }
     __device__ long long colB(int l, int n) const {
         const int mf = n >> 1, w = mw(l);
-        const int f = mf / w, mm = mf - f * w + (g.real ? l : 0);  // mm = m + l
+        const int f = g.batch == 1 ? 0 : mf / w, mm = mf - f * w + (g.real ? l : 0);  // mm = m + l
         return (l * l + mm - (int)sb.nu0) * (int)g.NB + f * 2 * g.SC + (n & 1);
     }
     __device__ long long rowC(int l, int r) const { return 2 * degree_offset32(l + 1 + r); }
     __device__ long long colC(int l, int n) const {
         const int mf = n >> 1, w = mw(l);
-        const int f = mf / w, mm = mf - f * w + (g.real ? l : 0);
+        const int f = g.batch == 1 ? 0 : mf / w, mm = mf - f * w + (g.real ? l : 0);
         return f * 2 * (int)omega + 2 * (l * l + mm) + (n & 1);
     }
     __device__ bool negC(int, int) const { return false; }
@@ -851,7 +854,7 @@ struct RadFwd {
     __device__ long long colC_mirror(int l, int n, bool& neg) const {
         if (!g.real) return -1;
         const int mf = n >> 1, w = mw(l);
-        const int f = mf / w, m = mf - f * w;
+        const int f = g.batch == 1 ? 0 : mf / w, m = mf - f * w;
         if (m == 0) return -1;
         neg = m & 1;
         return f * 2 * (int)omega + 2 * (l * l + l - m) + (n & 1);
@@ -885,23 +888,19 @@ struct RadInv {
     __device__ long long b_kstep(int) const { return 0; }
     __device__ long long colB(int l, int n) const {
         const int mf = n >> 1, w = mw(l);
-        const int f = mf / w, mm = mf - f * w + (g.real ? l : 0);
+        const int f = g.batch == 1 ? 0 : mf / w, mm = mf - f * w + (g.real ? l : 0);
         return f * 2 * (int)omega + 2 * (l * l + mm) + (n & 1);
     }
     __device__ long long rowC(int, int i) const { return sb.row(i); }
     __device__ long long colC(int l, int n) const {
         const int mf = n >> 1, w = mw(l);
-        const int f = mf / w, mm = mf - f * w + (g.real ? l : 0);
+        const int f = g.batch == 1 ? 0 : mf / w, mm = mf - f * w + (g.real ? l : 0);
         return (l * l + mm - (int)sb.nu0) * (int)g.NB + f * 2 * g.SC + (n & 1);
     }
     __device__ bool negC(int, int) const { return false; }
     __device__ bool c_affine(int, int, int) const { return false; }
 };
 
-__device__ __forceinline__ void cp_async8_zfill(void* smem_dst, const void* gmem_src, bool ok) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gmem_src), "r"(ok ? 8 : 0));
-}
 __device__ __forceinline__ void cp_async16_zfill(void* smem_dst, const void* gmem_src, bool ok) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem_src), "r"(ok ? 16 : 0));
@@ -1097,10 +1096,12 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
     const double* a_ptr[AU];
     int a_so[AU], a_k[AU];
     unsigned a_ok = 0, a_ok2 = 0;  // first / second element's row inside M
-    bool a_vec;
     {
+        // every kind's A is 16-byte aligned in 2-element units: tables start at even
+        // offsets with even row strides (the Legendre rows are padded to an even
+        // length, sgl_tables.cpp) and the unit's second element is the next k
+        // (A_KCONTIG) or the next row
         const long long abase = pr.rowA(pid, m0);
-        a_vec = P::A_KCONTIG ? a_sk == 1 && ((abase | a_sr) & 1) == 0 : a_sr == 1 && ((abase | a_sk) & 1) == 0;
 #pragma unroll
         for (int u = 0; u < AU; ++u) {
             const int e = tid + 128 * u;
@@ -1213,15 +1214,9 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
                 ok1 = ((a_ok >> u) & 1u) && kok;
                 ok2 = ((a_ok2 >> u) & 1u) && kok;
             }
-            if (a_vec) {
-                const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(as + a_so[u]));
-                const int nb = ok1 ? (ok2 ? 16 : 8) : 0;
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(ok1 ? src : pr.A),
-                             "r"(nb));
-            } else {
-                cp_async8_zfill(as + a_so[u], ok1 ? src : pr.A, ok1);
-                cp_async8_zfill(as + a_so[u] + 1, ok2 ? src + (P::A_KCONTIG ? a_sk : a_sr) : pr.A, ok2);
-            }
+            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(as + a_so[u]));
+            const int nb = ok1 ? (ok2 ? 16 : 8) : 0;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(ok1 ? src : pr.A), "r"(nb));
         }
         const int b_adv = k0 * (int)b_step;
 #pragma unroll

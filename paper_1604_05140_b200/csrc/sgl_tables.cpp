@@ -71,7 +71,10 @@ Tables build_tables(int B, const double* r, const double* a_mod, const double* b
     }
     t.bcal.assign(bcal, bcal + n2);
 
-    // ---- normalized Legendre table, rows grouped by (|m|, parity)
+    // ---- normalized Legendre table, rows grouped by (|m|, parity); rows padded
+    // to an even length (legendre_stride) so every row starts 16-byte aligned
+    // (the GEMM moves table elements in pairs); the pad entry is 0
+    const int LS = legendre_stride(B);
     t.legendre_off.assign(2 * B + 1, 0);
     {
         long long off = 0;
@@ -79,7 +82,7 @@ Tables build_tables(int B, const double* r, const double* a_mod, const double* b
             for (int p = 0; p < 2; ++p) {
                 t.legendre_off[2 * am + p] = off;
                 const int rows = std::max(0, (B - am - p + 1) / 2);
-                off += (long long)rows * B;
+                off += (long long)rows * LS;
             }
         }
         t.legendre_off[2 * B] = off;
@@ -117,7 +120,7 @@ Tables build_tables(int B, const double* r, const double* a_mod, const double* b
                 }
                 const int p = (l - am) & 1;
                 const int row = (l - am) >> 1;
-                t.legendre[t.legendre_off[2 * am + p] + (long long)row * B + j] = (double)v;
+                t.legendre[t.legendre_off[2 * am + p] + (long long)row * LS + j] = (double)v;
             }
         }
     });

@@ -49,7 +49,8 @@ class DeviceModel:
         B = self.B
         rows = max(0, (B - am - p + 1) // 2)
         o = self.t["leg_off"][2 * am + p]
-        return self.t["leg"][o:o + rows * B].reshape(rows, B)
+        ls = B + (B & 1)  # rows padded to an even length (sgl_tables.hpp legendre_stride)
+        return self.t["leg"][o:o + rows * ls].reshape(rows, ls)[:, :B]
 
     def forward(self, grid):
         B = self.B

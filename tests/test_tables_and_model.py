@@ -79,15 +79,19 @@ def test_sglt_crc_is_checked(tmp_path):
         sgl.load_radial_rule(str(bad))
 
 
-@pytest.mark.parametrize("B", [4, 16])
+@pytest.mark.parametrize("B", [4, 7, 16])
 def test_device_legendre_table_matches_closed_form(B):
     o = Oracle(B)
     t = host_tables(B, o.r, o.a_mod, o.b_cal)
     theta = o.theta
+    ls = B + (B & 1)  # rows padded to an even length, pad entry 0
     for am in range(B):
         for p in range(2):
             rows = max(0, (B - am - p + 1) // 2)
-            blk = t["leg"][t["leg_off"][2 * am + p]:][:rows * B].reshape(rows, B)
+            assert t["leg_off"][2 * am + p] % 2 == 0  # 16-byte aligned rows
+            blk = t["leg"][t["leg_off"][2 * am + p]:][:rows * ls].reshape(rows, ls)
+            assert not blk[:, B:].any()
+            blk = blk[:, :B]
             for row in range(rows):
                 l = am + p + 2 * row
                 # Y_l^am(theta, 0) = Pbar_l^am(cos theta), Condon-Shortley phase included
