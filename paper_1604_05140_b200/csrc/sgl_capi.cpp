@@ -176,7 +176,9 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
         plo = 0;
         phi = 2 * B;
     }
-    const char* wm_env = std::getenv(leg ? "SGL_WM_LEG" : "SGL_WM_RAD");
+    static const char* const kind_env[4] = {"SGL_WM_LEGFWD", "SGL_WM_LEGINV", "SGL_WM_RADFWD", "SGL_WM_RADINV"};
+    const char* wm_env = std::getenv(kind_env[kind]);  // experiments: force one kind's warp layout
+    if (!wm_env) wm_env = std::getenv(leg ? "SGL_WM_LEG" : "SGL_WM_RAD");
     const int wm_force = wm_env ? std::atoi(wm_env) : 0;
     struct Entry {
         int pid, lwm, halves, tm, tn, h0, mi0, ni0;
