@@ -1,41 +1,56 @@
-"""Summarise an `ncu --page source --csv --print-source sass` export: stall samples
-per opcode and per reason, and the hottest instructions (read here, not on the box)."""
+"""Summarise an `ncu --page source --csv --print-source sass` export of ONE kernel
+(read here, not on the box): stall samples per code region and per opcode.
+
+Instructions with the same execution count belong to the same region of the
+kernel (prologue / per-chunk issue / MMA body / barrier / epilogue), so grouping
+by execution count shows where the warps spend their samples.
+usage: python tools/sass_stalls.py export.csv [top]"""
 import collections
 import csv
 import sys
 
-rows = list(csv.reader(open(sys.argv[1])))
-h = rows[1]
-data = [r for r in rows[2:] if len(r) == len(h) and r[0].startswith("0x")]
-ix = {k: i for i, k in enumerate(h)}
-reasons = [k for k in h if k.startswith("stall_") and "Not Issued" not in k]
-tot = sum(int(r[ix["Warp Stall Sampling (All Samples)"]] or 0) for r in data)
-by_op = collections.Counter()
-by_reason = collections.Counter()
-by_op_reason = collections.defaultdict(collections.Counter)
-execd = collections.Counter()
-for r in data:
-    op = r[ix["Source"]].strip().split()[0] if r[ix["Source"]].strip() else "?"
-    if op.startswith("@"):
-        op = r[ix["Source"]].strip().split()[1]
-    op = op.split(".")[0]
-    s = int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
-    by_op[op] += s
-    execd[op] += int(r[ix["Instructions Executed"]] or 0)
-    for k in reasons:
-        v = int(r[ix[k]] or 0)
-        by_reason[k] += v
-        by_op_reason[op][k] += v
-print(f"total samples {tot}")
-print("by reason:", ", ".join(f"{k[6:]}={v / tot:.3f}" for k, v in by_reason.most_common(10)))
-print("by opcode (share of samples, warp-level instructions executed, top reasons):")
-for op, v in by_op.most_common(14):
-    top = ", ".join(f"{k[6:]}={c / tot:.3f}" for k, c in by_op_reason[op].most_common(3))
-    print(f"  {op:10s} {v / tot:6.3f}  exec={execd[op]:>10d}  {top}")
-n = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-print("hottest instructions:")
-hot = sorted(data, key=lambda r: -int(r[ix["Warp Stall Sampling (All Samples)"]] or 0))[:n]
-for r in hot:
-    s = int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
-    top = sorted(((int(r[ix[k]] or 0), k[6:]) for k in reasons), reverse=True)[:2]
-    print(f"  {r[ix['Address']][-5:]} {s / tot:6.3f} {r[ix['Source']].strip()[:60]:60s} {top}")
+
+def load(path):
+    rows = list(csv.reader(open(path)))
+    h = rows[1]
+    seen, data = set(), []
+    for r in rows[2:]:
+        if len(r) == len(h) and r[0].startswith("0x") and r[0] not in seen:  # the export repeats rows
+            seen.add(r[0])
+            data.append(r)
+    return h, data
+
+
+def opcode(src):
+    t = src.strip().split()
+    if not t:
+        return "?"
+    return (t[1] if t[0].startswith("@") and len(t) > 1 else t[0]).split(".")[0]
+
+
+def main(path, top=10):
+    h, data = load(path)
+    ix = {k: i for i, k in enumerate(h)}
+    reasons = [k for k in h if k.startswith("stall_") and "Not Issued" not in k]
+    tot_s = tot_i = 0
+    smp, ninstr = collections.Counter(), collections.Counter()
+    rs, ops = collections.defaultdict(collections.Counter), collections.defaultdict(collections.Counter)
+    for r in data:
+        e = int(r[ix["Instructions Executed"]] or 0)
+        s = int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
+        tot_s += s
+        tot_i += e
+        smp[e] += s
+        ninstr[e] += 1
+        ops[e][opcode(r[ix["Source"]])] += 1
+        for k in reasons:
+            rs[e][k[6:]] += int(r[ix[k]] or 0)
+    print(f"warp instructions executed {tot_i}, stall samples {tot_s}")
+    print("regions (instructions sharing an execution count), by share of samples:")
+    for e, s in smp.most_common(top):
+        print(f"  exec={e:9d} x {ninstr[e]:4d} instr  samples={s / max(tot_s, 1):.3f}  instr={e * ninstr[e] / max(tot_i, 1):.3f}  "
+              f"{dict(rs[e].most_common(3))}  {dict(ops[e].most_common(5))}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 10)
