@@ -801,6 +801,24 @@ struct LegInv {
     __device__ long long colC(int pid, int n) const { return g_col(g, pid & 1, am(pid), n); }
     __device__ bool negC(int pid, int n) const { return n >= g.NB && (am(pid) & 1); }
     __device__ bool c_affine(int, int, int) const { return false; }  // blocked G: per-column offsets
+    // offsets of columns col0 + 8 fn (fn < 4, all inside col0's sign half): the
+    // sign, bin and row part of g_col computed once
+    static constexpr bool HAS_COLC4 = true;
+    __device__ void colC4(int pid, int col0, int (&o)[4]) const {
+        const int NB = (int)g.NB;
+        const int sgn = col0 >= NB;
+        const int nn = col0 - (sgn ? NB : 0);
+        const int a = am(pid), p = pid & 1;
+        const int bin = sgn ? 2 * g.B - a : a;
+        const int gs = (2 * g.nbins) << g.lgib;          // complex per shell group
+        const int inner = ((p * g.nbins + bin) << g.lgib);  // (p, bin) row inside a group
+        const int mask = (1 << g.lgib) - 1;
+#pragma unroll
+        for (int fn = 0; fn < 4; ++fn) {
+            const int sh = (nn >> 1) + 4 * fn;
+            o[fn] = 2 * ((sh >> g.lgib) * gs + inner + (sh & mask)) + (nn & 1);
+        }
+    }
 };
 
 __host__ __device__ inline long long degree_offset(long long n) { return (n - 1) * n * (2 * n - 1) / 6; }
@@ -960,6 +978,11 @@ template <class P>
 struct has_out_row<P, std::void_t<decltype(std::declval<const P&>().out_row(0, 0))>> : std::true_type {};
 
 template <class P, class = void>
+struct has_colc4 : std::false_type {};
+template <class P>
+struct has_colc4<P, std::void_t<decltype(P::HAS_COLC4)>> : std::bool_constant<P::HAS_COLC4> {};
+
+template <class P, class = void>
 struct has_mirror : std::false_type {};
 template <class P>
 struct has_mirror<P, std::void_t<decltype(P::MIRROR)>> : std::bool_constant<P::MIRROR> {};
@@ -1050,11 +1073,12 @@ __device__ __forceinline__ void gemm_epilogue(const P& pr, int pid, int m0, int 
     unsigned long long csg[4];
     const bool caff = pr.c_affine(pid, n0, BN);
     const int cbase = caff ? (int)pr.colC(pid, n0) : 0;
+    if constexpr (has_colc4<P>::value) pr.colC4(pid, n0 + wc + 2 * (lane & 3), cofs);
 #pragma unroll
     for (int fn = 0; fn < 4; ++fn) {
         const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
         const bool ok = col < N;
-        cofs[fn] = ok ? (caff ? cbase + (col - n0) : (int)pr.colC(pid, col)) : 0;
+        if constexpr (!has_colc4<P>::value) cofs[fn] = ok ? (caff ? cbase + (col - n0) : (int)pr.colC(pid, col)) : 0;
         csg[fn] = ok && pr.negC(pid, col) ? 0x8000000000000000ULL : 0ULL;
     }
     auto flip = [](double v, unsigned long long m) { return __longlong_as_double(__double_as_longlong(v) ^ m); };
