@@ -729,6 +729,16 @@ __device__ __forceinline__ int g_col(const Geo& g, int p, int am, int n) {
     const int sl = s & ((1 << g.lgib) - 1);
     return 2 * ((((gx * 2 + p) * g.nbins + bin) << g.lgib) + sl) + (nn & 1);
 }
+// Table offsets in closed form (no dependent global load at CTA start; the
+// host tables' offset arrays, sgl_tables.cpp, hold the same values -- pinned by
+// tests/test_tables_and_model.py): Legendre problem 2|m| + p starts after
+// sum_{|m'| < |m|} (B - |m'|) rows plus, for p = 1, the (B - |m| + 1) / 2 rows of
+// parity 0; radial degree l after sum_{l' < l} (B - l') rows of 2B.
+__device__ __forceinline__ int leg_table_off(int B, int pid) {
+    const int am = pid >> 1, p = pid & 1;
+    return (B + (B & 1)) * (am * B - am * (am - 1) / 2 + p * ((B - am + 1) / 2));
+}
+__device__ __forceinline__ int rad_table_off(int B, int l) { return 2 * B * (l * B - l * (l - 1) / 2); }
 __device__ __forceinline__ int g_rowstride(const Geo& g) { return (2 * (int)g.ngx * 2 * g.nbins) << g.lgib; }
 
 struct LegFwd {
@@ -749,7 +759,7 @@ struct LegFwd {
     static constexpr bool B_COL_AFFINE = false;  // blocked G: per-column offsets
     // end (exclusive) of the sign half that column n0 lies in
     __device__ int nlim(int pid, int n0) const { return n0 < g.NB ? (int)g.NB : N(pid); }
-    __device__ long long rowA(int pid, int r) const { return aoff[pid] + r * lstride(); }
+    __device__ long long rowA(int pid, int r) const { return leg_table_off(g.B, pid) + r * lstride(); }
     __device__ long long colA(int, int k) const { return k; }
     __device__ int a_sr(int) const { return lstride(); }
     __device__ int a_sk(int) const { return 1; }
@@ -786,7 +796,7 @@ struct LegInv {
     __device__ int K(int pid) const { const int r = g.B - am(pid) - (pid & 1); return r > 0 ? (r + 1) / 2 : 0; }
     static constexpr bool B_COL_AFFINE = true;
     __device__ int nlim(int pid, int n0) const { return n0 < g.NB ? (int)g.NB : N(pid); }
-    __device__ long long rowA(int pid, int j) const { return aoff[pid] + j; }
+    __device__ long long rowA(int pid, int j) const { return leg_table_off(g.B, pid) + j; }
     __device__ long long colA(int, int k) const { return k * lstride(); }
     __device__ int a_sr(int) const { return 1; }
     __device__ int a_sk(int) const { return lstride(); }
@@ -860,7 +870,7 @@ struct RadFwd {
     __device__ int K(int) const { return 2 * g.B; }
     static constexpr bool B_COL_AFFINE = false;
     __device__ int nlim(int l, int) const { return N(l); }
-    __device__ long long rowA(int l, int r) const { return aoff[l] + r * 2 * g.B; }
+    __device__ long long rowA(int l, int r) const { return rad_table_off(g.B, l) + r * 2 * g.B; }
     __device__ long long colA(int, int k) const { return k; }
     __device__ int a_sr(int) const { return 2 * g.B; }
     __device__ int a_sk(int) const { return 1; }
@@ -910,7 +920,7 @@ struct RadInv {
     __device__ int K(int l) const { return g.B - l; }
     static constexpr bool B_COL_AFFINE = false;
     __device__ int nlim(int l, int) const { return N(l); }
-    __device__ long long rowA(int l, int i) const { return aoff[l] + i; }
+    __device__ long long rowA(int l, int i) const { return rad_table_off(g.B, l) + i; }
     __device__ long long colA(int, int k) const { return k * 2 * g.B; }
     __device__ int a_sr(int) const { return 1; }
     __device__ int a_sk(int) const { return 2 * g.B; }

@@ -99,6 +99,21 @@ def test_device_legendre_table_matches_closed_form(B):
                 assert np.abs(blk[row] - ref).max() < 1e-13
 
 
+@pytest.mark.parametrize("B", [1, 2, 7, 16, 33])
+def test_table_offsets_closed_form(B):
+    # the GEMM kernels compute these offsets in closed form instead of loading them
+    # (sgl_kernels.cu leg_table_off / rad_table_off)
+    o = Oracle(B)
+    t = host_tables(B, o.r, o.a_mod, o.b_cal)
+    ls = B + (B & 1)
+    for pid in range(2 * B):
+        am, p = pid >> 1, pid & 1
+        assert t["leg_off"][pid] == ls * (am * B - am * (am - 1) // 2 + p * ((B - am + 1) // 2))
+    for l in range(B):
+        off = 2 * B * (l * B - l * (l - 1) // 2)
+        assert t["W_off"][l] == off and t["V_off"][l] == off
+
+
 def test_device_tables_finite_at_b256():
     o = Oracle(256)
     t = host_tables(256, o.r, o.a_mod, o.b_cal)
