@@ -161,21 +161,38 @@ __device__ __forceinline__ void pair_sync() {
 // FFT reads global memory directly into registers and the last pass of the
 // inverse writes global memory directly, so only the middle exchanges touch
 // shared memory.  When IN_PLACE, all reads complete (pair_sync) before any write.
-template <int N, int R, int SIGN, bool IN_PLACE, class Ld, class St>
-__device__ __forceinline__ void stockham_pass(int Ns, int t, const double2* twp, Ld&& ld, St&& st) {
+// PAIRED (first pass only, Ns = 1, PER even): thread t runs the consecutive
+// butterflies j = t PER + b, so its inputs come in pairs of consecutive elements
+// (x, x + 1) that ld2(x, v0, v1) fetches with vector loads; the output position
+// j R + r of a first-pass butterfly depends on j alone, so any butterfly-to-thread
+// assignment is valid there.
+struct NoPairLoad {};
+template <int N, int R, int SIGN, bool IN_PLACE, class Ld, class St, class Ld2 = NoPairLoad>
+__device__ __forceinline__ void stockham_pass(int Ns, int t, const double2* twp, Ld&& ld, St&& st,
+                                              Ld2&& ld2 = NoPairLoad{}) {
     constexpr int T = FFTShape<N>::T;
     constexpr int NBF = N / R;          // butterflies in this pass
     constexpr int PER = NBF / T;        // butterflies per thread
+    constexpr bool PAIRED = !std::is_same_v<std::decay_t<Ld2>, NoPairLoad> && PER % 2 == 0;
+    auto bj = [&](int b) { return PAIRED ? t * PER + b : t + b * T; };
     double2 v[PER][R];
+    if constexpr (PAIRED) {
 #pragma unroll
-    for (int b = 0; b < PER; ++b) {
-        const int j = t + b * T;
+        for (int b = 0; b < PER; b += 2) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[b][r] = ld(j + r * NBF);
+            for (int r = 0; r < R; ++r) ld2(bj(b) + r * NBF, v[b][r], v[b + 1][r]);
+        }
+    } else {
+#pragma unroll
+        for (int b = 0; b < PER; ++b) {
+            const int j = bj(b);
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[b][r] = ld(j + r * NBF);
+        }
     }
 #pragma unroll
     for (int b = 0; b < PER; ++b) {
-        const int j = t + b * T;
+        const int j = bj(b);
         const int k = j & (Ns - 1);
         if (Ns > 1) {
 #pragma unroll
@@ -190,7 +207,7 @@ __device__ __forceinline__ void stockham_pass(int Ns, int t, const double2* twp,
     if (IN_PLACE) pair_sync<N>();
 #pragma unroll
     for (int b = 0; b < PER; ++b) {
-        const int j = t + b * T;
+        const int j = bj(b);
         const int k = j & (Ns - 1);
         const int base = (j - k) * R + k;
 #pragma unroll
@@ -200,8 +217,9 @@ __device__ __forceinline__ void stockham_pass(int Ns, int t, const double2* twp,
 
 // Full FFT of one ring: first pass reads ld, last pass writes st, middle
 // passes run in place on `ring` (padded).  Ends without a trailing sync.
-template <int N, int SIGN, bool FIRST_IN_PLACE, class Ld, class St>
-__device__ __forceinline__ void ring_fft_io(double2* ring, int t, const double2* tw, Ld&& ld, St&& st) {
+template <int N, int SIGN, bool FIRST_IN_PLACE, class Ld, class St, class Ld2 = NoPairLoad>
+__device__ __forceinline__ void ring_fft_io(double2* ring, int t, const double2* tw, Ld&& ld, St&& st,
+                                            Ld2&& ld2 = NoPairLoad{}) {
     using S = FFTShape<N>;
     auto rd = [&](int x) { return ring[phys(x)]; };
     auto wr = [&](int x, double2 v) { ring[phys(x)] = v; };
@@ -209,15 +227,15 @@ __device__ __forceinline__ void ring_fft_io(double2* ring, int t, const double2*
     constexpr int P16 = (N >= 16) ? (S::LOGN - (head ? ilog2c(S::R0) : 0)) / 4 : 0;
     constexpr int NPASS = (head ? 1 : 0) + P16;
     if constexpr (NPASS == 1) {
-        if constexpr (head) stockham_pass<N, S::R0, SIGN, FIRST_IN_PLACE>(1, t, tw, ld, st);
-        else stockham_pass<N, 16, SIGN, FIRST_IN_PLACE>(1, t, tw, ld, st);
+        if constexpr (head) stockham_pass<N, S::R0, SIGN, FIRST_IN_PLACE>(1, t, tw, ld, st, ld2);
+        else stockham_pass<N, 16, SIGN, FIRST_IN_PLACE>(1, t, tw, ld, st, ld2);
     } else {
         int Ns = 1;
         if constexpr (head) {
-            stockham_pass<N, S::R0, SIGN, FIRST_IN_PLACE>(Ns, t, tw, ld, wr);
+            stockham_pass<N, S::R0, SIGN, FIRST_IN_PLACE>(Ns, t, tw, ld, wr, ld2);
             Ns *= S::R0;
         } else {
-            stockham_pass<N, 16, SIGN, FIRST_IN_PLACE>(Ns, t, tw, ld, wr);
+            stockham_pass<N, 16, SIGN, FIRST_IN_PLACE>(Ns, t, tw, ld, wr, ld2);
             Ns *= 16;
         }
         pair_sync<N>();
@@ -413,9 +431,20 @@ az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, doub
             src2 = X + f * fstride + ((size_t)i * N + (N - 1 - jp)) * N;
         }
         double2* ring = rings + q * S::STRIDE;
+        // first-pass inputs in pairs of consecutive samples: 16-byte loads of both rings
+        auto ld2 = [&](int x, double2& z0, double2& z1) {
+            if (ok) {
+                const double2 a = __ldcs(reinterpret_cast<const double2*>(src1 + x));
+                const double2 b = __ldcs(reinterpret_cast<const double2*>(src2 + x));
+                z0 = make_double2(a.x, b.x);
+                z1 = make_double2(a.y, b.y);
+            } else {
+                z0 = z1 = make_double2(0.0, 0.0);
+            }
+        };
         ring_fft_io<N, -1, false>(
             ring, tt, twg, [&](int x) { return ok ? make_double2(__ldcs(src1 + x), __ldcs(src2 + x)) : make_double2(0.0, 0.0); },
-            [&](int x, double2 v) { ring[phys(x)] = v; });
+            [&](int x, double2 v) { ring[phys(x)] = v; }, ld2);
     }
     __syncthreads();
     const double b = __ldg(bcal + jp);
@@ -478,23 +507,21 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
             dst2 = X + f * fstride + ((size_t)i * N + (N - 1 - jp)) * N;
         }
         double2* ring = rings + q * S::STRIDE;
-        ring_fft_io<N, +1, false>(
-            ring, tt, twg,
-            [&](int bin) {
-                if (bin == B) return make_double2(0.0, 0.0);
-                const int m = bin < B ? bin : N - bin;
-                const double2 e = e_buf[m], o = e_buf[B + m];
-                const double2 x1 = cadd(e, o), x2 = csub(e, o);
-                if (bin == 0) return make_double2(x1.x, x2.x);
-                if (bin < B) return make_double2(x1.x - x2.y, x1.y + x2.x);  // X1 + i X2
-                return make_double2(x1.x + x2.y, x2.x - x1.y);                // conj X1 + i conj X2
-            },
-            [&](int x, double2 v) {
-                if (ok) {
-                    __stcs(dst1 + x, v.x);
-                    __stcs(dst2 + x, v.y);
-                }
-            });
+        auto in = [&](int bin) {
+            if (bin == B) return make_double2(0.0, 0.0);
+            const int m = bin < B ? bin : N - bin;
+            const double2 e = e_buf[m], o = e_buf[B + m];
+            const double2 x1 = cadd(e, o), x2 = csub(e, o);
+            if (bin == 0) return make_double2(x1.x, x2.x);
+            if (bin < B) return make_double2(x1.x - x2.y, x1.y + x2.x);  // X1 + i X2
+            return make_double2(x1.x + x2.y, x2.x - x1.y);                // conj X1 + i conj X2
+        };
+        ring_fft_io<N, +1, false>(ring, tt, twg, in, [&](int x, double2 v) {
+            if (ok) {
+                __stcs(dst1 + x, v.x);
+                __stcs(dst2 + x, v.y);
+            }
+        });
     }
 }
 
