@@ -471,10 +471,12 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
     using S = FFTShape<N>;
     constexpr int B = N / 2;
     constexpr int IGR = 2 * S::IG;
-    constexpr int EOS = N + 1;  // per shell: E[0..B) then O[0..B), padded
+    constexpr int EOS = S::STRIDE;  // per shell: E[0..B) then O[0..B), in the shell's own ring buffer
     extern __shared__ double2 smem[];
     double2* rings = smem;  // twiddles: per-pass tables from global
-    double2* eo = rings + IGR * S::STRIDE;
+    // E/O rows share the ring buffers (the first FFT pass reads all its inputs
+    // before its pair-synchronized writes), halving the CTA's shared memory
+    double2* eo = rings;
     const int tid = threadIdx.x;
     const int jp = blockIdx.y;
     const int s0 = blockIdx.x * IGR;
@@ -516,7 +518,7 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
             if (bin < B) return make_double2(x1.x - x2.y, x1.y + x2.x);  // X1 + i X2
             return make_double2(x1.x + x2.y, x2.x - x1.y);                // conj X1 + i conj X2
         };
-        ring_fft_io<N, +1, false>(ring, tt, twg, in, [&](int x, double2 v) {
+        ring_fft_io<N, +1, true>(ring, tt, twg, in, [&](int x, double2 v) {
             if (ok) {
                 __stcs(dst1 + x, v.x);
                 __stcs(dst2 + x, v.y);
@@ -548,7 +550,7 @@ static int az_inv_real_launch(const Geo& g, const double* G, double* X, size_t f
                               cudaStream_t s) {
     using S = FFTShape<N>;
     constexpr int IGR = 2 * S::IG;
-    const size_t smem = sizeof(double2) * (IGR * S::STRIDE + IGR * (N + 1));
+    const size_t smem = sizeof(double2) * (IGR * S::STRIDE);  // E/O rows live in the ring buffers
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(az_inverse_real_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
