@@ -116,8 +116,8 @@ __device__ __forceinline__ int phys(int x) { return x + (x >> 4); }
 #ifndef SGL_AZI_ELEMS
 #define SGL_AZI_ELEMS SGL_AZ_ELEMS  // inverse kernel tile size
 #endif
-#ifndef SGL_AZI_MINB
-#define SGL_AZI_MINB SGL_AZ_MINB
+#ifndef SGL_AZ_BIG512
+#define SGL_AZ_BIG512 1
 #endif
 
 template <int N, int ELEMS = SGL_AZ_ELEMS>
@@ -127,8 +127,12 @@ struct FFTShape {
     static constexpr int STRIDE = N + N / 16 + 1;   // padded ring stride (complex)
     static constexpr int LOGN = ilog2c(N);
     static constexpr int R0 = 1 << (LOGN % 4 == 0 ? (N < 16 ? LOGN : 4) : LOGN % 4);  // first radix
-    static constexpr int IG = (T * 2 <= 256) ? (ELEMS / 16) / T : 1;  // shell pairs per CTA
+    // N = 512 (B = 256) takes twice the elements per CTA: 4-shell G groups (64-byte
+    // runs for the Legendre GEMMs instead of 32) at 256 threads and 2 CTAs/SM
+    static constexpr int EL = (N >= 512 && SGL_AZ_BIG512) ? 2 * ELEMS : ELEMS;
+    static constexpr int IG = (T * 2 <= 256) ? (EL / 16) / T : 1;  // shell pairs per CTA
     static constexpr int THREADS = 2 * IG * T;
+    static constexpr int MINB = SGL_AZ_MINB * 128 / THREADS > 0 ? SGL_AZ_MINB * 128 / THREADS : 1;  // CTAs/SM
     // twiddle table: N plain entries, then 15 Ns entries per pass after the first
     // (sgl_tables.cpp); HEAD: a leading small-radix pass
     static constexpr bool HEAD = (R0 != RMAX || N < 16);
@@ -282,7 +286,7 @@ __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.w
 // parts, applies b_cal and writes rows of G[p][|m|][j'][sgn][s] (IG shells
 // contiguous per row).
 template <int N>
-__global__ void __launch_bounds__(FFTShape<N>::THREADS, SGL_AZ_MINB)
+__global__ void __launch_bounds__(FFTShape<N>::THREADS, FFTShape<N>::MINB)
 az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2* __restrict__ G,
                   const double* __restrict__ bcal, const double2* __restrict__ twg) {
     using S = FFTShape<N>;
@@ -335,7 +339,7 @@ az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2*
 // from both buffers (Nyquist bin B zero); the last pass writes the psi-order
 // samples straight to HBM (coalesced).
 template <int N>
-__global__ void __launch_bounds__(FFTShape<N, SGL_AZI_ELEMS>::THREADS, SGL_AZI_MINB)
+__global__ void __launch_bounds__(FFTShape<N, SGL_AZI_ELEMS>::THREADS, (FFTShape<N, SGL_AZI_ELEMS>::MINB))
 az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X, size_t fstride,
                   const double2* __restrict__ twg) {
     using S = FFTShape<N, SGL_AZI_ELEMS>;
@@ -407,7 +411,7 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
 // in (8 B per sample) and half the FFTs of the complex path.  CTA: 2*IG shells,
 // one packed ring each (same thread count and shared memory as the complex path).
 template <int N>
-__global__ void __launch_bounds__(FFTShape<N>::THREADS, SGL_AZ_MINB)
+__global__ void __launch_bounds__(FFTShape<N>::THREADS, FFTShape<N>::MINB)
 az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, double2* __restrict__ G,
                        const double* __restrict__ bcal, const double2* __restrict__ twg) {
     using S = FFTShape<N>;
@@ -465,7 +469,7 @@ az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, doub
 }
 
 template <int N>
-__global__ void __launch_bounds__(FFTShape<N>::THREADS, SGL_AZ_MINB)
+__global__ void __launch_bounds__(FFTShape<N>::THREADS, FFTShape<N>::MINB)
 az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict__ X, size_t fstride,
                        const double2* __restrict__ twg) {
     using S = FFTShape<N>;
