@@ -45,6 +45,25 @@ def test_inverse_and_forward_match_oracle(B):
     assert normwise(f, c) <= TOL  # round trip through the oracle grid
 
 
+@pytest.mark.parametrize("B", [7, 9, 33])
+def test_odd_bandlimit_batch_matches_oracle(B):
+    # odd B: Legendre table rows padded to an even length (16-byte A units), the
+    # naive DFT azimuthal kernels for non-power-of-two 2B, and a batch of three
+    import torch
+
+    plan, orc = plan_for(B)
+    rng = np.random.default_rng(3000 + B)
+    n, ns = coefficient_count(B), sample_count(B)
+    c = np.stack([complex_normal(rng, n) for _ in range(3)])
+    x = np.stack([complex_normal(rng, ns) for _ in range(3)])
+    g = sgl.ifsglft_batch(plan, torch.from_numpy(c).cuda()).cpu().numpy()
+    f = sgl.fsglft_batch(plan, torch.from_numpy(x).cuda()).cpu().numpy()
+    for b in range(3):
+        assert np.isfinite(g[b]).all() and np.isfinite(f[b]).all()
+        assert per_shell(g[b], orc.inverse(c[b]), B) <= TOL
+        assert normwise(f[b], orc.forward(x[b])) <= TOL
+
+
 def test_forward_random_grid_matches_oracle():
     # a non-bandlimited input: every stage contributes
     for B in (4, 16, 32):
