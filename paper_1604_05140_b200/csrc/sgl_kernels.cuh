@@ -43,12 +43,12 @@ constexpr int tile_rows(int wm) { return 32 * wm; }
 constexpr int tile_cols(int wm) { return 128 / wm; }
 // Largest wm each kind's kernel is built for (its shared-memory ring is sized for
 // the largest stage it can see): the Legendre-forward problems have M <= B/2 + 1
-// rows, so 128-row tiles never win there and its ring is sized for wm <= 2.
+// rows and always took 32 x 128 tiles, the only shape its TMA-fed kernel has.
 // The Legendre inverse (B columns affine in n) has a second kernel whose CTAs run
 // several consecutive n-blocks of a problem as one pipelined chunk sequence; the
 // count is chosen per launch (TileMap::seq) and seq > 1 selects that kernel.
 #ifndef SGL_MAXWM_LEGFWD
-#define SGL_MAXWM_LEGFWD 2
+#define SGL_MAXWM_LEGFWD 1  // 32 x 128 tiles (the only shape the tile chooser picked; the TMA-fed kernel's)
 #endif
 #ifndef SGL_MAXWM_LEGINV
 #define SGL_MAXWM_LEGINV 4
