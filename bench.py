@@ -394,7 +394,7 @@ def main():
     try:
         with open(os.path.join(REPO, "profiles", "r01_traffic.json")) as f:
             tr = json.load(f)["bytes"]
-        knames = {0: [f"void az_forward_kernel<{2 * B}>"], 1: ["void gemm_dmma_kernel<LegFwd>"],
+        knames = {0: [f"void az_forward_kernel<{2 * B}>"], 1: ["void gemm_dmma_kernel<LegFwdTma>", "void gemm_dmma_kernel<LegFwd>"],
                   2: ["void gemm_dmma_kernel<RadFwd>"], 3: ["void gemm_dmma_kernel<RadInv>"],
                   4: ["void gemm_dmma_kernel<LegInvSeq>", "void gemm_dmma_kernel<LegInv>"],
                   5: [f"void az_inverse_kernel<{2 * B}>"]}[dom]
