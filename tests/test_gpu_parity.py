@@ -92,6 +92,27 @@ def test_batched_device_matches_single(B):
         assert normwise(back[b], c[b]) <= TOL
 
 
+def test_batched_b128_matches_single_function():
+    # B = 128: the TMA-fed Legendre forward with several functions in G (the group
+    # coordinate runs over the batch) against one-function calls
+    import torch
+
+    B = 128
+    plan, _ = plan_for(B)
+    rng = np.random.default_rng(128)
+    nb = 3
+    c = complex_normal(rng, nb * coefficient_count(B)).reshape(nb, -1)
+    dg = sgl.ifsglft_batch(plan, torch.from_numpy(c).cuda())
+    db = sgl.fsglft_batch(plan, dg).cpu().numpy()
+    g = dg.cpu().numpy()
+    for b in range(nb):
+        g1 = sgl.ifsglft(sgl.SglCoefficients(B, c[b]), plan).values
+        f1 = sgl.fsglft(sgl.SampleGrid(B, g[b]), plan).values
+        assert per_shell(g[b], g1, B) <= 1e-14
+        assert normwise(db[b], f1) <= 1e-14
+        assert normwise(db[b], c[b]) <= TOL
+
+
 def test_roundtrip_b256():
     B = 256
     plan, orc = plan_for(B)
@@ -243,7 +264,7 @@ def test_config_c5_real_valued_b32():
 
 
 # ----------------------------------------------------------------- multi-GPU stage entry points
-@pytest.mark.parametrize("B,W,batch", [(16, 2, 1), (16, 4, 3), (64, 8, 1)])
+@pytest.mark.parametrize("B,W,batch", [(16, 2, 1), (16, 4, 3), (64, 8, 1), (128, 8, 1)])
 def test_stage_entry_points_emulated_split(B, W, batch):
     """The shell / (l, m) decomposition of paper_1604_05140_b200.distributed with the
     CUDA stages, all ranks emulated one after another on one GPU (the all-to-all
@@ -476,7 +497,7 @@ def test_separated_cross_oracle_rejects_large_bandlimit():
 
 
 # ---------------------------------------------------------------- fused exchange (peer stores instead of all-to-all)
-@pytest.mark.parametrize("B,W,nb", [(8, 2, 1), (16, 4, 2), (32, 8, 1)])
+@pytest.mark.parametrize("B,W,nb", [(8, 2, 1), (16, 4, 2), (32, 8, 1), (128, 8, 1)])
 def test_fused_exchange_emulated_ranks(B, W, nb):
     """The peer-store epilogues with W virtual ranks on one device (receive buffers
     as local allocations): every rank's spherical stage writes its S rows into the
