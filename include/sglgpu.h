@@ -145,8 +145,15 @@ int sglgpu_spherical_inverse(sglgpu_plan* plan, const double* shells, double* sa
  *   ([b * spb, (b+1) * spb)) is stored in rank b's full-nu S buffer dst[b]
  *   ([nu][f][i_local], NB = 2 * batch * spb), which sglgpu_spherical_inverse
  *   then reads; ndst = 2B / spb <= 8.
+ * radial_forward_to: like sglgpu_radial_forward (shell blocks of spb shells,
+ *   degrees [l_begin, l_end)), but every coefficient is stored into each of the
+ *   ndst <= 8 omega-order coefficient vectors dst[q] (batch * Omega complex each):
+ *   with disjoint degree ranges per rank this assembles the full vector on every
+ *   rank (replaces the all-reduce; fsglft's output).
  * The caller orders the peers' kernels (e.g. an NCCL barrier on the stream)
  * before the receive buffers are read. */
+int sglgpu_radial_forward_to(sglgpu_plan* plan, const double* shells, int l_begin, int l_end, int shells_per_block,
+                             size_t batch, int ndst, double* const* dst, void* stream);
 int sglgpu_spherical_forward_to(sglgpu_plan* plan, const double* samples, size_t sample_stride, int shell_begin,
                                 int shell_count, size_t batch, int ndst, double* const* dst, const int* l_bounds,
                                 void* stream);

@@ -65,8 +65,9 @@ def lib():
                                          _vp]
         L.sglgpu_spherical_forward_to.argtypes = [_vp, _vp, ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
                                                   ctypes.c_size_t, ctypes.c_int, _vp, _vp, _vp]
-        L.sglgpu_radial_inverse_to.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                               ctypes.c_size_t, ctypes.c_int, _vp, _vp]
+        for name in ("sglgpu_radial_inverse_to", "sglgpu_radial_forward_to"):
+            getattr(L, name).argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_size_t, ctypes.c_int, _vp, _vp]
         L.sglgpu_device_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(_vp)]
         L.sglgpu_device_free.argtypes = [_vp]
         L.sglgpu_ipc_export.argtypes = [_vp, _vp]

@@ -1019,6 +1019,36 @@ int sglgpu_spherical_forward_to(sglgpu_plan* p, const double* samples, size_t sa
     });
 }
 
+int sglgpu_radial_forward_to(sglgpu_plan* p, const double* shells, int l_begin, int l_end, int shells_per_block,
+                             size_t batch, int ndst, double* const* dst, void* stream) {
+    return guarded([&] {
+        check_plan(p);
+        const int B = p->B;
+        check_stage_batch(B, batch, "sglgpu_radial_forward_to");
+        if (l_begin < 0 || l_end > B || l_begin > l_end) fail(SGLGPU_EINVAL, "sglgpu_radial_forward_to: bad l range");
+        if (shells_per_block < 1 || (2 * B) % shells_per_block != 0)
+            fail(SGLGPU_EINVAL, "sglgpu_radial_forward_to: shells_per_block must divide 2B");
+        if (ndst < 1 || ndst > sglk::kMaxPeers || !dst)
+            fail(SGLGPU_EINVAL, "sglgpu_radial_forward_to: 1..8 destination coefficient vectors required");
+        for (int q = 0; q < ndst; ++q)
+            if (!dst[q]) fail(SGLGPU_EINVAL, "sglgpu_radial_forward_to: null destination");
+        if (batch == 0 || l_begin == l_end) return;
+        std::lock_guard<std::mutex> lock(p->mu);
+        set_device(p);
+        const int nb = (int)batch, sc = shells_per_block;
+        sglk::Geo g{B, sc, nb, 2LL * nb * sc};
+        const long long nu0 = (long long)l_begin * l_begin, nnu = (long long)l_end * l_end - nu0;
+        sglk::PeerDest pd;
+        pd.n = ndst;
+        for (int q = 0; q < ndst; ++q) pd.base[q] = dst[q];
+        auto rt = tiles_for(p, kRadFwd, nb, sc, l_begin, l_end);
+        int k = sglk::launch_radial_forward_bcast(g, sglk::RadialBlocks{sc, nnu * g.NB, nu0}, shells, pd, p->d_W,
+                                                  p->d_W_off, rt.first, rt.second, static_cast<cudaStream_t>(stream));
+        ck_launch(k, "radial_forward");
+        p->last_launches = k;
+    });
+}
+
 int sglgpu_radial_inverse_to(sglgpu_plan* p, const double* coeffs, int l_begin, int l_end, int shells_per_block,
                              size_t batch, int ndst, double* const* dst, void* stream) {
     return guarded([&] {

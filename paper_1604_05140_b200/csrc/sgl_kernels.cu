@@ -1039,6 +1039,14 @@ struct LegFwdTma : LegFwd {
 struct LegInvSeq : LegInv {  // CTAs run TileMap::seq consecutive n-blocks
     static constexpr bool GEMM_SEQ = true;
 };
+// Radial forward of one rank's degree range under the multi-GPU split whose
+// coefficients are stored into every rank's coefficient vector (pd.base[q]; the
+// degree ranges are disjoint, so each entry is written by exactly one rank): the
+// assembly all-reduce becomes NVLink peer stores overlapped with the GEMM.
+struct RadFwdBcast : RadFwd {
+    PeerDest pd;
+    static constexpr bool BCAST = true;
+};
 struct RadInvPeers : RadInv {
     PeerDest pd;  // shell block b goes to its owner (base[b])
     __device__ double* out_row(int l, int i) const {
@@ -1066,6 +1074,11 @@ template <class P, class = void>
 struct has_btma : std::false_type {};
 template <class P>
 struct has_btma<P, std::void_t<decltype(P::B_TMA)>> : std::bool_constant<P::B_TMA> {};
+
+template <class P, class = void>
+struct has_bcast : std::false_type {};
+template <class P>
+struct has_bcast<P, std::void_t<decltype(P::BCAST)>> : std::bool_constant<P::BCAST> {};
 
 template <class P, class = void>
 struct has_mirror : std::false_type {};
@@ -1177,6 +1190,26 @@ __device__ __forceinline__ void gemm_epilogue(const P& pr, int pid, int m0, int 
         double* out;
         if constexpr (has_out_row<P>::value) out = pr.out_row(pid, row);
         else out = pr.C + (int)pr.rowC(pid, row);
+        if constexpr (has_bcast<P>::value) {  // every destination gets the row (pr.C unused)
+            const int ro = (int)pr.rowC(pid, row);
+#pragma unroll
+            for (int fn = 0; fn < 4; ++fn) {
+                const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
+                if (col >= N) continue;
+                const double2 v = make_double2(flip(acc[fm][fn][0], csg[fn]), flip(acc[fm][fn][1], csg[fn]));
+                bool neg = false;
+                const long long mo = has_mirror<P>::value ? pr.colC_mirror(pid, col, neg) : -1;
+                const unsigned long long ms = neg ? 0x8000000000000000ULL : 0ULL;
+                for (int q = 0; q < pr.pd.n; ++q) {
+                    double* o = pr.pd.base[q] + ro;
+                    *reinterpret_cast<double2*>(o + cofs[fn]) = v;
+                    if (mo >= 0)  // (-1)^m conj (real path)
+                        *reinterpret_cast<double2*>(o + mo) =
+                            make_double2(flip(acc[fm][fn][0], ms), flip(acc[fm][fn][1], ms ^ 0x8000000000000000ULL));
+                }
+            }
+            continue;
+        }
 #pragma unroll
         for (int fn = 0; fn < 4; ++fn) {
             const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
@@ -1684,6 +1717,16 @@ int launch_radial_forward(const Geo& g, const RadialBlocks& rb, const double* S,
                           cudaStream_t s) {
     RadFwd p{g, W, w_off, S, C, degree_offset(g.B + 1), ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
     return gemm_launch<RadFwd>(p, tiles, ntiles, s);
+}
+
+int launch_radial_forward_bcast(const Geo& g, const RadialBlocks& rb, const double* S, const PeerDest& pd,
+                                const double* W, const long long* w_off, const TileMap* tiles, int ntiles,
+                                cudaStream_t s) {
+    RadFwdBcast p;
+    static_cast<RadFwd&>(p) = RadFwd{g, W, w_off, S, nullptr, degree_offset(g.B + 1),
+                                     ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
+    p.pd = pd;
+    return gemm_launch<RadFwdBcast>(p, tiles, ntiles, s);
 }
 
 int launch_radial_inverse(const Geo& g, const RadialBlocks& rb, const double* C, double* S,

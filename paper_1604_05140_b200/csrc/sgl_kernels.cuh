@@ -143,6 +143,10 @@ struct PeerDest {
 int launch_legendre_forward_peers(const Geo& g, const SView& sv, const double* G, const PeerDest& pd,
                                   const double* tab, const long long* tab_off, const TileMap* tiles, int ntiles,
                                   cudaStream_t s);
+// Radial forward whose coefficients go to every destination (pd.base[q], pd.n of them).
+int launch_radial_forward_bcast(const Geo& g, const RadialBlocks& rb, const double* S, const PeerDest& pd,
+                                const double* W, const long long* w_off, const TileMap* tiles, int ntiles,
+                                cudaStream_t s);
 // Radial inverse whose shell blocks go straight to the shells' owners.
 int launch_radial_inverse_peers(const Geo& g, const RadialBlocks& rb, const double* C, const PeerDest& pd,
                                 const double* V, const long long* v_off, const TileMap* tiles, int ntiles,

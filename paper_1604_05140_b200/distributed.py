@@ -24,7 +24,9 @@ The fused variant (`fsglft_distributed_fused` / `ifsglft_distributed_fused`)
 replaces the all-to-all by NVLink peer stores from the producing kernel's
 epilogue into the consumers' receive buffers (mapped with CUDA IPC,
 `PeerBuffers`), so the exchange overlaps the Legendre / radial-inverse GEMM
-tile by tile; a one-element all_reduce on the stream orders the stores.
+tile by tile; a one-element all_reduce on the stream orders the stores.  The
+coefficient assembly is fused the same way: each rank's radial-forward epilogue
+stores its degrees into every rank's coefficient vectors (no all-reduce).
 
 Degree ranges are balanced by the radial work (2l+1)(B-l) per degree.
 Batched transforms need none of this: shard whole functions across ranks.
@@ -133,9 +135,10 @@ class PeerBuffers:
     On a node the peers' buffers are mapped with CUDA IPC (`exchange`); `local`
     builds the same structure for W virtual ranks on one device (tests)."""
 
-    def __init__(self, part: "Partition", batch: int, fwd_ptrs, inv_ptrs, owned, opened):
+    def __init__(self, part: "Partition", batch: int, fwd_ptrs, inv_ptrs, owned, opened, coef_ptrs=None):
         self.part, self.batch = part, batch
         self.fwd, self.inv = fwd_ptrs, inv_ptrs
+        self.coef = coef_ptrs or []  # coef[q]: rank q's omega-order coefficient vectors (batch x Omega)
         self._owned, self._opened = owned, opened
 
     @staticmethod
@@ -143,6 +146,11 @@ class PeerBuffers:
         row = batch * part.shells_per_rank  # complex per nu row of a shell block
         nu0, nu1 = part.nu_range(q)
         return part.world * (nu1 - nu0) * row * 16, part.B * part.B * row * 16
+
+    @staticmethod
+    def coef_bytes(part: "Partition", batch: int):
+        B = part.B
+        return batch * (B * (B + 1) * (2 * B + 1) // 6) * 16
 
     @staticmethod
     def _alloc(L, nbytes):
@@ -159,12 +167,13 @@ class PeerBuffers:
         import paper_1604_05140_b200 as sgl
 
         L = sgl.lib()
-        fwd, inv = [], []
+        fwd, inv, coef = [], [], []
         for q in range(part.world):
             fb, ib = cls.sizes(part, batch, q)
             fwd.append(cls._alloc(L, fb))
             inv.append(cls._alloc(L, ib))
-        return cls(part, batch, fwd, inv, fwd + inv, [])
+            coef.append(cls._alloc(L, cls.coef_bytes(part, batch)))
+        return cls(part, batch, fwd, inv, fwd + inv + coef, [], coef)
 
     @classmethod
     def exchange(cls, part: "Partition", batch: int, dist, group=None):
@@ -176,7 +185,7 @@ class PeerBuffers:
         L = sgl.lib()
         r, W = dist.get_rank(group), part.world
         fb, ib = cls.sizes(part, batch, r)
-        mine = [cls._alloc(L, fb), cls._alloc(L, ib)]
+        mine = [cls._alloc(L, fb), cls._alloc(L, ib), cls._alloc(L, cls.coef_bytes(part, batch))]
         handles = []
         for p in mine:
             h = ctypes.create_string_buffer(64)
@@ -184,11 +193,12 @@ class PeerBuffers:
             handles.append(h.raw)
         allh = [None] * W
         dist.all_gather_object(allh, handles, group=group)
-        fwd, inv, opened = [], [], []
+        fwd, inv, coef, opened = [], [], [], []
         for q in range(W):
             if q == r:
                 fwd.append(mine[0])
                 inv.append(mine[1])
+                coef.append(mine[2])
                 continue
             ptrs = []
             for h in allh[q]:
@@ -198,7 +208,8 @@ class PeerBuffers:
                 opened.append(p.value)
             fwd.append(ptrs[0])
             inv.append(ptrs[1])
-        return cls(part, batch, fwd, inv, mine, opened)
+            coef.append(ptrs[2])
+        return cls(part, batch, fwd, inv, mine, opened, coef)
 
     def close(self):
         import paper_1604_05140_b200 as sgl
@@ -225,6 +236,24 @@ class PeerBuffers:
         import ctypes
 
         return (ctypes.c_void_p * self.part.world)(*self.inv)
+
+    def coef_dst(self):
+        import ctypes
+
+        return (ctypes.c_void_p * self.part.world)(*self.coef)
+
+    def coef_tensor(self, r: int):
+        """Rank r's coefficient vectors as a (batch, Omega) complex128 CUDA tensor view."""
+        import torch
+
+        B = self.part.B
+        omega = B * (B + 1) * (2 * B + 1) // 6
+
+        class _View:  # __cuda_array_interface__ over the raw allocation
+            __cuda_array_interface__ = {"shape": (self.batch, omega), "typestr": "<c16",
+                                        "data": (self.coef[r], False), "version": 3, "strides": None}
+
+        return torch.as_tensor(_View(), device="cuda")
 
 
 def _stream_of(t):
@@ -255,6 +284,17 @@ def fused_forward_radial(part: "Partition", stages: "CudaStages", peers: PeerBuf
         stages.sgl._check(stages.L.sglgpu_radial_forward(
             stages.plan.handle, peers.fwd[rank], coeffs.data_ptr(), l0, l1, part.shells_per_rank, peers.batch,
             _stream_of(coeffs)))
+
+
+def fused_forward_radial_bcast(part: "Partition", stages: "CudaStages", peers: PeerBuffers, rank: int, stream=None):
+    """Step 2 with the assembly fused in: rank `rank`'s radial stage stores its
+    degrees into EVERY rank's coefficient vectors (peers.coef, NVLink peer stores
+    from the GEMM epilogue; sglgpu_radial_forward_to) -- no all-reduce."""
+    l0, l1 = part.l_ranges[rank]
+    if l1 > l0:
+        stages.sgl._check(stages.L.sglgpu_radial_forward_to(
+            stages.plan.handle, peers.fwd[rank], l0, l1, part.shells_per_rank, peers.batch, part.world,
+            peers.coef_dst(), stream))
 
 
 def fused_inverse_radial(coeffs, part: "Partition", stages: "CudaStages", peers: PeerBuffers, rank: int):
@@ -297,6 +337,12 @@ def fsglft_distributed_fused(samples_local, part: "Partition", stages: "CudaStag
     r = dist.get_rank(group)
     fused_forward_spherical(samples_local, part, stages, peers, r, batch)
     _stream_barrier(dist, group, samples_local.device)
+    if peers.coef and part.world > 1:
+        # every rank's radial stage stores its degrees into all ranks' vectors
+        # (at one rank the all-reduce below is free and the extra barrier is not)
+        fused_forward_radial_bcast(part, stages, peers, r, _stream_of(samples_local))
+        _stream_barrier(dist, group, samples_local.device)
+        return peers.coef_tensor(r).clone()
     omega = part.B * (part.B + 1) * (2 * part.B + 1) // 6
     coeffs = torch.zeros((batch, omega), dtype=torch.complex128, device=samples_local.device)
     fused_forward_radial(part, stages, peers, r, coeffs)

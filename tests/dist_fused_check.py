@@ -17,8 +17,8 @@ sys.path.insert(0, os.path.dirname(HERE))
 import paper_1604_05140_b200 as sgl  # noqa: E402
 from oracle_bindings import Oracle, normwise  # noqa: E402
 from paper_1604_05140_b200.distributed import (CudaStages, Partition, PeerBuffers, fused_forward_radial,  # noqa: E402
-                                               fused_forward_spherical, fused_inverse_radial,
-                                               fused_inverse_spherical)
+                                               fused_forward_radial_bcast, fused_forward_spherical,
+                                               fused_inverse_radial, fused_inverse_spherical)
 
 
 def cpu_barrier():
@@ -54,6 +54,11 @@ def main():
     back = torch.view_as_real(coeffs).cpu()
     dist.all_reduce(back)  # disjoint degree ranges: the sum assembles the vector
     back = torch.view_as_complex(back).numpy()
+    # the fused assembly: every rank's radial epilogue stores its degrees into all
+    # ranks' (IPC-mapped) coefficient vectors
+    fused_forward_radial_bcast(part, st, peers, r)
+    cpu_barrier()
+    mine = peers.coef_tensor(r).cpu().numpy()
     s0, s1 = part.shell_range(r)
     nsh = 4 * B * B
     loc = loc.cpu().numpy()
@@ -61,6 +66,7 @@ def main():
         g_ref = orc.inverse(c[f])[s0 * nsh:s1 * nsh]
         assert normwise(loc[f], g_ref) < 1e-12, normwise(loc[f], g_ref)
         assert normwise(back[f], c[f]) < 1e-12, normwise(back[f], c[f])
+        assert np.array_equal(mine[f], back[f]), "broadcast assembly differs from the all-reduce"
     cpu_barrier()
     peers.close()
     if r == 0:

@@ -506,8 +506,8 @@ def test_fused_exchange_emulated_ranks(B, W, nb):
     import torch
 
     from paper_1604_05140_b200.distributed import (CudaStages, Partition, PeerBuffers, fused_forward_radial,
-                                                   fused_forward_spherical, fused_inverse_radial,
-                                                   fused_inverse_spherical)
+                                                   fused_forward_radial_bcast, fused_forward_spherical,
+                                                   fused_inverse_radial, fused_inverse_spherical)
 
     plan, orc = plan_for(B)
     part = Partition.make(B, W)
@@ -537,6 +537,12 @@ def test_fused_exchange_emulated_ranks(B, W, nb):
         back = coeffs.cpu().numpy()
         for f in range(nb):
             assert normwise(back[f], c[f]) <= TOL
+        # the fused assembly: each rank's radial stage stores into every rank's vectors
+        for r in range(W):
+            fused_forward_radial_bcast(part, st, peers, r)
+        torch.cuda.synchronize()
+        for q in range(W):
+            assert np.array_equal(peers.coef_tensor(q).cpu().numpy(), back)
     finally:
         peers.close()
 
