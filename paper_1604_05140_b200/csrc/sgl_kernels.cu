@@ -1397,7 +1397,8 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
                 const int gx0 = ((n0 - (sgn ? NB : 0)) >> 1) >> pr.g.lgib;
                 const unsigned bar = tma_bar0 + 8u * (unsigned)(v % ST);
                 mbar_expect_tx(bar, (unsigned)(BK * BN * sizeof(double)));
-                tma_load_5d(static_cast<unsigned>(__cvta_generic_to_shared(bs)), &pr.tmap, bar, 0, k0, gx0, bin, pid & 1);
+                tma_load_5d(static_cast<unsigned>(__cvta_generic_to_shared(bs)), &pr.tmap, bar, 0, k0, 0, gx0,
+                            (pid & 1) * pr.g.nbins + bin);
             }
             cp_async_commit();
             return;
@@ -1667,14 +1668,15 @@ static bool make_g_tensor_map(const Geo& g, const double* G, int bk, CUtensorMap
             return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
         return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }();
-    if (!encode || g.lgib != 2) return false;
-    const cuuint64_t W = 8, row = 2ULL * 2 * g.nbins * g.ngx * 4;  // complex per j' row x 2 -> doubles
-    const cuuint64_t dims[5] = {W, (cuuint64_t)g.B, (cuuint64_t)g.ngx, (cuuint64_t)g.nbins, 2};
-    const cuuint64_t strides[4] = {row * 8,                                   // j'
-                                   (cuuint64_t)2 * g.nbins * W * 8,          // group
-                                   W * 8,                                     // bin
-                                   (cuuint64_t)g.nbins * W * 8};             // p
-    const cuuint32_t box[5] = {8, (cuuint32_t)bk, 16, 1, 1};
+    // groups of 2^lgib shells = W = 2^(lgib+1) doubles, split into H blocks of 8
+    if (!encode || g.lgib < 2 || g.lgib > 6) return false;
+    const cuuint64_t W = 2ULL << g.lgib, H = W / 8, groups = (cuuint64_t)g.ngx;
+    const cuuint64_t row = 2ULL * groups * 2 * g.nbins * W / 2;  // doubles per j' row (g_rowstride)
+    // dims (innermost first): 8 doubles, j', block of 8 inside a group, group,
+    // (p, bin) as one index p * nbins + bin (its stride is W doubles either way)
+    const cuuint64_t dims[5] = {8, (cuuint64_t)g.B, H, groups, 2ULL * g.nbins};
+    const cuuint64_t strides[4] = {row * 8, 64, 2ULL * g.nbins * W * 8, W * 8};
+    const cuuint32_t box[5] = {8, (cuuint32_t)bk, (cuuint32_t)H, (cuuint32_t)(128 / W), 1};
     const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(G), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1684,7 +1686,7 @@ static bool make_g_tensor_map(const Geo& g, const double* G, int bk, CUtensorMap
 int launch_legendre_forward(const Geo& g, const SView& sv, const double* G, double* S, const double* tab,
                             const long long* tab_off, const TileMap* tiles, int ntiles, cudaStream_t s) {
     LegFwd p{g, tab, tab_off, G, S, sv};
-    if (SGL_LEGFWD_TMA && !g.real) {
+    if (SGL_LEGFWD_TMA) {
         LegFwdTma q;
         static_cast<LegFwd&>(q) = p;
         if (make_g_tensor_map(g, G, LegFwd::GEMM_BK, &q.tmap)) return gemm_launch<LegFwdTma>(q, tiles, ntiles, s);
