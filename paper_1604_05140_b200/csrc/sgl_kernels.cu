@@ -1036,6 +1036,16 @@ struct LegFwdTma : LegFwd {
     static constexpr int GEMM_MAXWM = 1;
     alignas(64) CUtensorMap tmap;  // G viewed as [p][bin][group][j'][8 doubles]
 };
+// ... and its multi-GPU form (S rows to their owners' receive buffers).
+struct LegFwdTmaPeers : LegFwdTma {
+    PeerDest pd;
+    __device__ double* out_row(int pid, int r) const {
+        const int l = am(pid) + (pid & 1) + 2 * r;
+        int q = 0;
+        while (q + 1 < pd.n && l >= pd.bound[q + 1]) ++q;
+        return pd.base[q] + rowC(pid, r);
+    }
+};
 struct LegInvSeq : LegInv {  // CTAs run TileMap::seq consecutive n-blocks
     static constexpr bool GEMM_SEQ = true;
 };
@@ -1697,6 +1707,12 @@ int launch_legendre_forward(const Geo& g, const SView& sv, const double* G, doub
 int launch_legendre_forward_peers(const Geo& g, const SView& sv, const double* G, const PeerDest& pd,
                                   const double* tab, const long long* tab_off, const TileMap* tiles, int ntiles,
                                   cudaStream_t s) {
+    if (SGL_LEGFWD_TMA) {
+        LegFwdTmaPeers q;
+        static_cast<LegFwd&>(q) = LegFwd{g, tab, tab_off, G, nullptr, sv};
+        q.pd = pd;
+        if (make_g_tensor_map(g, G, LegFwd::GEMM_BK, &q.tmap)) return gemm_launch<LegFwdTmaPeers>(q, tiles, ntiles, s);
+    }
     LegFwdPeers p;
     static_cast<LegFwd&>(p) = LegFwd{g, tab, tab_off, G, nullptr, sv};
     p.pd = pd;
