@@ -43,6 +43,7 @@ def test_library_is_sm100a_code():
     sass = subprocess.run(["cuobjdump", "-sass", sgl.LIB_PATH], capture_output=True, text=True).stdout
     assert "DMMA.8x8x4" in sass  # fp64 tensor-core contractions
     assert "LDGSTS" in sass       # cp.async staging
+    assert "UTMALDG" in sass      # TMA tensor loads (the Legendre forward's B tiles)
 
 
 def test_cpp_api_symbols_exported():
@@ -70,6 +71,9 @@ def test_plan_argument_validation():
     assert L.sglgpu_plan_create(ctypes.byref(d), ctypes.byref(h)) == sgl.SGLGPU_EINVAL
     assert b"increasing" in L.sglgpu_last_error()
     assert L.sglgpu_forward(None, None, None, 1, 0, None) == sgl.SGLGPU_EINVAL
+    # the fused-exchange entry points validate before touching a device
+    assert L.sglgpu_radial_forward_to(None, None, 0, 1, 1, 1, 1, None, None) == sgl.SGLGPU_EINVAL
+    assert L.sglgpu_radial_inverse_to(None, None, 0, 1, 1, 1, 1, None, None) == sgl.SGLGPU_EINVAL
 
 
 def test_transform_shape_errors_match_reference_messages():
