@@ -113,6 +113,62 @@ def test_batched_b128_matches_single_function():
         assert normwise(db[b], c[b]) <= TOL
 
 
+def _c4_coefficients(B, seed, count=1):
+    """BASELINE config C4: iid complex normal scaled by (1 + l)^-1."""
+    rng = np.random.default_rng(seed)
+    l = np.zeros(coefficient_count(B), dtype=int)
+    for n in range(1, B + 1):
+        for ll in range(n):
+            s = sgl.omega_index(n, ll, -ll)
+            l[s:s + 2 * ll + 1] = ll
+    return np.stack([complex_normal(rng, coefficient_count(B)) / (1.0 + l) for _ in range(count)])
+
+
+def test_b256_matches_oracle_both_directions():
+    """Config C4 (B = 256) against the CPU oracle in each direction separately
+    (a round trip alone would cancel an error common to both directions: a
+    permuted omega / nu index, a conjugation, an odd-m sign).  Covers the
+    paths only B = 256 takes: FFTShape<512> with doubled azimuthal CTAs and
+    4-shell G groups, the Legendre inverse's K = 128 row-table limit and the
+    radial forward's 512-row table."""
+    B = 256
+    plan, orc = plan_for(B)
+    c = _c4_coefficients(B, 2560)[0]
+    g_ref = orc.inverse(c)
+    assert np.isfinite(g_ref).all()
+    g = sgl.ifsglft(sgl.SglCoefficients(B, c), plan).values
+    assert np.isfinite(g).all()
+    assert per_shell(g, g_ref, B) <= TOL
+    f_ref = orc.forward(g_ref)
+    f = sgl.fsglft(sgl.SampleGrid(B, g_ref), plan).values
+    assert np.isfinite(f).all()
+    assert normwise(f, f_ref) <= TOL
+    assert normwise(f, c) <= TOL
+    # a non-bandlimited input (every row of every stage contributes)
+    rng = np.random.default_rng(2561)
+    x = complex_normal(rng, sample_count(B))
+    assert normwise(sgl.fsglft(sgl.SampleGrid(B, x), plan).values, orc.forward(x)) <= TOL
+
+
+def test_b256_batch_of_two_matches_oracle():
+    import torch
+
+    B = 256
+    plan, orc = plan_for(B)
+    c = _c4_coefficients(B, 2562, count=2)
+    dg = sgl.ifsglft_batch(plan, torch.from_numpy(c).cuda())
+    df = sgl.fsglft_batch(plan, dg)
+    g = dg.cpu().numpy()
+    f = df.cpu().numpy()
+    del dg, df
+    for b in range(2):
+        g_ref = orc.inverse(c[b])
+        assert np.isfinite(g[b]).all() and np.isfinite(f[b]).all()
+        assert per_shell(g[b], g_ref, B) <= TOL
+        assert normwise(f[b], orc.forward(g[b])) <= TOL
+        assert normwise(f[b], c[b]) <= TOL
+
+
 def test_roundtrip_b256():
     B = 256
     plan, orc = plan_for(B)

@@ -206,3 +206,43 @@ def test_oracle_valid_at_b128():
     g = o.inverse(c)
     assert np.isfinite(g).all()
     assert normwise(o.forward(g), c) < 1e-12
+
+
+def _lm_of_omega(B):
+    """(l, |m|) of every omega-order entry (indexing.cpp:50-78)."""
+    ls, ms = [], []
+    for n in range(1, B + 1):
+        for l in range(n):
+            ls += [l] * (2 * l + 1)
+            ms += list(range(-l, l + 1))
+    return np.array(ls), np.abs(np.array(ms))
+
+
+@pytest.mark.skipif(not Reference.available(), reason="oracle/_ref not built (needs /root/reference)")
+def test_oracle_pinned_to_reference_b128_representable_subset():
+    """Pins the oracle to the reference itself at B = 128 where the reference is
+    valid: M_lm (special_functions.cpp:81-88) stays representable for
+    l + |m| <~ 172, so on entries with l + |m| <= 160 the reference's fsglft /
+    ifsglft (sgl_transform.cpp:274-348) are exact and must agree with the
+    restatement.  Forward: every output coefficient depends only on its own
+    (l, m) row, so the valid rows are compared on a full random grid.  Inverse:
+    inputs supported on the valid rows only (the reference's underflowed rows are
+    zero, not NaN, at B = 128)."""
+    B = 128
+    ref, o = Reference(B), orc(B)
+    assert np.array_equal(ref.b_cal, o.b_cal)
+    l, am = _lm_of_omega(B)
+    ok = l + am <= 160
+    assert ok.sum() > 0.85 * ok.size  # 633,568 of 707,264
+    rng = np.random.default_rng(128)
+    n = coefficient_count(B)
+    c = (rng.standard_normal(n) + 1j * rng.standard_normal(n)) / np.sqrt(2)
+    g = o.inverse(c)
+    f_ref = ref.forward(g)
+    f_orc = o.forward(g)
+    assert np.isfinite(f_ref[ok]).all()
+    assert normwise(f_orc[ok], f_ref[ok]) <= 1e-12
+    c_ok = np.where(ok, c, 0)
+    g_ref = ref.inverse(c_ok)
+    assert np.isfinite(g_ref).all()
+    assert per_shell(o.inverse(c_ok), g_ref, B) <= 1e-12
