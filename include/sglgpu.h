@@ -8,7 +8,7 @@
  *       (include/sgl/sgl_transform.hpp:71-76, bodies src/sgl_transform.cpp:274-348)
  *
  * The reference has no FFI; its interface is that C++ API.  The C++ mirror of it
- * lives in include/sgl_b200/sgl_transform.hpp and is implemented on top of the
+ * lives in include/sgl/sgl_transform.hpp (the reference's own header path) and is implemented on top of the
  * entry points below, which is also what a ctypes / cgo / JNI binding would bind
  * (see INTEGRATION.md).  Plain pointers and sizes only.
  *
@@ -105,6 +105,18 @@ int sglgpu_forward_separated(sglgpu_plan* plan, const double* samples, double* c
                              int mem_kind, void* stream);
 int sglgpu_inverse_separated(sglgpu_plan* plan, const double* coeffs, double* samples, size_t batch,
                              int mem_kind, void* stream);
+
+/* The reference's naive O(B^7) transforms dsglft_naive / idsglft_naive
+ * (sgl_transform.cpp:122-187) on the device: every basis value evaluated afresh
+ * at every node from normalized closed forms, direct sums.  The last rung of the
+ * reference's oracle chain; B <= 32, else SGLGPU_EINVAL. */
+int sglgpu_forward_naive(sglgpu_plan* plan, const double* samples, double* coeffs, size_t batch,
+                         int mem_kind, void* stream);
+int sglgpu_inverse_naive(sglgpu_plan* plan, const double* coeffs, double* samples, size_t batch,
+                         int mem_kind, void* stream);
+/* sample_sgl_basis (sgl_transform.cpp:368-389): H_nlm on the plan's grid,
+ * psi-order, 8B^3 complex; SGLGPU_EINVAL unless |m| <= l < n <= B. */
+int sglgpu_sample_basis(sglgpu_plan* plan, int n, int l, int m, double* samples, int mem_kind, void* stream);
 
 /* Stage entry points (device memory only, asynchronous on `stream`), used by the
  * multi-GPU shell / (l, m) decomposition.  `shells` is the nu-major intermediate

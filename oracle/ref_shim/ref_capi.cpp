@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "sgl/indexing.hpp"
+#include "sgl/precompute_store.hpp"
 #include "sgl/radial_transform.hpp"
 #include "sgl/sgl_transform.hpp"
 #include "sgl/spherical_transform.hpp"
@@ -54,6 +55,20 @@ void* ref_plan_create(int B) {
 }
 
 void ref_plan_destroy(void* p) { delete static_cast<TransformPlan*>(p); }
+
+// The reference's own SGLT writers for the plan-table kinds 1-3
+// (precompute_store.cpp:160-194): the radial rule the plan was built with, the
+// closed-form spherical rule and LegendreDctTable::build(B).
+int ref_save_tables(void* p, const char* dir) {
+    return guard([&] {
+        const auto* plan = static_cast<TransformPlan*>(p);
+        const int B = plan->bandlimit;
+        const std::filesystem::path d(dir);
+        store::save_radial_rule(plan->radial, d / store::radial_rule_filename(B));
+        store::save_spherical_rule(sphere_rule(B), d / store::spherical_rule_filename(B));
+        store::save_legendre_table(LegendreDctTable::build(B), d / store::legendre_table_filename(B));
+    });
+}
 
 int ref_plan_arrays(void* p, double* r, double* a, double* a_mod, double* theta, double* phi,
                     double* b_cal, double* exp_neg_r2, double* m_norm) {

@@ -55,7 +55,8 @@ def lib():
         L.sglgpu_plan_table_bytes.restype = ctypes.c_size_t
         L.sglgpu_last_launch_count.argtypes = [_vp]
         for name in ("sglgpu_forward", "sglgpu_inverse", "sglgpu_forward_real", "sglgpu_inverse_real",
-                     "sglgpu_forward_separated", "sglgpu_inverse_separated"):
+                     "sglgpu_forward_separated", "sglgpu_inverse_separated", "sglgpu_forward_naive",
+                     "sglgpu_inverse_naive"):
             getattr(L, name).argtypes = [_vp, _vp, _vp, ctypes.c_size_t, ctypes.c_int, _vp]
         for name in ("sglgpu_spherical_forward", "sglgpu_spherical_inverse"):
             getattr(L, name).argtypes = [_vp, _vp, ctypes.c_size_t, _vp, ctypes.c_int, ctypes.c_int,
@@ -73,6 +74,7 @@ def lib():
         L.sglgpu_ipc_export.argtypes = [_vp, _vp]
         L.sglgpu_ipc_open.argtypes = [_vp, ctypes.POINTER(_vp)]
         L.sglgpu_ipc_close.argtypes = [_vp]
+        L.sglgpu_sample_basis.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp]
         L.sglgpu_profile_begin.argtypes = [_vp]
         L.sglgpu_profile_end.argtypes = [_vp, _vp, _vp]
         _lib = L
@@ -102,14 +104,22 @@ def coefficient_count(B: int) -> int:
 
 
 def psi_index(i: int, j: int, k: int, B: int) -> int:
+    """indexing.cpp:50-78 (IndexError stands in for std::out_of_range)."""
+    sample_count(B)
+    if not (0 <= i < 2 * B and 0 <= j < 2 * B and 0 <= k < 2 * B):
+        raise IndexError("psi_index: node indices out of range")
     return 4 * B * B * i + 2 * B * j + k
 
 
 def nu_index(l: int, m: int) -> int:
+    if l < 0 or abs(m) > l:
+        raise IndexError("nu_index: require |m| <= l")
     return l * (l + 1) + m
 
 
 def omega_index(n: int, l: int, m: int) -> int:
+    if n < 1 or l < 0 or l >= n or abs(m) > l:
+        raise IndexError("omega_index: require |m| <= l < n")
     return (n - 1) * n * (2 * n - 1) // 6 + l * (l + 1) + m
 
 
@@ -315,35 +325,69 @@ def idsglft_separated(coeffs: SglCoefficients, plan: TransformPlan, threads: int
     return SampleGrid(plan.bandlimit, out)
 
 
+def dsglft_naive(grid: SampleGrid, plan: TransformPlan, threads: int = 1) -> SglCoefficients:
+    """Naive O(B^7) forward transform (sgl_transform.cpp:122-153) on the device. B <= 32."""
+    _check_plan_grid(grid, plan)
+    g = np.ascontiguousarray(grid.values, dtype=np.complex128)
+    out = np.zeros(coefficient_count(plan.bandlimit), dtype=np.complex128)
+    _check(lib().sglgpu_forward_naive(plan.handle, g.ctypes.data, out.ctypes.data, 1, MEM_HOST, None))
+    return SglCoefficients(plan.bandlimit, out)
+
+
+def idsglft_naive(coeffs: SglCoefficients, plan: TransformPlan, threads: int = 1) -> SampleGrid:
+    """Naive O(B^7) inverse transform (sgl_transform.cpp:155-187) on the device. B <= 32."""
+    _check_plan_coeffs(coeffs, plan)
+    c = np.ascontiguousarray(coeffs.values, dtype=np.complex128)
+    out = np.zeros(sample_count(plan.bandlimit), dtype=np.complex128)
+    _check(lib().sglgpu_inverse_naive(plan.handle, c.ctypes.data, out.ctypes.data, 1, MEM_HOST, None))
+    return SampleGrid(plan.bandlimit, out)
+
+
+def sample_sgl_basis(n: int, l: int, m: int, plan: TransformPlan) -> SampleGrid:
+    """H_nlm sampled on the plan's grid, psi-order (sgl_transform.cpp:368-389), on the device."""
+    B = plan.bandlimit
+    if n < 1 or n > B or l < 0 or l >= n or abs(m) > l:
+        raise ValueError("sample_sgl_basis: invalid (n, l, m) for this plan")
+    out = np.zeros(sample_count(B), dtype=np.complex128)
+    _check(lib().sglgpu_sample_basis(plan.handle, n, l, m, out.ctypes.data, MEM_HOST, None))
+    return SampleGrid(B, out)
+
+
 def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
-def _batch_call(fn, plan: TransformPlan, src, n_in: int, n_out: int, out=None, stream=None):
-    if _is_torch(src):
-        import torch
+def _plan_device(plan: TransformPlan) -> int:
+    if plan.device >= 0:
+        return plan.device
+    import torch
 
-        if src.dtype != torch.complex128 or not src.is_contiguous():
-            raise ValueError("batched transforms take contiguous complex128 tensors")
-        if src.numel() % n_in:
-            raise ValueError("input length is not a whole number of functions")
-        batch = src.numel() // n_in
-        if out is None:
-            out = torch.empty((batch, n_out), dtype=torch.complex128, device=src.device)
-        if src.is_cuda:
-            st = stream if stream is not None else torch.cuda.current_stream(src.device).cuda_stream
-            _check(fn(plan.handle, src.data_ptr(), out.data_ptr(), batch, MEM_DEVICE, st))
-        else:
-            _check(fn(plan.handle, src.data_ptr(), out.data_ptr(), batch, MEM_HOST, None))
-        return out
-    a = np.ascontiguousarray(src, dtype=np.complex128)
-    if a.size % n_in:
-        raise ValueError("input length is not a whole number of functions")
-    batch = a.size // n_in
-    if out is None:
-        out = np.empty((batch, n_out), dtype=np.complex128)
-    _check(fn(plan.handle, a.ctypes.data, out.ctypes.data, batch, MEM_HOST, None))
-    return out
+    return torch.cuda.current_device()
+
+
+def _check_torch_out(plan, src, out, batch, n_out, dtype):
+    """A caller-supplied `out` must match what the C ABI will write: shape, dtype,
+    contiguity and memory kind / device of `src` (a host pointer handed to the
+    kernels, or a short buffer, would be memory corruption, not an exception)."""
+    if not _is_torch(out):
+        raise ValueError("out must be a torch tensor when the input is one")
+    if out.dtype != dtype or not out.is_contiguous() or out.numel() != batch * n_out:
+        raise ValueError(f"out must be a contiguous {dtype} tensor of {batch} x {n_out} elements")
+    if out.device != src.device:
+        raise ValueError(f"out is on {out.device}, the input on {src.device}")
+    if src.is_cuda and src.device.index != _plan_device(plan):
+        raise ValueError(f"input is on {src.device}, the plan on cuda:{_plan_device(plan)}")
+
+
+def _check_numpy_out(out, batch, n_out, dtype):
+    if not isinstance(out, np.ndarray) or out.dtype != dtype or not out.flags.c_contiguous \
+            or out.size != batch * n_out or not out.flags.writeable:
+        raise ValueError(f"out must be a writeable C-contiguous {np.dtype(dtype).name} array of "
+                         f"{batch} x {n_out} elements")
+
+
+def _batch_call(fn, plan: TransformPlan, src, n_in: int, n_out: int, out=None, stream=None):
+    return _batch_call_real(fn, plan, src, n_in, n_out, np.complex128, np.complex128, out, stream)
 
 
 def fsglft_batch(plan: TransformPlan, samples, out=None, stream=None):
@@ -370,6 +414,8 @@ def _batch_call_real(fn, plan, src, n_in, n_out, in_dtype, out_dtype, out=None, 
         batch = src.numel() // n_in
         if out is None:
             out = torch.empty((batch, n_out), dtype=td[out_dtype], device=src.device)
+        else:
+            _check_torch_out(plan, src, out, batch, n_out, td[out_dtype])
         if src.is_cuda:
             st = stream if stream is not None else torch.cuda.current_stream(src.device).cuda_stream
             _check(fn(plan.handle, src.data_ptr(), out.data_ptr(), batch, MEM_DEVICE, st))
@@ -382,6 +428,8 @@ def _batch_call_real(fn, plan, src, n_in, n_out, in_dtype, out_dtype, out=None, 
     batch = a.size // n_in
     if out is None:
         out = np.empty((batch, n_out), dtype=out_dtype)
+    else:
+        _check_numpy_out(out, batch, n_out, out_dtype)
     _check(fn(plan.handle, a.ctypes.data, out.ctypes.data, batch, MEM_HOST, None))
     return out
 
@@ -431,7 +479,7 @@ def roundtrip_error(reference, actual) -> RoundtripError:
 
 __all__ = [
     "SphericalRule", "RadialRule", "TransformPlan", "SglCoefficients", "SampleGrid", "fsglft", "ifsglft",
-    "dsglft_separated", "idsglft_separated", "fsglft_batch", "ifsglft_batch", "fsglft_real_batch",
+    "dsglft_separated", "idsglft_separated", "dsglft_naive", "idsglft_naive", "sample_sgl_basis", "fsglft_batch", "ifsglft_batch", "fsglft_real_batch",
     "ifsglft_real_batch", "roundtrip_error", "sphere_rule", "load_radial_rule", "sample_count",
     "coefficient_count", "psi_index", "nu_index", "omega_index", "lib",
 ]

@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUDA_SOURCES = ["sgl_kernels.cu", "sgl_separated.cu"]
-CXX_SOURCES = ["sgl_tables.cpp", "sgl_capi.cpp", "sgl_api.cpp"]
+CXX_SOURCES = ["sgl_tables.cpp", "sgl_capi.cpp", "sgl_api.cpp", "sgl_host.cpp"]
 
 
 def _sources():

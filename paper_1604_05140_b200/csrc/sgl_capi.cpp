@@ -610,8 +610,9 @@ int run_real(sglgpu_plan* p, const double* in, double* out, size_t batch, int me
 
 // dsglft_separated / idsglft_separated (sgl_transform.cpp:189-272) on the device:
 // the cross-oracle rung of SURVEY.md 8(f).  Synchronous w.r.t. host memory.
+// naive = true: the O(B^7) naive rung (sgl_transform.cpp:122-187), B <= 32.
 int run_separated(sglgpu_plan* p, const double* in, double* out, size_t batch, int mem_kind, void* stream,
-                  bool forward) {
+                  bool forward, bool naive = false) {
     return guarded([&] {
         check_plan(p);
         if (mem_kind != SGLGPU_MEM_HOST && mem_kind != SGLGPU_MEM_DEVICE)
@@ -619,7 +620,9 @@ int run_separated(sglgpu_plan* p, const double* in, double* out, size_t batch, i
         if (batch == 0) return;
         if (!in || !out) fail(SGLGPU_EINVAL, "sglgpu: null data pointer");
         const int B = p->B;
-        if (B > 64) fail(SGLGPU_EINVAL, "sglgpu separated transform: bandlimit must be <= 64 (reference validity)");
+        if (!naive && B > 64)
+            fail(SGLGPU_EINVAL, "sglgpu separated transform: bandlimit must be <= 64 (reference validity)");
+        if (naive && B > 32) fail(SGLGPU_EINVAL, "sglgpu naive transform: bandlimit must be <= 32 (O(B^7))");
         std::lock_guard<std::mutex> lock(p->mu);
         set_device(p);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -639,10 +642,13 @@ int run_separated(sglgpu_plan* p, const double* in, double* out, size_t batch, i
                 src = p->in.p;
             }
             double* d_dst = mem_kind == SGLGPU_MEM_HOST ? p->out.p : dst;
-            const int k = forward ? sglk::launch_separated_forward(B, nb, src, d_dst, p->S.p, p->d_r, p->d_amod,
+            const int k = naive ? (forward ? sglk::launch_naive_forward(B, nb, src, d_dst, p->d_r, p->d_amod,
+                                                                        p->d_bcal, st)
+                                           : sglk::launch_naive_inverse(B, nb, src, d_dst, p->d_r, st))
+                        : forward ? sglk::launch_separated_forward(B, nb, src, d_dst, p->S.p, p->d_r, p->d_amod,
                                                                    p->d_bcal, st)
                                   : sglk::launch_separated_inverse(B, nb, src, d_dst, p->S.p, p->d_r, st);
-            ck_launch(k, forward ? "separated_forward" : "separated_inverse");
+            ck_launch(k, naive ? "naive transform" : forward ? "separated_forward" : "separated_inverse");
             launches += k;
             if (mem_kind == SGLGPU_MEM_HOST)
                 ck(cudaMemcpyAsync(dst, p->out.p, nb * out_len * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
@@ -872,6 +878,44 @@ int sglgpu_forward_separated(sglgpu_plan* plan, const double* samples, double* c
 int sglgpu_inverse_separated(sglgpu_plan* plan, const double* coeffs, double* samples, size_t batch, int mem_kind,
                              void* stream) {
     return run_separated(plan, coeffs, samples, batch, mem_kind, stream, false);
+}
+
+int sglgpu_forward_naive(sglgpu_plan* plan, const double* samples, double* coeffs, size_t batch, int mem_kind,
+                         void* stream) {
+    return run_separated(plan, samples, coeffs, batch, mem_kind, stream, true, true);
+}
+
+int sglgpu_inverse_naive(sglgpu_plan* plan, const double* coeffs, double* samples, size_t batch, int mem_kind,
+                         void* stream) {
+    return run_separated(plan, coeffs, samples, batch, mem_kind, stream, false, true);
+}
+
+int sglgpu_sample_basis(sglgpu_plan* p, int n, int l, int m, double* samples, int mem_kind, void* stream) {
+    return guarded([&] {
+        check_plan(p);
+        const int B = p->B;
+        if (n < 1 || n > B || l < 0 || l >= n || m < -l || m > l)
+            fail(SGLGPU_EINVAL, "sample_sgl_basis: invalid (n, l, m) for this plan");
+        if (mem_kind != SGLGPU_MEM_HOST && mem_kind != SGLGPU_MEM_DEVICE)
+            fail(SGLGPU_EINVAL, "sglgpu: unknown mem_kind");
+        if (!samples) fail(SGLGPU_EINVAL, "sglgpu: null data pointer");
+        std::lock_guard<std::mutex> lock(p->mu);
+        set_device(p);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const size_t len = 2 * (size_t)sample_count(B);
+        double* dst = samples;
+        if (mem_kind == SGLGPU_MEM_HOST) {
+            p->out.ensure(len);
+            dst = p->out.p;
+        }
+        const int k = sglk::launch_sample_basis(B, n, l, m, dst, p->d_r, st);
+        ck_launch(k, "sample_basis");
+        if (mem_kind == SGLGPU_MEM_HOST) {
+            ck(cudaMemcpyAsync(samples, dst, len * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        }
+        p->last_launches = k;
+    });
 }
 
 int sglgpu_forward_real(sglgpu_plan* plan, const double* samples, double* coeffs, size_t batch, int mem_kind,

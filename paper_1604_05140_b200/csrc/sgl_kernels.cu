@@ -26,11 +26,33 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cstdlib>
 #include <type_traits>
 #include <utility>
 
 namespace sglk {
+
+// Opt-in to more than 48 KB of dynamic shared memory, once per kernel and
+// device: the attribute belongs to the current device's context, and plans may
+// live on several devices of one process (sglgpu_plan_desc::device) and be used
+// from several threads.
+struct SmemAttrOnce {
+    std::atomic<unsigned long long> done{0};  // bit d: set on device d
+    std::mutex mu;
+    template <class Kernel>
+    void ensure(Kernel k, size_t smem) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+        const unsigned long long bit = 1ULL << dev;
+        if (done.load(std::memory_order_acquire) & bit) return;
+        std::lock_guard<std::mutex> lock(mu);
+        if (done.load(std::memory_order_relaxed) & bit) return;
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess)
+            done.fetch_or(bit, std::memory_order_release);
+    }
+};
 
 // ------------------------------------------------------------------ complex helpers
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -565,11 +587,8 @@ static int az_fwd_real_launch(const Geo& g, const double* X, size_t fstride, dou
     using S = FFTShape<N>;
     constexpr int IGR = 2 * S::IG;
     const size_t smem = sizeof(double2) * (IGR * S::STRIDE);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(az_forward_real_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    static SmemAttrOnce attr;
+    attr.ensure(az_forward_real_kernel<N>, smem);
     const int nshell = g.batch * g.SC;
     dim3 grid((nshell + IGR - 1) / IGR, g.B);
     az_forward_real_kernel<N><<<grid, S::THREADS, smem, s>>>(g, X, fstride, reinterpret_cast<double2*>(G), bcal,
@@ -583,11 +602,8 @@ static int az_inv_real_launch(const Geo& g, const double* G, double* X, size_t f
     using S = FFTShape<N>;
     constexpr int IGR = 2 * S::IG;
     const size_t smem = sizeof(double2) * (IGR * S::STRIDE);  // E/O rows live in the ring buffers
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(az_inverse_real_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    static SmemAttrOnce attr;
+    attr.ensure(az_inverse_real_kernel<N>, smem);
     const int nshell = g.batch * g.SC;
     dim3 grid((nshell + IGR - 1) / IGR, g.B);
     az_inverse_real_kernel<N><<<grid, S::THREADS, smem, s>>>(g, reinterpret_cast<const double2*>(G), X, fstride,
@@ -1573,11 +1589,8 @@ static int az_fwd_launch(const Geo& g, const double* X, size_t fstride, double* 
                          const double* tw, cudaStream_t s) {
     using S = FFTShape<N>;
     const size_t smem = sizeof(double2) * (2 * S::IG * S::STRIDE);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(az_forward_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    static SmemAttrOnce attr;
+    attr.ensure(az_forward_kernel<N>, smem);
     const int nshell = g.batch * g.SC;
     dim3 grid((nshell + S::IG - 1) / S::IG, g.B);
     az_forward_kernel<N><<<grid, S::THREADS, smem, s>>>(g, reinterpret_cast<const double2*>(X), fstride / 2,
@@ -1592,11 +1605,8 @@ static int az_inv_launch(const Geo& g, const double* G, double* X, size_t fstrid
     using S = FFTShape<N, SGL_AZI_ELEMS>;
     static_assert(S::IG == FFTShape<N>::IG, "forward and inverse azimuthal tiles must match the G blocking");
     const size_t smem = sizeof(double2) * (2 * S::IG * S::STRIDE);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(az_inverse_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    static SmemAttrOnce attr;
+    attr.ensure(az_inverse_kernel<N>, smem);
     const int nshell = g.batch * g.SC;
     dim3 grid((nshell + S::IG - 1) / S::IG, g.B);
     az_inverse_kernel<N><<<grid, S::THREADS, smem, s>>>(g, reinterpret_cast<const double2*>(G),
@@ -1654,11 +1664,8 @@ template <class P>
 static int gemm_launch(const P& p, const TileMap* tiles, int ntiles, cudaStream_t s) {
     if (ntiles <= 0) return 0;
     constexpr size_t smem = gemm_smem_bytes<P>();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(gemm_dmma_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    static SmemAttrOnce attr;
+    attr.ensure(gemm_dmma_kernel<P>, smem);
     gemm_dmma_kernel<P><<<ntiles, 128, smem, s>>>(p, *tiles);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }

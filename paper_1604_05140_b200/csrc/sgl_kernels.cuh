@@ -167,4 +167,11 @@ int launch_separated_forward(int B, int batch, const double* samples, double* co
 int launch_separated_inverse(int B, int batch, const double* coeffs, double* samples, double* shells,
                              const double* r, cudaStream_t s);
 
+// The reference's naive O(B^7) rung (sgl_transform.cpp:122-187) and
+// sample_sgl_basis (:368-389) with normalized closed-form basis values.
+int launch_naive_forward(int B, int batch, const double* samples, double* coeffs, const double* r,
+                         const double* a_mod, const double* bcal, cudaStream_t s);
+int launch_naive_inverse(int B, int batch, const double* coeffs, double* samples, const double* r, cudaStream_t s);
+int launch_sample_basis(int B, int n, int l, int m, double* samples, const double* r, cudaStream_t s);
+
 }  // namespace sglk

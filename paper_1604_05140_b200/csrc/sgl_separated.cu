@@ -206,7 +206,162 @@ __global__ void sep_sphere_inverse(int B, int batch, const double2* __restrict__
 
 int grid_of(long long n, int threads) { return (int)((n + threads - 1) / threads); }
 
+// ------------------------------------------------------------------ naive rung and basis sampling
+// The reference's O(B^7) naive transforms (sgl_transform.cpp:122-187) and
+// sample_sgl_basis (:368-389): every basis value H_nlm(r_i, theta_j, phi_k)
+// evaluated afresh at every node.  Unlike the separated kernels above these use
+// normalized recurrences, so the basis stays finite at every bandlimit:
+//   Pbar_lm(t) = M_lm P_lm(t): Pbar_mm in log space, Pbar_{m+1,m} = sqrt(2m+3) t Pbar_mm,
+//     Pbar_l = a_l (t Pbar_{l-1} - Pbar_{l-2} / a_{l-1}),  a_l = sqrt((4l^2-1)/(l^2-m^2));
+//   N_nl R_nl(r) = sqrt(2) q_k(r^2) r^l, k = n-l-1, alpha = l+1/2, with the
+//     normalized Laguerre q_k = sqrt(k!/Gamma(k+alpha+1)) L_k^alpha:
+//     q_{k+1} = ((2k+alpha+1-t) q_k - sqrt(k(k+alpha)) q_{k-1}) / sqrt((k+1)(k+alpha+1)),
+//     seeded in log space (the e^{-r^2} of the forward folded into the seed).
+__device__ double pbar_lm(int l, int am, double t) {
+    const double s2 = (1.0 - t) * (1.0 + t);
+    double lg = 0.5 * log((2 * am + 1) / (4.0 * 3.14159265358979323846));
+    for (int k = 1; k <= am; ++k) lg += 0.5 * log((2.0 * k - 1.0) / (2.0 * k));
+    double pmm;
+    if (am == 0) pmm = exp(lg);
+    else pmm = s2 > 0.0 ? ((am & 1) ? -1.0 : 1.0) * exp(lg + 0.5 * am * log(s2)) : 0.0;
+    if (l == am) return pmm;
+    double p0 = pmm, p1 = sqrt(2.0 * am + 3.0) * t * pmm;
+    for (int ll = am + 2; ll <= l; ++ll) {
+        const double a = sqrt((4.0 * ll * ll - 1.0) / ((double)ll * ll - (double)am * am));
+        const double b = sqrt(((double)(ll - 1) * (ll - 1) - (double)am * am) / (4.0 * (ll - 1) * (ll - 1) - 1.0));
+        const double p = a * (t * p1 - b * p0);
+        p0 = p1;
+        p1 = p;
+    }
+    return p1;
+}
+
+// N_nl R_nl(r) (decayed: times e^{-r^2})
+__device__ double radial_norm(int n, int l, double r, bool decayed) {
+    const double alpha = l + 0.5, t = r * r;
+    double lg = 0.5 * 0.69314718055994530942 - 0.5 * lgamma(alpha + 1.0);
+    if (l > 0) lg += l * log(r);
+    if (decayed) lg -= t;
+    double q0 = 0.0, q1 = exp(lg);
+    for (int k = 0; k < n - l - 1; ++k) {
+        const double q = ((2 * k + alpha + 1.0 - t) * q1 - sqrt(k * (k + alpha)) * q0) / sqrt((k + 1) * (k + alpha + 1.0));
+        q0 = q1;
+        q1 = q;
+    }
+    return q1;
+}
+
+__device__ void omega_to_nlm(long long w, int& n, int& l, int& m) {
+    n = 1;
+    while ((long long)n * (n + 1) * (2 * n + 1) / 6 <= w) ++n;
+    nu_to_lm((int)(w - (long long)(n - 1) * n * (2 * n - 1) / 6), l, m);
+}
+
+__device__ __forceinline__ double cos_theta(int j, int N) { return cospi((2 * j + 1) / (2.0 * N)); }
+
+// out[f][omega] = sum_psi a_mod_i b_j e^{-r_i^2} conj(H_nlm(psi)) X[f][psi]; one CTA per (f, omega)
+__global__ void naive_forward(int B, const double2* __restrict__ X, double2* __restrict__ C,
+                              const double* __restrict__ r, const double* __restrict__ a_mod,
+                              const double* __restrict__ bcal) {
+    const int N = 2 * B;
+    const long long om = (long long)B * (B + 1) * (2 * B + 1) / 6;
+    const long long w = blockIdx.x;
+    const int f = blockIdx.y;
+    int n, l, m;
+    omega_to_nlm(w, n, l, m);
+    const int am = m < 0 ? -m : m;
+    const double sg = (m < 0 && (am & 1)) ? -1.0 : 1.0;  // M_{l,-a} P_{l,-a} = (-1)^a M_la P_la (sgl_transform.cpp:80-85)
+    const double2* x = X + (long long)f * N * N * N;
+    double ar = 0.0, ai = 0.0;
+    for (long long q = threadIdx.x; q < (long long)N * N * N; q += blockDim.x) {
+        const int k = (int)(q % N), j = (int)((q / N) % N), i = (int)(q / ((long long)N * N));
+        const double basis = radial_norm(n, l, r[i], true) * sg * pbar_lm(l, am, cos_theta(j, N)) * a_mod[i] * bcal[j];
+        double sn, cs;
+        sincospi((double)(m * k) / B, &sn, &cs);  // conj(e^{i m phi_k}), phi_k = k pi / B
+        const double2 v = x[q];
+        ar += basis * (v.x * cs + v.y * sn);
+        ai += basis * (v.y * cs - v.x * sn);
+    }
+    __shared__ double red[2][256];
+    red[0][threadIdx.x] = ar;
+    red[1][threadIdx.x] = ai;
+    __syncthreads();
+    for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+        if ((int)threadIdx.x < h) {
+            red[0][threadIdx.x] += red[0][threadIdx.x + h];
+            red[1][threadIdx.x] += red[1][threadIdx.x + h];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) C[(long long)f * om + w] = make_double2(red[0][0], red[1][0]);
+}
+
+// X[f][psi] = sum_omega c[f][omega] H_nlm(psi); one thread per (f, psi)
+__global__ void naive_inverse(int B, int batch, const double2* __restrict__ C, double2* __restrict__ X,
+                              const double* __restrict__ r) {
+    const int N = 2 * B;
+    const long long om = (long long)B * (B + 1) * (2 * B + 1) / 6, ns = (long long)N * N * N;
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx >= batch * ns) return;
+    const int f = (int)(idx / ns);
+    const long long q = idx - f * ns;
+    const int k = (int)(q % N), j = (int)((q / N) % N), i = (int)(q / ((long long)N * N));
+    const double2* c = C + (long long)f * om;
+    const double t = cos_theta(j, N);
+    double ar = 0.0, ai = 0.0;
+    for (int n = 1; n <= B; ++n)
+        for (int l = 0; l < n; ++l) {
+            const double rad = radial_norm(n, l, r[i], false);
+            for (int m = -l; m <= l; ++m) {
+                const int am = m < 0 ? -m : m;
+                const double sg = (m < 0 && (am & 1)) ? -1.0 : 1.0;
+                const double basis = rad * sg * pbar_lm(l, am, t);
+                double sn, cs;
+                sincospi((double)(m * k) / B, &sn, &cs);
+                const double2 v = c[(long long)(n - 1) * n * (2 * n - 1) / 6 + l * (l + 1) + m];
+                ar += basis * (v.x * cs - v.y * sn);
+                ai += basis * (v.x * sn + v.y * cs);
+            }
+        }
+    X[idx] = make_double2(ar, ai);
+}
+
+// X[psi] = H_nlm(r_i, theta_j, phi_k)
+__global__ void basis_samples(int B, int n, int l, int m, double2* __restrict__ X, const double* __restrict__ r) {
+    const int N = 2 * B;
+    const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (q >= (long long)N * N * N) return;
+    const int k = (int)(q % N), j = (int)((q / N) % N), i = (int)(q / ((long long)N * N));
+    const int am = m < 0 ? -m : m;
+    const double sg = (m < 0 && (am & 1)) ? -1.0 : 1.0;
+    const double base = radial_norm(n, l, r[i], false) * sg * pbar_lm(l, am, cos_theta(j, N));
+    double sn, cs;
+    sincospi((double)(m * k) / B, &sn, &cs);
+    X[q] = make_double2(base * cs, base * sn);
+}
+
 }  // namespace
+
+int launch_naive_forward(int B, int batch, const double* samples, double* coeffs, const double* r,
+                         const double* a_mod, const double* bcal, cudaStream_t s) {
+    const long long om = (long long)B * (B + 1) * (2 * B + 1) / 6;
+    naive_forward<<<dim3((unsigned)om, batch), 256, 0, s>>>(B, reinterpret_cast<const double2*>(samples),
+                                                              reinterpret_cast<double2*>(coeffs), r, a_mod, bcal);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_naive_inverse(int B, int batch, const double* coeffs, double* samples, const double* r, cudaStream_t s) {
+    const long long nx = (long long)batch * 8 * B * B * B;
+    naive_inverse<<<grid_of(nx, 128), 128, 0, s>>>(B, batch, reinterpret_cast<const double2*>(coeffs),
+                                                   reinterpret_cast<double2*>(samples), r);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_sample_basis(int B, int n, int l, int m, double* samples, const double* r, cudaStream_t s) {
+    basis_samples<<<grid_of(8LL * B * B * B, 128), 128, 0, s>>>(B, n, l, m, reinterpret_cast<double2*>(samples), r);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
 
 int launch_separated_forward(int B, int batch, const double* samples, double* coeffs, double* shells,
                              const double* r, const double* a_mod, const double* bcal, cudaStream_t s) {

@@ -334,6 +334,8 @@ def fsglft_distributed_fused(samples_local, part: "Partition", stages: "CudaStag
     (NVLink peer stores into the owners' receive buffers; see PeerBuffers)."""
     import torch
 
+    if batch != peers.batch:  # the receive buffers and the peer offsets are sized for peers.batch
+        raise ValueError(f"fsglft_distributed_fused: batch {batch} != the peer buffers' batch {peers.batch}")
     r = dist.get_rank(group)
     fused_forward_spherical(samples_local, part, stages, peers, r, batch)
     _stream_barrier(dist, group, samples_local.device)
@@ -352,11 +354,20 @@ def fsglft_distributed_fused(samples_local, part: "Partition", stages: "CudaStag
 
 def ifsglft_distributed_fused(coeffs, part: "Partition", stages: "CudaStages", peers: PeerBuffers, dist,
                               group=None, batch: int = 1):
-    """ifsglft_distributed with the all-to-all fused into the radial-inverse epilogue."""
+    """ifsglft_distributed with the all-to-all fused into the radial-inverse epilogue.
+
+    Ends with a stream barrier: the next call's radial-inverse peer stores go
+    into every rank's S buffer, which this call's spherical inverse on that rank
+    may still be reading (the forward path is ordered by its own trailing
+    collective)."""
+    if batch != peers.batch:
+        raise ValueError(f"ifsglft_distributed_fused: batch {batch} != the peer buffers' batch {peers.batch}")
     r = dist.get_rank(group)
     fused_inverse_radial(coeffs, part, stages, peers, r)
     _stream_barrier(dist, group, coeffs.device)
-    return fused_inverse_spherical(part, stages, peers, r, coeffs.device)
+    out = fused_inverse_spherical(part, stages, peers, r, coeffs.device)
+    _stream_barrier(dist, group, coeffs.device)
+    return out
 
 
 def _a2a(dist, group, send, send_counts, recv_counts):

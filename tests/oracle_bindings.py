@@ -198,6 +198,7 @@ class Reference:
             L.ref_drt_forward.argtypes = [_vp, ctypes.c_int, _vp, _vp]
             L.ref_drt_inverse.argtypes = [_vp, ctypes.c_int, _vp, _vp]
             L.ref_plan_arrays.argtypes = [_vp] * 9
+            L.ref_save_tables.argtypes = [_vp, ctypes.c_char_p]
             cls._lib = L
         return cls._lib
 
@@ -235,6 +236,10 @@ class Reference:
         out = np.zeros(sample_count(self.B), dtype=np.complex128)
         self._check(self.lib().ref_inverse(self._p, variant, _P(c), _P(out), threads))
         return out
+
+    def save_tables(self, directory: str):
+        """SGLT kinds 1-3 written by the reference itself (precompute_store.cpp)."""
+        self._check(self.lib().ref_save_tables(self._p, directory.encode()))
 
     def roundtrip_batch(self, coeffs: np.ndarray, pool: int):
         c = np.ascontiguousarray(coeffs, dtype=np.complex128)

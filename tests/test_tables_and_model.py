@@ -19,7 +19,9 @@ import pytest
 
 import paper_1604_05140_b200 as sgl
 from device_model import DeviceModel, host_tables
-from oracle_bindings import Oracle, coefficient_count, normwise, per_shell, sample_count
+from oracle_bindings import Oracle, Reference, coefficient_count, normwise, per_shell, sample_count
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 TABLES = os.path.join(os.path.dirname(sgl.__file__), "tables")
 ALL_B = sorted(int(f[len("radial_rule_B"):-5]) for f in os.listdir(TABLES) if f.startswith("radial_rule_B"))
@@ -153,3 +155,30 @@ def test_device_radial_tables_match_closed_form(B):
             assert np.abs(V[q] - rad).max() < 1e-12 * max(1.0, np.abs(rad).max())
             w = rad * np.exp(-o.r ** 2) * o.a_mod
             assert np.abs(W[q] - w).max() < 1e-12 * max(1.0, np.abs(w).max())
+
+
+@pytest.mark.skipif(not Reference.available(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("B", [2, 7, 16, 64])
+def test_cpp_mirror_plan_tables_against_reference_store(B, tmp_path):
+    """TransformPlan::from_tables reads the SGLT kinds 1-3 the REFERENCE writes
+    (precompute_store.cpp:160-237); the 4-argument assemble validates orders
+    (sgl_transform.cpp:52-63); LegendreDctTable::build reproduces the
+    reference's rows (spherical_transform.cpp:31-86); and the mirror's writers
+    are byte-identical to the reference's.  Host only (no device plan)."""
+    import filecmp
+    import subprocess
+
+    ref_dir, out_dir = tmp_path / "ref", tmp_path / "mirror"
+    ref_dir.mkdir()
+    Reference(B).save_tables(str(ref_dir))
+    exe = tmp_path / "test_tables_mirror"
+    lib = os.path.join(REPO, "paper_1604_05140_b200")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(REPO, "include"),
+                    os.path.join(REPO, "tests", "cpp", "test_tables_mirror.cpp"), "-L", lib, "-lsglb200",
+                    "-Wl,-rpath," + lib, "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), str(ref_dir), str(B), str(out_dir)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    err = float(out.stdout.split("max_row_err")[1].split()[0])
+    assert err < 1e-12, err  # the reference's own double recurrence: 1.7e-13 at B = 64
+    for name in (f"radial_rule_B{B}.sglt", f"sphere_rule_B{B}.sglt", f"legendre_dct_B{B}.sglt"):
+        assert filecmp.cmp(ref_dir / name, out_dir / name, shallow=False), name
