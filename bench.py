@@ -34,6 +34,16 @@ sys.path.insert(0, REPO)
 sys.path.insert(0, os.path.join(REPO, "tests"))
 
 FP64_PEAK_TFLOPS = 37.1  # measured DMMA m8n8k4 peak on this pool's B200 (profiles/fp64_peak_r01.txt)
+TRAFFIC_FILE = "r02_traffic.json"  # per-kernel DRAM bytes of the committed ncu capture (B = 128, one function)
+
+
+def KERNEL_NAMES(B):  # noqa: N802 -- ncu names of each stage's kernels
+    return {0: [f"void az_forward_kernel<{2 * B}>"],
+            1: ["void gemm_dmma_kernel<LegFwdTma>", "void gemm_dmma_kernel<LegFwd>"],
+            2: ["void gemm_dmma_kernel<RadFwd>"], 3: ["void gemm_dmma_kernel<RadInv>"],
+            4: ["void gemm_dmma_kernel<LegInvSeq>", "void gemm_dmma_kernel<LegInv>"],
+            5: [f"void az_inverse_kernel<{2 * B}>"],
+            6: [f"void sph_fwd_fused_kernel<{2 * B}>"], 7: [f"void sph_inv_fused_kernel<{2 * B}>"]}
 
 
 def load_peaks():
@@ -44,9 +54,32 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "_fallback": True}
 
 
-def config_id(B, nb):
-    """BASELINE.json config label for a (B, functions per step) workload."""
+def config_id(B, nb, real=False):
+    """BASELINE.json config label for a (B, functions per step, real-valued) workload."""
+    if real:
+        return {(32, 4096): "C5"}.get((B, nb), "custom")
     return {(16, 1): "C1", (64, 64): "C2", (128, 1): "C3", (256, 1): "C4"}.get((B, nb), "custom")
+
+
+def workload_config(B, nb, real):
+    """The `config` dict -- identical in both arms (ours and --impl reference), so the
+    driver can match the lines; run details go to the line's `setup` key."""
+    kind = "real-valued" if real else "complex"
+    return {"workload": f"{config_id(B, nb, real)}: B={B}, {nb} {kind} function(s) per step, ifsglft then fsglft",
+            "B": B, "batch": nb, "real": bool(real)}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def env_rank():
@@ -75,6 +108,30 @@ def real_valued_coeffs(rng, B, shape):
     neg = np.nonzero(m_of < 0)[0]
     mirror = neg - 2 * m_of[neg]  # omega(n, l, -m) = omega(n, l, m) - 2m
     c[..., neg] = ((-1.0) ** m_of[neg]) * np.conj(c[..., mirror])
+    return c
+
+
+def nl_of_omega(B):
+    n_of, l_of = [], []
+    for n in range(1, B + 1):
+        for l in range(n):
+            n_of += [n] * (2 * l + 1)
+            l_of += [l] * (2 * l + 1)
+    return np.array(n_of), np.array(l_of)
+
+
+def config_coefficients(rng, B, shape, real=False):
+    """Coefficients with BASELINE.json's value distribution for the config:
+    C2 (B = 64): complex normal x exp(-n/16); C4 (B = 256): complex normal x
+    (1 + l)^-1; C5 (real): see real_valued_coeffs; otherwise iid complex normal."""
+    if real:
+        return real_valued_coeffs(rng, B, shape)
+    n_of, l_of = nl_of_omega(B)
+    c = complex_normal(rng, shape + (len(n_of),))
+    if B == 64:
+        c *= np.exp(-n_of / 16.0)
+    elif B == 256:
+        c /= 1.0 + l_of
     return c
 
 
@@ -136,79 +193,115 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference arm
-def reference_arm(args, rank, world):
-    if rank != 0:
-        return
-    from oracle_bindings import Oracle, Reference, coefficient_count
+def _input_coefficients(B, nb, real, seed=0):
+    return config_coefficients(np.random.default_rng(seed), B, (nb,), real)
 
-    B = args.B
+
+def cpu_reference(B, nb, real, budget_s, max_steps=None):
+    """The reference's own CPU implementation of the timed round trip
+    (ifsglft then fsglft, tools/commands.cpp:152-177) on this host, as BASELINE.md
+    section 3 prescribes: oracle/_ref (the reference compiled from its sources)
+    with threads=0 for single functions, an outer pool of nproc threads with
+    threads=1 per function for batches (ref_roundtrip_batch); the oracle port
+    (C restatement) only if the reference was not built.  At B >= 128 the
+    reference's output is invalid (M_lm underflow), so the robust port is timed
+    beside it.  Bounded to ~budget_s of CPU time: a step is one round trip of
+    one function (single) or of a sample of the batch (pool)."""
+    from oracle_bindings import Oracle, Reference
+
     cores = os.cpu_count() or 1
-    rng = np.random.default_rng(0)
-    c = complex_normal(rng, coefficient_count(B))
     kind = "reference"
     try:
         impl = Reference(B)
-        note = "reference fsglft/ifsglft (oracle/_ref, built from /root/reference) threads=0"
-        if B >= 128:
-            note += "; NOTE: reference output is numerically invalid at B>=128 (M_lm underflow), timing only"
-    except Exception as e:  # reference not built here
-        impl = Oracle(B)
-        kind = "port"
-        note = f"oracle port (C restatement, OpenMP) -- reference unavailable: {e}"
-    # one untimed warm-up round trip (plan caches, page faults); the reference's
-    # CPU round trip at B=128 takes ~1 s, so the timed steps are capped at ~120 s
-    t0 = time.perf_counter()
-    impl.forward(impl.inverse(c, threads=0), threads=0)
-    est = time.perf_counter() - t0
-    run = max(1, min(args.steps, int(120.0 / max(est, 1e-6))))
+    except Exception as e:  # noqa: BLE001 -- reference not built on this host
+        impl, kind = Oracle(B), "port"
+        why = f"{e}"
+    out = {"unit": "transforms/s", "cores": cores, "kind": kind, "cpu_model": cpu_model()}
+
+    def one(obj, c, threads=0):
+        obj.forward(obj.inverse(c, threads=threads), threads=threads)
+
+    if nb == 1:
+        # threads=0 (all cores) as BASELINE.md prescribes -- unless one thread is
+        # faster (small B: the reference spawns threads per call, parallel.cpp:14-41)
+        c = _input_coefficients(B, 1, real)[0]
+        est = {}
+        for th in ((0, 1) if B <= 32 else (0,)):
+            one(impl, c, th)  # warm (plan caches, page faults)
+            t0 = time.perf_counter()
+            one(impl, c, th)
+            est[th] = time.perf_counter() - t0
+        th = min(est, key=est.get)
+        steps = max(1, int(budget_s / max(est[th], 1e-6)))
+        if max_steps:
+            steps = min(steps, max_steps)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            one(impl, c, th)
+        dt = time.perf_counter() - t0
+        out["value"] = steps / dt
+        out["cores"] = cores if th == 0 else 1
+        out["sample"] = (f"{steps} round trips of one B={B} function, fsglft/ifsglft threads={th} "
+                         f"({'reference oracle/_ref' if kind == 'reference' else 'oracle port: ' + why})")
+    else:
+        # outer pool: sample enough functions for ~budget_s
+        pool = cores
+        c1 = _input_coefficients(B, pool, real)
+        if kind == "reference":
+            t0 = time.perf_counter()
+            impl.roundtrip_batch(c1, pool)
+            est = (time.perf_counter() - t0) / pool  # per function, with the pool busy
+            n = int(min(nb, max(pool, budget_s / max(est, 1e-9)))) // pool * pool or pool
+            c = _input_coefficients(B, n, real)
+            t0 = time.perf_counter()
+            impl.roundtrip_batch(c, pool)
+            dt = time.perf_counter() - t0
+            out["sample"] = (f"{n} of the {nb} B={B} functions of one step through an outer pool of {pool} threads, "
+                             "threads=1 per function (reference oracle/_ref, ref_roundtrip_batch)")
+        else:
+            c = c1
+            t0 = time.perf_counter()
+            for f in range(pool):
+                one(impl, c[f])
+            dt = time.perf_counter() - t0
+            n = pool
+            out["sample"] = f"{n} B={B} functions, oracle port with OpenMP threads ({why})"
+        out["value"] = n / dt
+    if B >= 128 and kind == "reference":
+        out["reference_output_valid"] = False
+        out["note"] = ("reference output is numerically invalid at B >= 128 (M_lm underflow, "
+                       "special_functions.cpp:81-88): timing only; port_value = the robust C restatement")
+        orc = Oracle(B)
+        c = _input_coefficients(B, 1, real)[0]
+        one(orc, c)
+        t0 = time.perf_counter()
+        one(orc, c)
+        out["port_value"] = 1.0 / (time.perf_counter() - t0)
+    return out
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: rank 0 times the reference's CPU implementation on the
+    same workload (config dict identical to our arm's); other ranks exit."""
+    if rank != 0:
+        return
+    B, nb = args.B, args.batch
     t_all = time.perf_counter()
-    for _ in range(run):
-        g = impl.inverse(c, threads=0)
-        impl.forward(g, threads=0)
-    total = time.perf_counter() - t_all
-    ms = 1000.0 * total / run
-    note += f"; timed {run} of the requested {args.steps} steps (each step = one fwd+inv round trip)"
-    value = args.batch / (ms / 1000.0) if args.batch == 1 else 1.0 / (ms / 1000.0)
+    budget = max(20.0, min(150.0, 0.75 * args.steps))  # a few minutes at most for the whole run
+    cb = cpu_reference(B, nb, args.real, budget, max_steps=args.steps)
+    value = cb["value"]
     line = {
         "impl": "reference", "metric": f"fwd+inv SGL transforms/s at B={B} fp64", "value": value,
         "unit": "transforms/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: iid complex normal coefficients (numpy PCG64 seed 0)",
-        "config": {"workload": f"C3: B={B}, 1 function, ifsglft then fsglft", "B": B, "batch": 1},
-        "cpu_baseline": {"value": value, "unit": "transforms/s", "cores": cores, "kind": kind,
-                         "sample": f"{args.steps} round trips, {note}"},
+        "ms_per_step": 1000.0 * nb / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic: BASELINE.json config coefficients (numpy PCG64 seed 0)",
+        "config": workload_config(B, nb, args.real),
+        "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "transforms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup": {"wall_s": round(time.perf_counter() - t_all, 1),
+                  "ms_per_step": "per step of `batch` functions, extrapolated from the timed sample"},
     }
     print(json.dumps(line), flush=True)
-
-
-def cpu_baseline(B, budget_s=12.0):
-    """Reference (or oracle port) round trips on the host cores, bounded to ~budget_s."""
-    from oracle_bindings import Oracle, Reference, coefficient_count
-
-    rng = np.random.default_rng(0)
-    c = complex_normal(rng, coefficient_count(B))
-    kind = "reference"
-    try:
-        impl = Reference(B)
-        note = "reference fsglft/ifsglft, threads=0 (all cores)"
-        if B >= 128:
-            note += "; reference output invalid at B>=128 (M_lm underflow) -- timing only"
-    except Exception:
-        impl = Oracle(B)
-        kind = "port"
-        note = "oracle C restatement, OpenMP all cores"
-    impl.forward(impl.inverse(c, threads=0), threads=0)  # warm
-    n = 0
-    t0 = time.perf_counter()
-    while True:
-        impl.forward(impl.inverse(c, threads=0), threads=0)
-        n += 1
-        if time.perf_counter() - t0 > budget_s or n >= 200:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "transforms/s", "cores": os.cpu_count() or 1, "kind": kind,
-            "sample": f"{n} fwd+inv round trips at B={B} in {dt:.1f} s; {note}"}
 
 
 # ------------------------------------------------------------------ our arm
@@ -268,9 +361,7 @@ def main():
     rng = np.random.default_rng(rank)
     if args.real:
         nrot = max(2, min(nrot, 8))
-        cin = torch.from_numpy(real_valued_coeffs(rng, B, (nrot, nb))).cuda()
-    else:
-        cin = torch.from_numpy(complex_normal(rng, (nrot, nb, Om))).cuda()
+    cin = torch.from_numpy(config_coefficients(rng, B, (nrot, nb), args.real)).cuda()
     grid = torch.empty((nb, Ps), dtype=torch.float64 if args.real else torch.complex128, device="cuda")
     cout = torch.empty((nb, Om), dtype=torch.complex128, device="cuda")
     # a dedicated (non-default) stream: the library replays CUDA graphs of
@@ -299,8 +390,8 @@ def main():
     err = float((cout - cin[wl_last % nrot]).abs().max() / cin[wl_last % nrot].abs().max())
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    stage_ms = np.zeros(6)
-    stage_n = np.zeros(6, dtype=np.int32)
+    stage_ms = np.zeros(8)
+    stage_n = np.zeros(8, dtype=np.int32)
     with ClockSampler(local) as clk:
         if dist:
             dist.barrier()
@@ -353,26 +444,30 @@ def main():
     e2e_err = float(np.abs(hb - hc).max() / np.abs(hc).max())
 
     # ---- roofline of the dominant kernel (live CUDA-event times from the timed region)
+    # Algorithmic work is the reference algorithm's (workload.py);
+    # the real fast path does half of it (only m >= 0), so it is credited half.
     peaks = load_peaks()
     work = wl.stage_work(B)
+    rscale = 0.5 if args.real else 1.0
     dom = int(np.argmax(stage_ms))
     per_launch_ms = stage_ms[dom] / max(1, stage_n[dom])
-    flops, nbytes = work[dom]
+    flops, nbytes, gbytes = work[dom]
     # algorithmic work of one launch = per-step work / launches per step
     lps = max(1, int(stage_n[dom]) // args.steps)
-    flops *= nb / lps
-    nbytes *= nb / lps
+    flops *= rscale * nb / lps
+    nbytes *= rscale * nb / lps
     stage_info = {}
-    for s in range(6):
+    for s in range(8):
         if stage_n[s]:
             t_ms = stage_ms[s] / args.steps  # per step (a stage may be split into several launches)
-            tf = work[s][0] * nb / (t_ms * 1e-3) / 1e12
-            gb = work[s][1] * nb / (t_ms * 1e-3) / 1e9
-            hbm = s in (0, 5)  # the azimuthal kernels are HBM-bound, the contractions FP64-bound
+            tf = rscale * work[s][0] * nb / (t_ms * 1e-3) / 1e12
+            gb = rscale * work[s][1] * nb / (t_ms * 1e-3) / 1e9
+            gi = rscale * (work[s][1] + work[s][2]) * nb / (t_ms * 1e-3) / 1e9
+            hbm = s in (0, 5)  # the azimuthal kernels are HBM-bound, the contractions (and fused stages) FP64-bound
             stage_info[wl.STAGE_NAMES[s]] = {
                 "ms": round(t_ms, 5), "launches_per_step": int(stage_n[s]) // args.steps,
-                "tflops": round(tf, 3), "gbs": round(gb, 1),
-                "bound": "hbm" if hbm else "tensor",
+                "tflops": round(tf, 3), "gbs_compulsory": round(gb, 1), "gbs_with_intermediate": round(gi, 1),
+                "bound": "hbm" if hbm else "fp64",
                 "roofline_frac": round(gb / peaks["hbm_gbs"] if hbm else tf / FP64_PEAK_TFLOPS, 3),
                 "share": round(stage_ms[s] / stage_ms.sum(), 4),
             }
@@ -381,53 +476,55 @@ def main():
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": None,
                 "kernel": wl.STAGE_NAMES[dom], "algorithmic_bytes_per_launch": nbytes,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"}
+                "intermediate_bytes_per_launch": rscale * gbytes * nb / lps,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"}
     else:
         achieved = flops / (per_launch_ms * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
                 "kernel": wl.STAGE_NAMES[dom], "algorithmic_flops_per_launch": flops,
-                "peak_source": "measured fp64 DMMA (mma.sync m8n8k4) peak, profiles/fp64_peak_r01.txt; "
+                "peak_source": "builder-measured fp64 DMMA (mma.sync m8n8k4) peak, profiles/fp64_peak_r01.txt; "
                                "MEASURED_PEAKS.json has no fp64 entry"}
     roof["launch_ms"] = per_launch_ms
     # DRAM traffic of this kernel from the committed ncu --set full capture (B = 128)
     try:
-        with open(os.path.join(REPO, "profiles", "r01_traffic.json")) as f:
+        with open(os.path.join(REPO, "profiles", TRAFFIC_FILE)) as f:
             tr = json.load(f)["bytes"]
-        knames = {0: [f"void az_forward_kernel<{2 * B}>"], 1: ["void gemm_dmma_kernel<LegFwdTma>", "void gemm_dmma_kernel<LegFwd>"],
-                  2: ["void gemm_dmma_kernel<RadFwd>"], 3: ["void gemm_dmma_kernel<RadInv>"],
-                  4: ["void gemm_dmma_kernel<LegInvSeq>", "void gemm_dmma_kernel<LegInv>"],
-                  5: [f"void az_inverse_kernel<{2 * B}>"]}[dom]
+        knames = KERNEL_NAMES(B)[dom]
         kname = next((k for k in knames if k in tr), None)
-        if B == 128 and nb == 1 and kname is not None:
+        if B == 128 and nb == 1 and not args.real and kname is not None:
             roof["traffic"] = tr[kname]
-            roof["traffic_source"] = "profiles/r01_ncu_full.txt (dram__bytes_read.sum + dram__bytes_write.sum)"
+            roof["traffic_source"] = f"profiles/{TRAFFIC_FILE} (dram__bytes_read.sum + dram__bytes_write.sum, ncu)"
     except (OSError, KeyError, ValueError):
         pass
     roof["timing"] = ("live: CUDA events around each stage launch inside the timed region" if live_profile else
                       "live: CUDA events around each stage launch (eager launches) in a second timed pass of "
                       "the same steps, right after the headline pass")
+    t_roof = rscale * nb * wl.roofline_time(B, FP64_PEAK_TFLOPS * 1e12, peaks["hbm_gbs"] * 1e9)
     whole = 2 * wl.f_fwd(B) * nb / (ms * 1e-3) / 1e12
 
     line = {
         "metric": f"fwd+inv SGL transforms/s at B={B} fp64", "value": value, "unit": "transforms/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: iid complex normal coefficients (numpy PCG64, seed = rank)",
-        "config": {"workload": (f"C5: B={B}, {nb} real-valued functions per step per GPU (real fast path)"
-                                if args.real else f"{config_id(B, nb)}: B={B}, {nb} function(s) per step per GPU, "
-                                                  "ifsglft then fsglft"),
-                   "B": B, "batch_per_gpu": nb, "parallelism": f"replicas x{world}" if world > 1 else "single",
-                   "l2": f"inputs rotated over {nrot} coefficient buffers ({nrot * 16 * Om * nb / 1e6:.0f} MB) "
-                         f"and every step writes/reads a {16 * Ps * nb / 2**20:.0f} MiB grid (> 126 MB L2)"},
+        "data": "synthetic: coefficients with the config's BASELINE.json distribution (numpy PCG64, seed = rank)",
+        "config": workload_config(B, nb, args.real),
+        "setup": {"parallelism": f"replicas x{world}" if world > 1 else "single",
+                  "batch_per_gpu": nb,
+                  "path": "real fast path (sglgpu_*_real)" if args.real else "complex path (sglgpu_forward/inverse)",
+                  "l2": f"inputs rotated over {nrot} coefficient buffers ({nrot * 16 * Om * nb / 1e6:.0f} MB) "
+                        f"and every step writes/reads a {(8 if args.real else 16) * Ps * nb / 2**20:.0f} MiB grid "
+                        "(> 126 MB L2)"},
         "e2e": {"value": world * nb / (e2e_ms / 1000.0), "unit": "transforms/s",
                 "h2d_bytes_per_step": (16 * Om + (8 if args.real else 16) * Ps) * nb,
                 "d2h_bytes_per_step": ((8 if args.real else 16) * Ps + 16 * Om) * nb,
                 "ms_per_step": e2e_ms, "api": "paper_1604_05140_b200.ifsglft_batch/fsglft_batch (C ABI, host mem)"},
         "gpu_launches": gpu_launches,
         "roofline": roof,
-        "transform_fp64_tflops": whole,
-        "transform_roofline_frac": whole / FP64_PEAK_TFLOPS,
+        "transform_fp64_tflops": rscale * whole,
+        "transform_roofline": {"per_stage_roofline_ms": 1e3 * t_roof, "measured_ms": ms, "frac": 1e3 * t_roof / ms,
+                               "definition": "sum over both directions of max(F_s/P_fp64, Q_s/BW_hbm) for the "
+                                             "spherical and radial stages (SURVEY.md 8(d))"},
         "stages": stage_info,
         "clocks": clk.summary(),
         "roundtrip_normwise_err": max(err, e2e_err),
@@ -436,7 +533,7 @@ def main():
         raise SystemExit(f"bench: round trip failed (normwise error {line['roundtrip_normwise_err']:.3e}); "
                          "refusing to report a timing of wrong results")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(B)
+        line["cpu_baseline"] = cpu_reference(B, nb, args.real, budget_s=15.0)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

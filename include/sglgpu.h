@@ -186,8 +186,10 @@ int sglgpu_last_launch_count(const sglgpu_plan* plan);
  * of sglgpu_forward / sglgpu_inverse is bracketed by CUDA events on the call's
  * stream; end synchronizes and returns, per stage, the summed milliseconds and
  * the number of launches.  Stages: 0 az_forward, 1 legendre_forward,
- * 2 radial_forward, 3 radial_inverse, 4 legendre_inverse, 5 az_inverse. */
-#define SGLGPU_NUM_STAGES 6
+ * 2 radial_forward, 3 radial_inverse, 4 legendre_inverse, 5 az_inverse,
+ * 6 spherical_forward (the fused persistent az + Legendre launch),
+ * 7 spherical_inverse (fused).  Arrays have SGLGPU_NUM_STAGES entries. */
+#define SGLGPU_NUM_STAGES 8
 int sglgpu_profile_begin(sglgpu_plan* plan);
 int sglgpu_profile_end(sglgpu_plan* plan, double* stage_ms, int* stage_launches);
 

@@ -87,7 +87,9 @@ struct DevBuf {
     }
 };
 
-enum Kind { kLegFwd = 0, kLegInv = 1, kRadFwd = 2, kRadInv = 3 };
+// kLegFwdS: the Legendre forward over one shell slice of the fused spherical
+// forward (tiles straddle the +m / -m halves).
+enum Kind { kLegFwd = 0, kLegInv = 1, kRadFwd = 2, kRadInv = 3, kLegFwdS = 4 };
 
 }  // namespace
 
@@ -107,6 +109,7 @@ struct sglgpu_plan {
     double* d_r = nullptr;     // radial rule (separated cross-oracle only)
     double* d_amod = nullptr;
     DevBuf G, S, in, out;
+    DevBuf counters;  // work-queue counters of the fused persistent kernels (ints)
     std::map<std::tuple<int, int, int, int, int>, std::pair<sglk::TileMap*, int>> tiles;
     std::mutex mu;
     int last_launches = 0;
@@ -134,6 +137,7 @@ namespace {
 // Host-side mirror of the per-problem shapes in sgl_kernels.cu.
 void problem_shape(Kind kind, int B, int batch, long long NB, int pid, bool real, int& M, int& N, int& K) {
     switch (kind) {
+        case kLegFwdS:
         case kLegFwd: {
             const int am = pid >> 1, r = B - am - (pid & 1);
             M = r > 0 ? (r + 1) / 2 : 0;
@@ -172,12 +176,13 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
     const int B = p->B;
     const long long NB = 2LL * batch * SC;
     int plo = lo, phi = hi;
-    const bool leg = kind == kLegFwd || kind == kLegInv;
+    const bool leg = kind == kLegFwd || kind == kLegInv || kind == kLegFwdS;
     if (leg) {
         plo = 0;
         phi = 2 * B;
     }
-    static const char* const kind_env[4] = {"SGL_WM_LEGFWD", "SGL_WM_LEGINV", "SGL_WM_RADFWD", "SGL_WM_RADINV"};
+    static const char* const kind_env[5] = {"SGL_WM_LEGFWD", "SGL_WM_LEGINV", "SGL_WM_RADFWD", "SGL_WM_RADINV",
+                                            "SGL_WM_LEGFWD"};
     const char* wm_env = std::getenv(kind_env[kind]);  // experiments: force one kind's warp layout
     if (!wm_env) wm_env = std::getenv(leg ? "SGL_WM_LEG" : "SGL_WM_RAD");
     const int wm_force = wm_env ? std::atoi(wm_env) : 0;
@@ -194,7 +199,7 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
         if (K <= 0 && kind != kLegInv) continue;  // LegInv with K = 0 must still write zeros
         // Legendre tiles never straddle the +m / -m halves of N (column addresses
         // stay affine inside a tile)
-        const long long half = leg ? NB : N;
+        const long long half = leg && kind != kLegFwdS ? NB : N;  // kLegFwdS: one tile spans both halves
         const int halves = (int)(N / half);
         // ties: the widest tile, except for the radial inverse (M = 2B rows of
         // V_l against a few coefficient columns), where 128 x 32 measured faster
@@ -209,7 +214,7 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
             }
         }
         if (wm_force == 1 || wm_force == 2 || wm_force == 4) lwm = wm_force == 1 ? 0 : wm_force == 2 ? 1 : 2;
-        const int max_wm = kind == kLegFwd ? SGL_MAXWM_LEGFWD : kind == kLegInv ? SGL_MAXWM_LEGINV
+        const int max_wm = kind == kLegFwdS ? 1 : kind == kLegFwd ? SGL_MAXWM_LEGFWD : kind == kLegInv ? SGL_MAXWM_LEGINV
                          : kind == kRadFwd ? SGL_MAXWM_RADFWD : SGL_MAXWM_RADINV;
         while ((1 << lwm) > max_wm) --lwm;
         const int bm = 32 << lwm, bn = 128 >> lwm;
@@ -240,7 +245,7 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
         for (const Entry& e : ents) {
             int M, N, K;
             problem_shape(kind, B, batch, NB, e.pid, real, M, N, K);
-            const long long half = leg ? NB : N, kk = std::max(K, 1);
+            const long long half = leg && kind != kLegFwdS ? NB : N, kk = std::max(K, 1);
             const int bm = 32 << e.lwm, bn = 128 >> e.lwm;
             for (int mi = 0; mi < e.tm; ++mi)
                 for (int h = 0; h < e.halves; ++h)
@@ -379,12 +384,62 @@ Slices plan_slices(int B, int nb) {
 
 // Stage sequences on device memory.  X: samples (function stride Psi complex),
 // C: coefficients (function stride Omega complex).
+// The fused persistent spherical forward (launch_spherical_forward_fused), opt-in
+// with SGL_FUSED=1 for power-of-two 2B in [32, 256].  Measured at B = 128 (one
+// function): 218 us against 95.5 + 94.2 us for the two kernels it replaces (its
+// azimuthal items alone 125 us, its Legendre tiles alone 109 us -- the two
+// latency-bound halves do not overlap on the same SMs, and the persistent loop
+// adds per-item cost), with the L2 discard of consumed G lines 469 us.  Kept as a
+// tested alternative; DESIGN.md section 4.  SGL_FUSED_SLICE sets the shell slice
+// (default 32), SGL_FUSED_DISCARD=1 drops consumed G lines from L2,
+// SGL_FUSED_GRID overrides the persistent grid.
+int fused_slice_shells(int B, int nb, int lgib) {
+    const char* e = std::getenv("SGL_FUSED");
+    if (!e || e[0] != '1') return 0;
+    if (B < 16 || B > 128 || (B & (B - 1))) return 0;
+    int sls = 32;
+    if (const char* v = std::getenv("SGL_FUSED_SLICE")) sls = std::atoi(v);
+    if (sls < (1 << lgib) || sls > 32 || sls % (1 << lgib) || (2 * B) % sls) return 0;
+    (void)nb;
+    return sls;
+}
+
 int forward_device(sglgpu_plan* p, const double* X, double* C, int nb, cudaStream_t st) {
     const int B = p->B;
     const size_t psi2 = 2 * (size_t)sample_count(B), om2 = 2 * (size_t)coefficient_count(B);
     const Slices sl = plan_slices(B, nb);
     p->S.ensure((size_t)4 * B * B * B * nb);
     int n = 0, k;
+    {
+        sglk::Geo g{B, 2 * B, nb, 2LL * nb * 2 * B};
+        const long long gsize = sglk::g_layout(g);
+        const int sls = sl.count == 1 ? fused_slice_shells(B, nb, g.lgib) : 0;
+        if (sls > 0) {
+            p->G.ensure(2 * (size_t)gsize);
+            const int nslices = nb * 2 * B / sls;
+            p->counters.ensure((size_t)(1 + 2 * nslices + 1) / 2 + 1);
+            auto lt = tiles_for(p, kLegFwdS, 1, sls, 0, 2 * B);
+            const char* dz = std::getenv("SGL_FUSED_DISCARD");
+            const char* gr = std::getenv("SGL_FUSED_GRID");
+            k = staged(p, 6, st, [&] {
+                return sglk::launch_spherical_forward_fused(
+                    g, X, psi2, p->G.p, p->d_bcal, p->d_tw, p->S.p, sglk::SView{g.NB, 2 * B, 0}, p->d_leg,
+                    p->d_leg_off, lt.first, lt.second, sls, reinterpret_cast<int*>(p->counters.p), dz && dz[0] == '1',
+                    gr ? std::atoi(gr) : 0, st);
+            });
+            if (k != -2) {
+                ck_launch(k, "spherical_forward_fused");
+                n += k;
+                auto rt = tiles_for(p, kRadFwd, nb, 2 * B, 0, B);
+                k = staged(p, 2, st, [&] {
+                    return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, p->S.p, C, p->d_W, p->d_W_off,
+                                                       rt.first, rt.second, st);
+                });
+                ck_launch(k, "radial_forward");
+                return n + k;
+            }
+        }
+    }
     if (nb == 1) {
         // shell slices: az + Legendre per slice into the full S, then radial once
         const int SC = sl.shells;

@@ -292,6 +292,34 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
     return v;
 }
 
+// L2 eviction-priority policies (createpolicy): streamed-once data (samples in,
+// S out) marked evict_first so that the intermediate G, written by one kernel and
+// read by the next, is what the L2 keeps (SGL_L2HINTS experiments).
+#ifndef SGL_L2HINTS
+#define SGL_L2HINTS 0
+#endif
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double2 ld_stream_hint(const double2* p, unsigned long long pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;\n"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_hint(double2* p, double2 v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+                 : "memory");
+}
+
 // ------------------------------------------------------------------ async copy helpers
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
@@ -320,11 +348,21 @@ __device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
 }
 __device__ __forceinline__ void tma_load_5d(unsigned dst, const void* tmap, unsigned bar, int c0, int c1, int c2,
                                             int c3, int c4) {
+#if SGL_L2HINTS
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, "
+        "%4, %5, %6}], [%7], %8;\n" ::"r"(dst),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar), "l"(pol)
+        : "memory");
+#else
     asm volatile(
         "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], "
         "[%7];\n" ::"r"(dst),
         "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
         : "memory");
+#endif
 }
 
 // ------------------------------------------------------------------ azimuthal forward
@@ -335,17 +373,17 @@ __device__ __forceinline__ void tma_load_5d(unsigned dst, const void* tmap, unsi
 // lands in shared memory, where the epilogue folds the ring pair into even/odd
 // parts, applies b_cal and writes rows of G[p][|m|][j'][sgn][s] (IG shells
 // contiguous per row).
+// One azimuthal-forward work item: shells [s0, s0 + IG) at polar node pair
+// (jp, 2B-1-jp), on `rings` (2 IG padded rings of shared memory).  Called by
+// az_forward_kernel (one item per CTA) and by the fused persistent spherical
+// forward (sph_fwd_fused_kernel).
 template <int N>
-__global__ void __launch_bounds__(FFTShape<N>::THREADS, FFTShape<N>::MINB)
-az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2* __restrict__ G,
-                  const double* __restrict__ bcal, const double2* __restrict__ twg) {
+__device__ __forceinline__ void az_fwd_item(const Geo& g, const double2* __restrict__ X, size_t fstride,
+                                            double2* __restrict__ G, const double* __restrict__ bcal,
+                                            const double2* __restrict__ twg, int s0, int jp, double2* rings) {
     using S = FFTShape<N>;
     constexpr int B = N / 2;
-    extern __shared__ double2 smem[];
-    double2* rings = smem;
     const int tid = threadIdx.x;
-    const int jp = blockIdx.y;
-    const int s0 = blockIdx.x * S::IG;
     const int nshell = g.batch * g.SC;
     {
         // twiddles come straight from the (L1-resident) per-pass global tables;
@@ -362,12 +400,17 @@ az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2*
             src = X + (size_t)f * fstride + ((size_t)i * N + j) * N;
         }
         double2* ring = rings + q * S::STRIDE;
+        const unsigned long long pol = SGL_L2HINTS ? policy_evict_first() : 0ull;
         ring_fft_io<N, -1, false>(
-            ring, tt, twg, [&](int x) { return ok ? ld_stream(src + x) : make_double2(0.0, 0.0); },
+            ring, tt, twg,
+            [&](int x) {
+                return ok ? (SGL_L2HINTS ? ld_stream_hint(src + x, pol) : ld_stream(src + x)) : make_double2(0.0, 0.0);
+            },
             [&](int x, double2 v) { ring[phys(x)] = v; });
     }
     __syncthreads();
     // epilogue: E/O fold, b_cal, scatter rows G[p][|m|][j'][sgn][s]
+    const unsigned long long gpol = SGL_L2HINTS ? policy_evict_last() : 0ull;
     const double b = __ldg(bcal + jp);
 #pragma unroll 4
     for (int idx = tid; idx < 2 * N * S::IG; idx += S::THREADS) {
@@ -379,8 +422,21 @@ az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2*
         const double2 f1 = rings[(2 * sl) * S::STRIDE + phys(bin)];
         const double2 f2 = rings[(2 * sl + 1) * S::STRIDE + phys(bin)];
         const double2 v = p ? csub(f1, f2) : cadd(f1, f2);
-        G[g_index(g, p, bin, jp, s)] = cscale(b, v);
+#ifdef SGL_G_WRAP  // timing-only experiment: G stores wrap inside an L2-sized window (wrong results)
+        G[g_index(g, p, bin, jp, s) % (SGL_G_WRAP * 65536LL)] = cscale(b, v);
+#else
+        if (SGL_L2HINTS) st_hint(G + g_index(g, p, bin, jp, s), cscale(b, v), gpol);
+        else G[g_index(g, p, bin, jp, s)] = cscale(b, v);
+#endif
     }
+}
+
+template <int N>
+__global__ void __launch_bounds__(FFTShape<N>::THREADS, FFTShape<N>::MINB)
+az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2* __restrict__ G,
+                  const double* __restrict__ bcal, const double2* __restrict__ twg) {
+    extern __shared__ double2 smem[];
+    az_fwd_item<N>(g, X, fstride, G, bcal, twg, blockIdx.x * FFTShape<N>::IG, blockIdx.y, smem);
 }
 
 // ------------------------------------------------------------------ azimuthal inverse
@@ -415,7 +471,15 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
         const int rowi = idx / S::IG;  // p * N + bin
         const int p = rowi / N, bin = rowi - p * N;
         const int s = s0 + sl;
-        pv[q] = (bin != B && s < nshell) ? ld_stream(G + g_index(g, p, bin, jp, s)) : make_double2(0.0, 0.0);
+#ifdef SGL_G_WRAP
+        pv[q] = (bin != B && s < nshell) ? ld_stream(G + g_index(g, p, bin, jp, s) % (SGL_G_WRAP * 65536LL))
+                                         : make_double2(0.0, 0.0);
+#else
+        pv[q] = (bin != B && s < nshell)
+                    ? (SGL_L2HINTS ? ld_stream_hint(G + g_index(g, p, bin, jp, s), policy_evict_first())
+                                   : ld_stream(G + g_index(g, p, bin, jp, s)))
+                    : make_double2(0.0, 0.0);
+#endif
     }
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
@@ -1062,6 +1126,21 @@ struct LegFwdTmaPeers : LegFwdTma {
         return pd.base[q] + rowC(pid, r);
     }
 };
+// Legendre forward over one SLICE of at most 32 shells (the fused persistent
+// spherical forward): 32 x 128 tiles that straddle the +m / -m halves (NB <= 64
+// reals per half), so a tile's B operand is two TMA boxes per k-chunk -- bin m and
+// bin 2B - m of the slice's shell groups -- and the G block a slice needs stays
+// L2-sized.  The tensor map lives in the kernel's grid-constant parameters
+// (tmap_ptr points there); gx_base is the slice's first shell group.
+struct LegFwdSlice : LegFwd {
+    static constexpr bool B_TMA = true;
+    static constexpr bool STRADDLE = true;
+    static constexpr int GEMM_MAXWM = 1;
+    const CUtensorMap* tmap_ptr;
+    int gx_base;
+    unsigned box_bytes;  // one half's box: NB x BK doubles
+    __device__ int nlim(int pid, int) const { return N(pid); }
+};
 struct LegInvSeq : LegInv {  // CTAs run TileMap::seq consecutive n-blocks
     static constexpr bool GEMM_SEQ = true;
 };
@@ -1100,6 +1179,11 @@ template <class P, class = void>
 struct has_btma : std::false_type {};
 template <class P>
 struct has_btma<P, std::void_t<decltype(P::B_TMA)>> : std::bool_constant<P::B_TMA> {};
+
+template <class P, class = void>
+struct has_straddle : std::false_type {};
+template <class P>
+struct has_straddle<P, std::void_t<decltype(P::STRADDLE)>> : std::bool_constant<P::STRADDLE> {};
 
 template <class P, class = void>
 struct has_bcast : std::false_type {};
@@ -1240,8 +1324,11 @@ __device__ __forceinline__ void gemm_epilogue(const P& pr, int pid, int m0, int 
         for (int fn = 0; fn < 4; ++fn) {
             const int col = n0 + wc + fn * 8 + 2 * (lane & 3);
             if (col >= N) continue;
-            *reinterpret_cast<double2*>(out + cofs[fn]) =
-                make_double2(flip(acc[fm][fn][0], csg[fn]), flip(acc[fm][fn][1], csg[fn]));
+            const double2 v = make_double2(flip(acc[fm][fn][0], csg[fn]), flip(acc[fm][fn][1], csg[fn]));
+            if (SGL_L2HINTS && has_colc4<P>::value)  // the Legendre inverse writes G: keep it in L2
+                st_hint(reinterpret_cast<double2*>(out + cofs[fn]), v, policy_evict_last());
+            else
+                *reinterpret_cast<double2*>(out + cofs[fn]) = v;
             if constexpr (has_mirror<P>::value) {
                 bool neg = false;
                 const long long mo = pr.colC_mirror(pid, col, neg);
@@ -1413,7 +1500,22 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
             const int nb = ok1 ? (ok2 ? 16 : 8) : 0;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(ok1 ? src : pr.A), "r"(nb));
         }
-        if constexpr (has_btma<P>::value) {
+        if constexpr (has_straddle<P>::value) {
+            // two TMA boxes per chunk: the slice's shells at bin m (columns [0, NB))
+            // and, for m != 0, at bin 2B - m (columns [NB, 2 NB))
+            if (tid == 0) {
+                const int a = pr.am(pid);
+                const bool two = N > (int)pr.g.NB;
+                const unsigned bar = tma_bar0 + 8u * (unsigned)(v % ST);
+                const int row = (pid & 1) * pr.g.nbins;
+                mbar_expect_tx(bar, two ? 2 * pr.box_bytes : pr.box_bytes);
+                const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(bs));
+                tma_load_5d(dst, pr.tmap_ptr, bar, 0, k0, 0, pr.gx_base, row + a);
+                if (two) tma_load_5d(dst + pr.box_bytes, pr.tmap_ptr, bar, 0, k0, 0, pr.gx_base, row + 2 * pr.g.B - a);
+            }
+            cp_async_commit();
+            return;
+        } else if constexpr (has_btma<P>::value) {
             // one TMA per chunk: box {8 doubles, BK rows j', BN/8 groups} of G
             if (tid == 0) {
                 const int NB = (int)pr.g.NB;
@@ -1519,8 +1621,7 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
 // Tile of this CTA from the launch's problem table (kernel parameter space: a
 // handful of constant-cache reads instead of a dependent global load at CTA start).
 template <int SEQ>
-__device__ __forceinline__ Tile decode_tile(const TileMap& tm, long long NB) {
-    const int b = blockIdx.x;
+__device__ __forceinline__ Tile decode_tile(const TileMap& tm, long long NB, int b) {
     int lo = 0, hi = tm.nprob - 1;  // last entry with first[q] <= b
     if (tm.first[tm.nprob] == tm.nprob) lo = hi = b;  // one entry per tile
     while (lo < hi) {
@@ -1549,7 +1650,7 @@ __device__ __forceinline__ Tile decode_tile(const TileMap& tm, long long NB) {
 template <class P>
 __global__ void __launch_bounds__(128, P::GEMM_MINB) gemm_dmma_kernel(const __grid_constant__ P pr, const __grid_constant__ TileMap tm) {
     extern __shared__ __align__(128) double gsm[];
-    const Tile t = decode_tile<P::GEMM_SEQ>(tm, pr.g.NB);
+    const Tile t = decode_tile<P::GEMM_SEQ>(tm, pr.g.NB, blockIdx.x);
     switch (t.pad) {  // warp layout chosen per tile (the host keeps wm <= P::GEMM_MAXWM)
         case 1: gemm_tile<P, 1>(pr, t, gsm); break;
         case 2: if constexpr (P::GEMM_MAXWM >= 2) gemm_tile<P, 2>(pr, t, gsm); break;
@@ -1676,7 +1777,7 @@ static int gemm_launch(const P& p, const TileMap* tiles, int ntiles, cudaStream_
 // TMA descriptor of the blocked G as a 5-D tensor [p][bin][group][j'][8 doubles]
 // (innermost first: 8 doubles = 4 shells x re/im, j', group, bin, p) whose box
 // {8, BK, 16, 1, 1} is one 32 x 128 tile's k-chunk of B.
-static bool make_g_tensor_map(const Geo& g, const double* G, int bk, CUtensorMap* out) {
+static bool make_g_tensor_map(const Geo& g, const double* G, int bk, CUtensorMap* out, int box_groups = 0) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -1693,11 +1794,184 @@ static bool make_g_tensor_map(const Geo& g, const double* G, int bk, CUtensorMap
     // (p, bin) as one index p * nbins + bin (its stride is W doubles either way)
     const cuuint64_t dims[5] = {8, (cuuint64_t)g.B, H, groups, 2ULL * g.nbins};
     const cuuint64_t strides[4] = {row * 8, 64, 2ULL * g.nbins * W * 8, W * 8};
-    const cuuint32_t box[5] = {8, (cuuint32_t)bk, (cuuint32_t)H, (cuuint32_t)(128 / W), 1};
+    const cuuint32_t box[5] = {8, (cuuint32_t)bk, (cuuint32_t)H, (cuuint32_t)(box_groups > 0 ? box_groups : 128 / W), 1};
     const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(G), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// ------------------------------------------------------------------ fused spherical forward
+// One persistent launch for the whole spherical forward stage: CTAs pull work
+// items from a global ticket counter -- azimuthal items (IG shells x one polar
+// node pair, az_fwd_item) and Legendre tiles (LegFwdSlice) -- in the order
+//   A_0, A_1 L_0, A_2 L_1, ..., A_{S-1} L_{S-2}, L_{S-1}
+// (A_s: the azimuthal items of shell slice s, L_s: its Legendre tiles), so the
+// DMMA-bound Legendre tiles of one slice run on the same SMs as, and overlap, the
+// HBM-bound FFTs of the next.  A Legendre tile waits (one thread, acquire loads)
+// until its slice's azimuthal items are all done; azimuthal items never wait, so
+// the ticket order makes the schedule deadlock-free (every item a waiter depends
+// on holds a lower ticket and is running or finished).  A slice's G block (at most
+// 32 shells: 32 MB at B = 128) is consumed right after it is produced, from L2;
+// with `discard` the last tile of a slice drops the slice's G lines from L2
+// (discard.global.L2) so they are never written back to HBM.
+struct SphFwdFused {
+    Geo g;  // the call (batch, SC = 2B, G layout)
+    const double2* X;
+    size_t fstride;
+    double2* G;
+    const double* bcal;
+    const double2* twg;
+    LegFwdSlice leg;  // slice template: C = S base, sv = the full S view
+    alignas(64) CUtensorMap tmap;
+    int slice_shells, nslices, az_per_slice, leg_per_slice, total, discard;
+    int mode;  // experiments (timing only, wrong results): 1 = azimuthal items only, 2 = Legendre tiles only
+    int* ticket;
+    int* az_done;
+    int* leg_done;
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int N>
+__global__ void __launch_bounds__(128, 4)
+sph_fwd_fused_kernel(const __grid_constant__ SphFwdFused prm, const __grid_constant__ TileMap tm) {
+    static_assert(FFTShape<N>::THREADS == 128, "fused items share 128-thread CTAs");
+    extern __shared__ __align__(128) double gsm[];
+    __shared__ int s_item, s_last;
+    const int tid = threadIdx.x;
+    const int nA = prm.az_per_slice, nL = prm.leg_per_slice, S = prm.nslices;
+    constexpr int IG = FFTShape<N>::IG;
+    for (;;) {
+        if (tid == 0) s_item = atomicAdd(prm.ticket, 1);
+        __syncthreads();
+        const int t = s_item;
+        __syncthreads();
+        if (t >= prm.total) return;
+        int slice, idx;
+        bool az;
+        if (t < nA) {
+            az = true;
+            slice = 0;
+            idx = t;
+        } else {
+            const int u = t - nA, k = 1 + u / (nA + nL), r = u - (k - 1) * (nA + nL);
+            if (k < S && r < nA) {
+                az = true;
+                slice = k;
+                idx = r;
+            } else {
+                az = false;
+                slice = k - 1;
+                idx = k < S ? r - nA : r;
+            }
+        }
+        const int s_first = slice * prm.slice_shells;
+        if ((prm.mode == 1 && !az) || (prm.mode == 2 && az)) continue;
+        if (az) {
+            const int gps = prm.slice_shells / IG;  // shell groups per slice
+            az_fwd_item<N>(prm.g, prm.X, prm.fstride, prm.G, prm.bcal, prm.twg, s_first + (idx % gps) * IG, idx / gps,
+                           reinterpret_cast<double2*>(gsm));
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) atomicAdd(prm.az_done + slice, 1);
+            continue;
+        }
+        if (tid == 0) {
+            while (prm.mode == 0 && ld_acquire_gpu(prm.az_done + slice) < nA) __nanosleep(200);
+            // the G block was written through the generic proxy by other CTAs; the
+            // TMA reads it through the async proxy
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        }
+        __syncthreads();
+        LegFwdSlice pr = prm.leg;
+        const int f = s_first / prm.g.SC;
+        pr.C = prm.leg.C + (size_t)f * 2 * prm.g.SC;  // S[nu][f][i]: this function's block
+        pr.sv.i0 = s_first - f * prm.g.SC;
+        pr.gx_base = s_first >> prm.g.lgib;
+        pr.tmap_ptr = &prm.tmap;
+        gemm_tile<LegFwdSlice, 1>(pr, decode_tile<false>(tm, pr.g.NB, idx), gsm);
+        __syncthreads();
+        if (tid == 0) s_last = prm.discard && atomicAdd(prm.leg_done + slice, 1) + 1 == nL;
+        __syncthreads();
+        if (s_last) {  // every tile of the slice has read its G block: drop it from L2 unwritten
+            const long long row = (long long)prm.g.ngx * 2 * prm.g.nbins * IG;  // complex per j' row
+            const long long blk = 2LL * prm.g.nbins * prm.slice_shells;         // the slice's complex per row
+            const long long lines = blk * 16 / 128;
+            const double2* base = prm.G + (long long)(s_first >> prm.g.lgib) * 2 * prm.g.nbins * IG;
+            for (long long q = tid; q < (long long)prm.g.B * lines; q += 128) {
+                const long long jp = q / lines, ln = q - jp * lines;
+                const char* a = reinterpret_cast<const char*>(base + jp * row) + ln * 128;
+                asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(a) : "memory");
+            }
+        }
+    }
+}
+
+template <int N>
+static int sph_fwd_fused_launch(const SphFwdFused& prm, const TileMap* tiles, int grid, cudaStream_t s) {
+    using S = FFTShape<N>;
+    constexpr size_t az_smem = sizeof(double2) * (2 * S::IG * S::STRIDE);
+    constexpr size_t gm_smem = gemm_smem_bytes<LegFwdSlice>();
+    constexpr size_t smem = az_smem > gm_smem ? az_smem : gm_smem;
+    static SmemAttrOnce attr;
+    attr.ensure(sph_fwd_fused_kernel<N>, smem);
+    if (grid <= 0) {
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sph_fwd_fused_kernel<N>, 128, smem);
+        grid = sms * (per > 0 ? per : 1);
+    }
+    sph_fwd_fused_kernel<N><<<grid, 128, smem, s>>>(prm, *tiles);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_spherical_forward_fused(const Geo& g, const double* X, size_t sample_stride, double* G, const double* bcal,
+                                   const double* tw, double* S, const SView& sv, const double* tab,
+                                   const long long* tab_off, const TileMap* tiles, int tiles_per_slice,
+                                   int slice_shells, int* counters, bool discard, int grid, cudaStream_t s) {
+    const int nshell = g.batch * g.SC;
+    const int ig = 1 << g.lgib;
+    if (g.real || slice_shells <= 0 || slice_shells > 32 || slice_shells % ig || nshell % slice_shells ||
+        g.SC % slice_shells)
+        return -2;
+    SphFwdFused prm{};
+    prm.g = g;
+    prm.X = reinterpret_cast<const double2*>(X);
+    prm.fstride = sample_stride / 2;
+    prm.G = reinterpret_cast<double2*>(G);
+    prm.bcal = bcal;
+    prm.twg = reinterpret_cast<const double2*>(tw);
+    Geo gs = g;  // one slice's Legendre geometry (the G row stride keeps the full ngx)
+    gs.SC = slice_shells;
+    gs.batch = 1;
+    gs.NB = 2LL * slice_shells;
+    static_cast<LegFwd&>(prm.leg) = LegFwd{gs, tab, tab_off, G, S, sv};
+    prm.leg.box_bytes = (unsigned)(gs.NB * LegFwd::GEMM_BK * sizeof(double));
+    if (!make_g_tensor_map(g, G, LegFwd::GEMM_BK, &prm.tmap, slice_shells / ig)) return -2;
+    prm.slice_shells = slice_shells;
+    prm.nslices = nshell / slice_shells;
+    prm.az_per_slice = (slice_shells / ig) * g.B;
+    prm.leg_per_slice = tiles_per_slice;
+    prm.total = prm.nslices * (prm.az_per_slice + tiles_per_slice);
+    prm.discard = discard ? 1 : 0;
+    if (const char* e = std::getenv("SGL_FUSED_MODE")) prm.mode = std::atoi(e);
+    prm.ticket = counters;
+    prm.az_done = counters + 1;
+    prm.leg_done = counters + 1 + prm.nslices;
+    if (cudaMemsetAsync(counters, 0, sizeof(int) * (1 + 2 * prm.nslices), s) != cudaSuccess) return -1;
+    switch (2 * g.B) {
+        case 32: return sph_fwd_fused_launch<32>(prm, tiles, grid, s);
+        case 64: return sph_fwd_fused_launch<64>(prm, tiles, grid, s);
+        case 128: return sph_fwd_fused_launch<128>(prm, tiles, grid, s);
+        case 256: return sph_fwd_fused_launch<256>(prm, tiles, grid, s);
+        default: return -2;
+    }
 }
 
 int launch_legendre_forward(const Geo& g, const SView& sv, const double* G, double* S, const double* tab,

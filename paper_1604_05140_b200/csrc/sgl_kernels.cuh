@@ -120,6 +120,17 @@ int launch_legendre_inverse(const Geo& g, const SView& sv, const double* S, doub
                             const long long* tab_off, const TileMap* tiles, int ntiles,
                             cudaStream_t s);
 
+// The whole spherical forward (azimuthal FFT + Legendre contraction) as ONE
+// persistent launch over shell slices of `slice_shells` (<= 32) shells: the
+// Legendre tiles of a slice (a straddling tile map from the host, tiles_per_slice
+// entries) overlap the FFTs of the next slice and read its G block from L2.
+// counters: 1 + 2 * nslices ints of device scratch (zeroed by the launcher).
+// grid <= 0: one CTA per resident slot.  Returns -2 if the shape is unsupported.
+int launch_spherical_forward_fused(const Geo& g, const double* X, size_t sample_stride, double* G, const double* bcal,
+                                   const double* tw, double* S, const SView& sv, const double* tab,
+                                   const long long* tab_off, const TileMap* tiles, int tiles_per_slice,
+                                   int slice_shells, int* counters, bool discard, int grid, cudaStream_t s);
+
 // Radial stage: per l DMMA contraction against W_l (forward) / V_l (inverse).
 // S is read/written as shell blocks (see ShellBlocks in sgl_kernels.cu); for the
 // single-GPU transform rb = {2B, 0, 0} and g.SC = 2B.

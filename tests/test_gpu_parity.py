@@ -741,3 +741,19 @@ def test_fast_transform_exact_on_sampled_basis_at_large_b(B):
         target = np.zeros_like(f)
         target[sgl.omega_index(n, l, m)] = 1.0
         assert np.abs(f - target).max() <= 1e-10, (n, l, m, np.abs(f - target).max())
+
+
+@pytest.mark.parametrize("B", [16, 64, 128])
+def test_fused_spherical_forward_matches_oracle(B, monkeypatch):
+    """The opt-in persistent fused spherical forward (SGL_FUSED=1: azimuthal items
+    and straddling Legendre slice tiles in one launch) gives
+    the same coefficients as the oracle, also for a batch."""
+    import torch
+
+    monkeypatch.setenv("SGL_FUSED", "1")
+    plan, orc = plan_for(B)
+    rng = np.random.default_rng(500 + B)
+    x = complex_normal(rng, (2, sample_count(B)))
+    f = sgl.fsglft_batch(plan, torch.from_numpy(x).cuda()).cpu().numpy()
+    for b in range(2):
+        assert normwise(f[b], orc.forward(x[b])) <= TOL
