@@ -7,10 +7,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -89,6 +93,48 @@ struct DevBuf {
 
 // kLegFwdS: the Legendre forward over one shell slice of the fused spherical
 // forward (tiles straddle the +m / -m halves).
+// Device workspaces of one transform in flight: the intermediates G and S and
+// the work-queue counters of the fused kernels.
+struct Work {
+    DevBuf G, S, counters;
+    void release() {
+        G.release();
+        S.release();
+        counters.release();
+    }
+};
+
+// One host-memory call in flight (sglgpu_* with SGLGPU_MEM_HOST): its own
+// workspaces, double-buffered device staging of inputs and outputs, three
+// streams (H2D, compute, D2H) so that chunk k+1 uploads while chunk k computes
+// and chunk k-1 downloads, and pinned host staging for pageable user memory.
+// A plan keeps up to kHostSlots of them, so that host calls from several threads
+// run concurrently (PCIe is full duplex: one caller's downloads overlap
+// another's uploads).
+constexpr int kHostSlots = 2;
+struct HostSlot {
+    Work w;
+    DevBuf din[2], dout[2];
+    double* hst[2] = {nullptr, nullptr};  // pinned staging pieces (pageable user memory)
+    size_t hst_cap = 0;                   // doubles per staging piece
+    cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
+    cudaEvent_t eh[2] = {}, ec[2] = {}, ed[2] = {}, es[2] = {};
+    bool busy = false;
+    void release() {
+        w.release();
+        for (int b = 0; b < 2; ++b) {
+            din[b].release();
+            dout[b].release();
+            if (hst[b]) cudaFreeHost(hst[b]);
+            hst[b] = nullptr;
+            for (cudaEvent_t* e : {&eh[b], &ec[b], &ed[b], &es[b]})
+                if (*e) cudaEventDestroy(*e);
+        }
+        for (cudaStream_t* q : {&sh, &sc, &sd})
+            if (*q) cudaStreamDestroy(*q);
+    }
+};
+
 enum Kind { kLegFwd = 0, kLegInv = 1, kRadFwd = 2, kRadInv = 3, kLegFwdS = 4 };
 
 }  // namespace
@@ -108,11 +154,13 @@ struct sglgpu_plan {
     long long* d_V_off = nullptr;
     double* d_r = nullptr;     // radial rule (separated cross-oracle only)
     double* d_amod = nullptr;
-    DevBuf G, S, in, out;
-    DevBuf counters;  // work-queue counters of the fused persistent kernels (ints)
+    Work main;  // workspaces of device-memory calls and the stage entry points (under mu)
+    std::vector<std::unique_ptr<HostSlot>> slots;  // host-memory calls (acquired under mu)
+    std::condition_variable slot_cv;
     std::map<std::tuple<int, int, int, int, int>, std::pair<sglk::TileMap*, int>> tiles;
-    std::mutex mu;
-    int last_launches = 0;
+    std::mutex mu;       // device-memory calls, stage entry points, slot acquisition
+    std::mutex meta_mu;  // the tile-map cache and the profiling records
+    std::atomic<int> last_launches{0};
     // live per-stage timing (sglgpu_profile_begin/end)
     bool profiling = false;
     std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> prof;
@@ -171,6 +219,7 @@ void problem_shape(Kind kind, int B, int batch, long long NB, int pid, bool real
 std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int SC, int lo, int hi,
                                          bool real = false) {
     const auto key = std::make_tuple((int)kind + (real ? 16 : 0), batch, SC, lo, hi);
+    std::lock_guard<std::mutex> meta(p->meta_mu);
     auto it = p->tiles.find(key);
     if (it != p->tiles.end()) return it->second;
     const int B = p->B;
@@ -280,6 +329,7 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
 void set_device(sglgpu_plan* p) { ck(cudaSetDevice(p->device), "cudaSetDevice"); }
 
 cudaEvent_t pool_event(sglgpu_plan* p) {
+    std::lock_guard<std::mutex> meta(p->meta_mu);
     if (!p->ev_pool.empty()) {
         cudaEvent_t e = p->ev_pool.back();
         p->ev_pool.pop_back();
@@ -302,6 +352,7 @@ int staged(sglgpu_plan* p, int stage, cudaStream_t st, F&& launch) {
     const int k = launch();
     if (p->profiling) {
         ck(cudaEventRecord(b, st), "cudaEventRecord");
+        std::lock_guard<std::mutex> meta(p->meta_mu);
         p->prof.emplace_back(stage, a, b);
     }
     return k;
@@ -404,27 +455,27 @@ int fused_slice_shells(int B, int nb, int lgib) {
     return sls;
 }
 
-int forward_device(sglgpu_plan* p, const double* X, double* C, int nb, cudaStream_t st) {
+int forward_device(sglgpu_plan* p, Work& w, const double* X, double* C, int nb, cudaStream_t st) {
     const int B = p->B;
     const size_t psi2 = 2 * (size_t)sample_count(B), om2 = 2 * (size_t)coefficient_count(B);
     const Slices sl = plan_slices(B, nb);
-    p->S.ensure((size_t)4 * B * B * B * nb);
+    w.S.ensure((size_t)4 * B * B * B * nb);
     int n = 0, k;
     {
         sglk::Geo g{B, 2 * B, nb, 2LL * nb * 2 * B};
         const long long gsize = sglk::g_layout(g);
         const int sls = sl.count == 1 ? fused_slice_shells(B, nb, g.lgib) : 0;
         if (sls > 0) {
-            p->G.ensure(2 * (size_t)gsize);
+            w.G.ensure(2 * (size_t)gsize);
             const int nslices = nb * 2 * B / sls;
-            p->counters.ensure((size_t)(1 + 2 * nslices + 1) / 2 + 1);
+            w.counters.ensure((size_t)(1 + 2 * nslices + 1) / 2 + 1);
             auto lt = tiles_for(p, kLegFwdS, 1, sls, 0, 2 * B);
             const char* dz = std::getenv("SGL_FUSED_DISCARD");
             const char* gr = std::getenv("SGL_FUSED_GRID");
             k = staged(p, 6, st, [&] {
                 return sglk::launch_spherical_forward_fused(
-                    g, X, psi2, p->G.p, p->d_bcal, p->d_tw, p->S.p, sglk::SView{g.NB, 2 * B, 0}, p->d_leg,
-                    p->d_leg_off, lt.first, lt.second, sls, reinterpret_cast<int*>(p->counters.p), dz && dz[0] == '1',
+                    g, X, psi2, w.G.p, p->d_bcal, p->d_tw, w.S.p, sglk::SView{g.NB, 2 * B, 0}, p->d_leg,
+                    p->d_leg_off, lt.first, lt.second, sls, reinterpret_cast<int*>(w.counters.p), dz && dz[0] == '1',
                     gr ? std::atoi(gr) : 0, st);
             });
             if (k != -2) {
@@ -432,7 +483,7 @@ int forward_device(sglgpu_plan* p, const double* X, double* C, int nb, cudaStrea
                 n += k;
                 auto rt = tiles_for(p, kRadFwd, nb, 2 * B, 0, B);
                 k = staged(p, 2, st, [&] {
-                    return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, p->S.p, C, p->d_W, p->d_W_off,
+                    return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, w.S.p, C, p->d_W, p->d_W_off,
                                                        rt.first, rt.second, st);
                 });
                 ck_launch(k, "radial_forward");
@@ -444,20 +495,20 @@ int forward_device(sglgpu_plan* p, const double* X, double* C, int nb, cudaStrea
         // shell slices: az + Legendre per slice into the full S, then radial once
         const int SC = sl.shells;
         sglk::Geo gc{B, SC, 1, 2LL * SC};
-        p->G.ensure(2 * (size_t)sglk::g_layout(gc));
+        w.G.ensure(2 * (size_t)sglk::g_layout(gc));
         const sglk::SView sv{2LL * 2 * B, 2 * B, 0};
         auto lt = tiles_for(p, kLegFwd, 1, SC, 0, 2 * B);
         for (int c = 0; c < sl.count; ++c) {
             const int i0 = c * SC;
             k = staged(p, 0, st, [&] {
-                return sglk::launch_az_forward(gc, X + (size_t)i0 * 2 * 4 * B * B, psi2, p->G.p, p->d_bcal, p->d_tw, st);
+                return sglk::launch_az_forward(gc, X + (size_t)i0 * 2 * 4 * B * B, psi2, w.G.p, p->d_bcal, p->d_tw, st);
             });
             ck_launch(k, "az_forward");
             n += k;
             sglk::SView v = sv;
             v.i0 = i0;
             k = staged(p, 1, st, [&] {
-                return sglk::launch_legendre_forward(gc, v, p->G.p, p->S.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+                return sglk::launch_legendre_forward(gc, v, w.G.p, w.S.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
             });
             ck_launch(k, "legendre_forward");
             n += k;
@@ -465,7 +516,7 @@ int forward_device(sglgpu_plan* p, const double* X, double* C, int nb, cudaStrea
         sglk::Geo g{B, 2 * B, 1, 2LL * 2 * B};
         auto rt = tiles_for(p, kRadFwd, 1, 2 * B, 0, B);
         k = staged(p, 2, st, [&] {
-            return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, p->S.p, C, p->d_W, p->d_W_off,
+            return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, w.S.p, C, p->d_W, p->d_W_off,
                                                rt.first, rt.second, st);
         });
         ck_launch(k, "radial_forward");
@@ -475,22 +526,22 @@ int forward_device(sglgpu_plan* p, const double* X, double* C, int nb, cudaStrea
     for (int f0 = 0; f0 < nb; f0 += sl.functions) {
         const int fb = std::min(sl.functions, nb - f0);
         sglk::Geo g{B, 2 * B, fb, 2LL * fb * 2 * B};
-        p->G.ensure(2 * (size_t)sglk::g_layout(g));
+        w.G.ensure(2 * (size_t)sglk::g_layout(g));
         const sglk::SView sv{g.NB, 2 * B, 0};
         auto lt = tiles_for(p, kLegFwd, fb, 2 * B, 0, 2 * B);
         auto rt = tiles_for(p, kRadFwd, fb, 2 * B, 0, B);
         k = staged(p, 0, st, [&] {
-            return sglk::launch_az_forward(g, X + (size_t)f0 * psi2, psi2, p->G.p, p->d_bcal, p->d_tw, st);
+            return sglk::launch_az_forward(g, X + (size_t)f0 * psi2, psi2, w.G.p, p->d_bcal, p->d_tw, st);
         });
         ck_launch(k, "az_forward");
         n += k;
         k = staged(p, 1, st, [&] {
-            return sglk::launch_legendre_forward(g, sv, p->G.p, p->S.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+            return sglk::launch_legendre_forward(g, sv, w.G.p, w.S.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
         });
         ck_launch(k, "legendre_forward");
         n += k;
         k = staged(p, 2, st, [&] {
-            return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, p->S.p, C + (size_t)f0 * om2,
+            return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, w.S.p, C + (size_t)f0 * om2,
                                                p->d_W, p->d_W_off, rt.first, rt.second, st);
         });
         ck_launch(k, "radial_forward");
@@ -499,35 +550,35 @@ int forward_device(sglgpu_plan* p, const double* X, double* C, int nb, cudaStrea
     return n;
 }
 
-int inverse_device(sglgpu_plan* p, const double* C, double* X, int nb, cudaStream_t st) {
+int inverse_device(sglgpu_plan* p, Work& w, const double* C, double* X, int nb, cudaStream_t st) {
     const int B = p->B;
     const size_t psi2 = 2 * (size_t)sample_count(B), om2 = 2 * (size_t)coefficient_count(B);
     const Slices sl = plan_slices(B, nb);
-    p->S.ensure((size_t)4 * B * B * B * nb);
+    w.S.ensure((size_t)4 * B * B * B * nb);
     int n = 0, k;
     if (nb == 1) {
         sglk::Geo g{B, 2 * B, 1, 2LL * 2 * B};
         auto rt = tiles_for(p, kRadInv, 1, 2 * B, 0, B);
         k = staged(p, 3, st, [&] {
-            return sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, 0}, C, p->S.p, p->d_V, p->d_V_off,
+            return sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, 0}, C, w.S.p, p->d_V, p->d_V_off,
                                                rt.first, rt.second, st);
         });
         ck_launch(k, "radial_inverse");
         n += k;
         const int SC = sl.shells;
         sglk::Geo gc{B, SC, 1, 2LL * SC};
-        p->G.ensure(2 * (size_t)sglk::g_layout(gc));
+        w.G.ensure(2 * (size_t)sglk::g_layout(gc));
         auto lt = tiles_for(p, kLegInv, 1, SC, 0, 2 * B);
         for (int c = 0; c < sl.count; ++c) {
             const int i0 = c * SC;
             const sglk::SView v{2LL * 2 * B, 2 * B, i0};
             k = staged(p, 4, st, [&] {
-                return sglk::launch_legendre_inverse(gc, v, p->S.p, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+                return sglk::launch_legendre_inverse(gc, v, w.S.p, w.G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
             });
             ck_launch(k, "legendre_inverse");
             n += k;
             k = staged(p, 5, st, [&] {
-                return sglk::launch_az_inverse(gc, p->G.p, X + (size_t)i0 * 2 * 4 * B * B, psi2, p->d_tw, st);
+                return sglk::launch_az_inverse(gc, w.G.p, X + (size_t)i0 * 2 * 4 * B * B, psi2, p->d_tw, st);
             });
             ck_launch(k, "az_inverse");
             n += k;
@@ -537,23 +588,23 @@ int inverse_device(sglgpu_plan* p, const double* C, double* X, int nb, cudaStrea
     for (int f0 = 0; f0 < nb; f0 += sl.functions) {
         const int fb = std::min(sl.functions, nb - f0);
         sglk::Geo g{B, 2 * B, fb, 2LL * fb * 2 * B};
-        p->G.ensure(2 * (size_t)sglk::g_layout(g));
+        w.G.ensure(2 * (size_t)sglk::g_layout(g));
         const sglk::SView sv{g.NB, 2 * B, 0};
         auto rt = tiles_for(p, kRadInv, fb, 2 * B, 0, B);
         auto lt = tiles_for(p, kLegInv, fb, 2 * B, 0, 2 * B);
         k = staged(p, 3, st, [&] {
-            return sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, 0}, C + (size_t)f0 * om2, p->S.p,
+            return sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, 0}, C + (size_t)f0 * om2, w.S.p,
                                                p->d_V, p->d_V_off, rt.first, rt.second, st);
         });
         ck_launch(k, "radial_inverse");
         n += k;
         k = staged(p, 4, st, [&] {
-            return sglk::launch_legendre_inverse(g, sv, p->S.p, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+            return sglk::launch_legendre_inverse(g, sv, w.S.p, w.G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
         });
         ck_launch(k, "legendre_inverse");
         n += k;
         k = staged(p, 5, st, [&] {
-            return sglk::launch_az_inverse(g, p->G.p, X + (size_t)f0 * psi2, psi2, p->d_tw, st);
+            return sglk::launch_az_inverse(g, w.G.p, X + (size_t)f0 * psi2, psi2, p->d_tw, st);
         });
         ck_launch(k, "az_inverse");
         n += k;
@@ -567,33 +618,33 @@ void check_plan(const sglgpu_plan* p) {
 
 // Real-valued fast path (samples real, coefficients Hermitian in m): same three
 // stages with only m >= 0 computed; the radial epilogue writes m < 0 by symmetry.
-int real_device(sglgpu_plan* p, const double* in, double* out, int nb, cudaStream_t st, bool forward) {
+int real_device(sglgpu_plan* p, Work& w, const double* in, double* out, int nb, cudaStream_t st, bool forward) {
     const int B = p->B;
     const size_t psi = (size_t)sample_count(B), om2 = 2 * (size_t)coefficient_count(B);
     const Slices sl = plan_slices(B, nb);
-    p->S.ensure((size_t)4 * B * B * B * nb);
+    w.S.ensure((size_t)4 * B * B * B * nb);
     int n = 0, k;
     for (int f0 = 0; f0 < nb; f0 += sl.functions) {
         const int fb = std::min(sl.functions, nb - f0);
         sglk::Geo g{B, 2 * B, fb, 2LL * fb * 2 * B, 1};
-        p->G.ensure(2 * (size_t)sglk::g_layout(g));
+        w.G.ensure(2 * (size_t)sglk::g_layout(g));
         const sglk::SView sv{g.NB, 2 * B, 0};
         if (forward) {
             auto lt = tiles_for(p, kLegFwd, fb, 2 * B, 0, 2 * B, true);
             auto rt = tiles_for(p, kRadFwd, fb, 2 * B, 0, B, true);
             k = staged(p, 0, st, [&] {
-                return sglk::launch_az_forward_real(g, in + (size_t)f0 * psi, psi, p->G.p, p->d_bcal, p->d_tw, st);
+                return sglk::launch_az_forward_real(g, in + (size_t)f0 * psi, psi, w.G.p, p->d_bcal, p->d_tw, st);
             });
             if (k == -2) fail(SGLGPU_EINVAL, "sglgpu real path: 2B must be a power of two >= 4");
             ck_launch(k, "az_forward_real");
             n += k;
             k = staged(p, 1, st, [&] {
-                return sglk::launch_legendre_forward(g, sv, p->G.p, p->S.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+                return sglk::launch_legendre_forward(g, sv, w.G.p, w.S.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
             });
             ck_launch(k, "legendre_forward");
             n += k;
             k = staged(p, 2, st, [&] {
-                return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, p->S.p, out + (size_t)f0 * om2,
+                return sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, w.S.p, out + (size_t)f0 * om2,
                                                    p->d_W, p->d_W_off, rt.first, rt.second, st);
             });
             ck_launch(k, "radial_forward");
@@ -602,18 +653,18 @@ int real_device(sglgpu_plan* p, const double* in, double* out, int nb, cudaStrea
             auto rt = tiles_for(p, kRadInv, fb, 2 * B, 0, B, true);
             auto lt = tiles_for(p, kLegInv, fb, 2 * B, 0, 2 * B, true);
             k = staged(p, 3, st, [&] {
-                return sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, 0}, in + (size_t)f0 * om2, p->S.p,
+                return sglk::launch_radial_inverse(g, sglk::RadialBlocks{2 * B, 0, 0}, in + (size_t)f0 * om2, w.S.p,
                                                    p->d_V, p->d_V_off, rt.first, rt.second, st);
             });
             ck_launch(k, "radial_inverse");
             n += k;
             k = staged(p, 4, st, [&] {
-                return sglk::launch_legendre_inverse(g, sv, p->S.p, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+                return sglk::launch_legendre_inverse(g, sv, w.S.p, w.G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
             });
             ck_launch(k, "legendre_inverse");
             n += k;
             k = staged(p, 5, st, [&] {
-                return sglk::launch_az_inverse_real(g, p->G.p, out + (size_t)f0 * psi, psi, p->d_tw, st);
+                return sglk::launch_az_inverse_real(g, w.G.p, out + (size_t)f0 * psi, psi, p->d_tw, st);
             });
             if (k == -2) fail(SGLGPU_EINVAL, "sglgpu real path: 2B must be a power of two >= 4");
             ck_launch(k, "az_inverse_real");
@@ -621,6 +672,182 @@ int real_device(sglgpu_plan* p, const double* in, double* out, int nb, cudaStrea
         }
     }
     return n;
+}
+
+// ------------------------------------------------------------------ host-memory calls
+// Acquires a free host slot of the plan (creating up to kHostSlots), waiting if
+// all are busy; released by the guard's destructor.
+struct SlotGuard {
+    sglgpu_plan* p;
+    HostSlot* s;
+    explicit SlotGuard(sglgpu_plan* plan) : p(plan), s(nullptr) {
+        std::unique_lock<std::mutex> lock(p->mu);
+        for (;;) {
+            for (auto& sl : p->slots)
+                if (!sl->busy) {
+                    s = sl.get();
+                    break;
+                }
+            if (!s && (int)p->slots.size() < kHostSlots) {
+                p->slots.push_back(std::make_unique<HostSlot>());
+                s = p->slots.back().get();
+            }
+            if (s) break;
+            p->slot_cv.wait(lock);
+        }
+        s->busy = true;
+    }
+    ~SlotGuard() {
+        {
+            std::lock_guard<std::mutex> lock(p->mu);
+            s->busy = false;
+        }
+        p->slot_cv.notify_one();
+    }
+};
+
+void slot_init(HostSlot& s) {
+    if (s.sh) return;
+    for (cudaStream_t* q : {&s.sh, &s.sc, &s.sd}) ck(cudaStreamCreateWithFlags(q, cudaStreamNonBlocking), "stream");
+    for (int b = 0; b < 2; ++b)
+        for (cudaEvent_t* e : {&s.eh[b], &s.ec[b], &s.ed[b], &s.es[b]})
+            ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+}
+
+bool is_pinned(const void* ptr) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// memcpy with a few host threads (pageable <-> pinned staging).
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+    static const unsigned nt = std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2));
+    if (bytes < (4u << 20) || nt == 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t per = (bytes / nt + 4095) & ~(size_t)4095;
+    std::vector<std::thread> ts;
+    for (unsigned t = 1; t < nt && t * per < bytes; ++t)
+        ts.emplace_back([=] {
+            const size_t o = t * per;
+            std::memcpy((char*)dst + o, (const char*)src + o, std::min(per, bytes - o));
+        });
+    std::memcpy(dst, src, std::min(per, bytes));
+    for (auto& t : ts) t.join();
+}
+
+constexpr size_t kStagePiece = (size_t)4 << 20;  // doubles per pinned staging piece (32 MiB)
+
+void ensure_staging(HostSlot& s) {
+    if (s.hst_cap) return;
+    for (int b = 0; b < 2; ++b) ck(cudaMallocHost(&s.hst[b], kStagePiece * sizeof(double)), "cudaMallocHost(staging)");
+    s.hst_cap = kStagePiece;
+}
+
+// H2D of n doubles on stream q: direct from pinned memory, else through the
+// pinned staging pieces (the host copy of piece k+1 overlaps the DMA of piece k).
+void upload(HostSlot& s, double* dst, const double* src, size_t n, bool pinned, cudaStream_t q) {
+    if (pinned) {
+        ck(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, q), "H2D");
+        return;
+    }
+    ensure_staging(s);
+    int k = 0;
+    for (size_t o = 0; o < n; o += kStagePiece, ++k) {
+        const size_t m = std::min(kStagePiece, n - o);
+        const int b = k & 1;
+        if (k >= 2) ck(cudaEventSynchronize(s.es[b]), "staging");  // the DMA of piece k-2 has left hst[b]
+        par_memcpy(s.hst[b], src + o, m * sizeof(double));
+        ck(cudaMemcpyAsync(dst + o, s.hst[b], m * sizeof(double), cudaMemcpyHostToDevice, q), "H2D");
+        ck(cudaEventRecord(s.es[b], q), "event");
+    }
+}
+
+// D2H of n doubles on stream q (after what q already waits for); pinned: async,
+// else through the staging pieces (DMA of piece k+1 overlaps the host copy of k)
+// and synchronous.
+void download(HostSlot& s, double* dst, const double* src, size_t n, bool pinned, cudaStream_t q) {
+    if (pinned) {
+        ck(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, q), "D2H");
+        return;
+    }
+    ensure_staging(s);
+    const size_t pieces = (n + kStagePiece - 1) / kStagePiece;
+    auto issue = [&](size_t k) {
+        const size_t o = k * kStagePiece, m = std::min(kStagePiece, n - o);
+        ck(cudaMemcpyAsync(s.hst[k & 1], src + o, m * sizeof(double), cudaMemcpyDeviceToHost, q), "D2H");
+        ck(cudaEventRecord(s.es[k & 1], q), "event");
+    };
+    if (pieces) issue(0);
+    for (size_t k = 0; k < pieces; ++k) {
+        if (k + 1 < pieces) issue(k + 1);  // hst[(k+1)&1] was emptied by the host copy of piece k-1
+        ck(cudaEventSynchronize(s.es[k & 1]), "D2H");
+        const size_t o = k * kStagePiece, m = std::min(kStagePiece, n - o);
+        par_memcpy(dst + o, s.hst[k & 1], m * sizeof(double));
+    }
+}
+
+// A host-memory transform of `batch` functions through one slot: chunks of
+// `chunk` functions, H2D (stream sh) -> compute (sc) -> D2H (sd), double-buffered
+// so that consecutive chunks overlap.  compute(work, d_in, d_out, nb, stream)
+// enqueues the kernels and returns their count.  Returns after the result is in
+// host memory.
+template <class Compute>
+int host_pipeline(sglgpu_plan* p, const double* in, double* out, size_t batch, size_t in_len, size_t out_len,
+                  size_t chunk, void* user_stream, Compute&& compute) {
+    SlotGuard guard(p);
+    HostSlot& s = *guard.s;
+    set_device(p);
+    slot_init(s);
+    if (user_stream) {  // order after the caller's earlier work on its stream
+        ck(cudaEventRecord(s.ed[0], static_cast<cudaStream_t>(user_stream)), "event");
+        ck(cudaStreamWaitEvent(s.sh, s.ed[0], 0), "wait");
+    }
+    const bool pin_in = is_pinned(in), pin_out = is_pinned(out);
+    const size_t nchunks = (batch + chunk - 1) / chunk;
+    const size_t cap_in = in_len * std::min(chunk, batch), cap_out = out_len * std::min(chunk, batch);
+    const int nbuf = nchunks > 1 ? 2 : 1;
+    for (int b = 0; b < nbuf; ++b) {
+        s.din[b].ensure(cap_in);
+        s.dout[b].ensure(cap_out);
+    }
+    int launches = 0;
+    auto h2d = [&](size_t c) {
+        const int b = (int)(c & 1);
+        const size_t b0 = c * chunk, nb = std::min(chunk, batch - b0);
+        if (c >= 2) ck(cudaStreamWaitEvent(s.sh, s.ec[b], 0), "wait");  // din[b] consumed by chunk c-2
+        upload(s, s.din[b].p, in + b0 * in_len, nb * in_len, pin_in, s.sh);
+        ck(cudaEventRecord(s.eh[b], s.sh), "event");
+    };
+    h2d(0);
+    for (size_t c = 0; c < nchunks; ++c) {
+        const int b = (int)(c & 1);
+        const size_t b0 = c * chunk, nb = std::min(chunk, batch - b0);
+        ck(cudaStreamWaitEvent(s.sc, s.eh[b], 0), "wait");
+        if (c >= 2) ck(cudaStreamWaitEvent(s.sc, s.ed[b], 0), "wait");  // dout[b] drained by chunk c-2
+        launches += compute(s.w, s.din[b].p, s.dout[b].p, (int)nb, s.sc);
+        ck(cudaEventRecord(s.ec[b], s.sc), "event");
+        if (c + 1 < nchunks) h2d(c + 1);
+        ck(cudaStreamWaitEvent(s.sd, s.ec[b], 0), "wait");
+        download(s, out + b0 * out_len, s.dout[b].p, nb * out_len, pin_out, s.sd);
+        ck(cudaEventRecord(s.ed[b], s.sd), "event");
+    }
+    ck(cudaStreamSynchronize(s.sd), "cudaStreamSynchronize");
+    return launches;
+}
+
+// Functions per pipelined chunk of a host call: about four chunks per call (so
+// transfers overlap compute), at least ~64 MB of samples per chunk, within the
+// workspace budget (batch_chunk).
+size_t host_chunk(int B, size_t batch) {
+    const size_t cap = batch_chunk(B, batch);
+    const size_t min_fn = std::max<size_t>(1, ((size_t)64 << 20) / ((size_t)128 * B * B * B));
+    return std::max<size_t>(1, std::min(cap, std::max(min_fn, (batch + 3) / 4)));
 }
 
 int run_real(sglgpu_plan* p, const double* in, double* out, size_t batch, int mem_kind, void* stream, bool forward) {
@@ -633,31 +860,23 @@ int run_real(sglgpu_plan* p, const double* in, double* out, size_t batch, int me
         const int B = p->B;
         if (B < 2 || ((2 * B) & (2 * B - 1)) != 0)
             fail(SGLGPU_EINVAL, "sglgpu real path: 2B must be a power of two >= 4");
-        std::lock_guard<std::mutex> lock(p->mu);
-        set_device(p);
-        cudaStream_t st = static_cast<cudaStream_t>(stream);
         const size_t psi = (size_t)sample_count(B), om = 2 * (size_t)coefficient_count(B);
         const size_t in_len = forward ? psi : om, out_len = forward ? om : psi;
-        const size_t chunk = batch_chunk(B, batch);
         int launches = 0;
         if (mem_kind == SGLGPU_MEM_DEVICE) {
+            std::lock_guard<std::mutex> lock(p->mu);
+            set_device(p);
+            cudaStream_t st = static_cast<cudaStream_t>(stream);
+            const size_t chunk = batch_chunk(B, batch);
             for (size_t b0 = 0; b0 < batch; b0 += chunk) {
                 const int nb = (int)std::min(chunk, batch - b0);
-                launches += real_device(p, in + b0 * in_len, out + b0 * out_len, nb, st, forward);
+                launches += real_device(p, p->main, in + b0 * in_len, out + b0 * out_len, nb, st, forward);
             }
         } else {
-            p->in.ensure(in_len * chunk);
-            p->out.ensure(out_len * chunk);
-            for (size_t b0 = 0; b0 < batch; b0 += chunk) {
-                const int nb = (int)std::min(chunk, batch - b0);
-                ck(cudaMemcpyAsync(p->in.p, in + b0 * in_len, nb * in_len * sizeof(double), cudaMemcpyHostToDevice, st),
-                   "H2D");
-                launches += real_device(p, p->in.p, p->out.p, nb, st, forward);
-                ck(cudaMemcpyAsync(out + b0 * out_len, p->out.p, nb * out_len * sizeof(double), cudaMemcpyDeviceToHost,
-                                   st),
-                   "D2H");
-            }
-            ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+            launches = host_pipeline(p, in, out, batch, in_len, out_len, host_chunk(B, batch), stream,
+                                     [&](Work& w, const double* di, double* dout, int nb, cudaStream_t q) {
+                                         return real_device(p, w, di, dout, nb, q, forward);
+                                     });
         }
         p->last_launches = launches;
     });
@@ -678,37 +897,31 @@ int run_separated(sglgpu_plan* p, const double* in, double* out, size_t batch, i
         if (!naive && B > 64)
             fail(SGLGPU_EINVAL, "sglgpu separated transform: bandlimit must be <= 64 (reference validity)");
         if (naive && B > 32) fail(SGLGPU_EINVAL, "sglgpu naive transform: bandlimit must be <= 32 (O(B^7))");
-        std::lock_guard<std::mutex> lock(p->mu);
-        set_device(p);
-        cudaStream_t st = static_cast<cudaStream_t>(stream);
         const size_t psi = 2 * (size_t)sample_count(B), om = 2 * (size_t)coefficient_count(B);
         const size_t in_len = forward ? psi : om, out_len = forward ? om : psi;
         const size_t chunk = std::max<size_t>(1, std::min<size_t>(batch, 64));
-        p->S.ensure((size_t)4 * B * B * B * chunk);
-        int launches = 0;
-        for (size_t b0 = 0; b0 < batch; b0 += chunk) {
-            const int nb = (int)std::min(chunk, batch - b0);
-            const double* src = in + b0 * in_len;
-            double* dst = out + b0 * out_len;
-            if (mem_kind == SGLGPU_MEM_HOST) {
-                p->in.ensure(in_len * chunk);
-                p->out.ensure(out_len * chunk);
-                ck(cudaMemcpyAsync(p->in.p, src, nb * in_len * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
-                src = p->in.p;
-            }
-            double* d_dst = mem_kind == SGLGPU_MEM_HOST ? p->out.p : dst;
-            const int k = naive ? (forward ? sglk::launch_naive_forward(B, nb, src, d_dst, p->d_r, p->d_amod,
+        auto compute = [&](Work& w, const double* src, double* dst, int nb, cudaStream_t st) {
+            w.S.ensure((size_t)4 * B * B * B * nb);
+            const int k = naive ? (forward ? sglk::launch_naive_forward(B, nb, src, dst, p->d_r, p->d_amod,
                                                                         p->d_bcal, st)
-                                           : sglk::launch_naive_inverse(B, nb, src, d_dst, p->d_r, st))
-                        : forward ? sglk::launch_separated_forward(B, nb, src, d_dst, p->S.p, p->d_r, p->d_amod,
+                                           : sglk::launch_naive_inverse(B, nb, src, dst, p->d_r, st))
+                        : forward ? sglk::launch_separated_forward(B, nb, src, dst, w.S.p, p->d_r, p->d_amod,
                                                                    p->d_bcal, st)
-                                  : sglk::launch_separated_inverse(B, nb, src, d_dst, p->S.p, p->d_r, st);
+                                  : sglk::launch_separated_inverse(B, nb, src, dst, w.S.p, p->d_r, st);
             ck_launch(k, naive ? "naive transform" : forward ? "separated_forward" : "separated_inverse");
-            launches += k;
-            if (mem_kind == SGLGPU_MEM_HOST)
-                ck(cudaMemcpyAsync(dst, p->out.p, nb * out_len * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+            return k;
+        };
+        int launches = 0;
+        if (mem_kind == SGLGPU_MEM_HOST) {
+            launches = host_pipeline(p, in, out, batch, in_len, out_len, chunk, stream, compute);
+        } else {
+            std::lock_guard<std::mutex> lock(p->mu);
+            set_device(p);
+            for (size_t b0 = 0; b0 < batch; b0 += chunk) {
+                const int nb = (int)std::min(chunk, batch - b0);
+                launches += compute(p->main, in + b0 * in_len, out + b0 * out_len, nb, static_cast<cudaStream_t>(stream));
+            }
         }
-        if (mem_kind == SGLGPU_MEM_HOST) ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
         p->last_launches = launches;
     });
 }
@@ -721,10 +934,19 @@ int run(sglgpu_plan* p, const double* in, double* out, size_t batch, int mem_kin
             fail(SGLGPU_EINVAL, "sglgpu: unknown mem_kind");
         if (batch == 0) return;
         if (!in || !out) fail(SGLGPU_EINVAL, "sglgpu: null data pointer");
+        const int B = p->B;
+        if (mem_kind == SGLGPU_MEM_HOST) {
+            const size_t psi = 2 * (size_t)sample_count(B), om = 2 * (size_t)coefficient_count(B);
+            p->last_launches = host_pipeline(
+                p, in, out, batch, forward ? psi : om, forward ? om : psi, host_chunk(B, batch), stream,
+                [&](Work& w, const double* di, double* dout, int nb, cudaStream_t q) {
+                    return forward ? forward_device(p, w, di, dout, nb, q) : inverse_device(p, w, di, dout, nb, q);
+                });
+            return;
+        }
         std::lock_guard<std::mutex> lock(p->mu);
         set_device(p);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
-        const int B = p->B;
         const size_t psi = 2 * (size_t)sample_count(B), om = 2 * (size_t)coefficient_count(B);
         const size_t in_len = forward ? psi : om, out_len = forward ? om : psi;
         const size_t chunk = batch_chunk(B, batch);
@@ -733,8 +955,8 @@ int run(sglgpu_plan* p, const double* in, double* out, size_t batch, int mem_kin
             int n = 0;
             for (size_t b0 = 0; b0 < batch; b0 += chunk) {
                 const int nb = (int)std::min(chunk, batch - b0);
-                n += forward ? forward_device(p, in + b0 * in_len, out + b0 * out_len, nb, st)
-                             : inverse_device(p, in + b0 * in_len, out + b0 * out_len, nb, st);
+                n += forward ? forward_device(p, p->main, in + b0 * in_len, out + b0 * out_len, nb, st)
+                             : inverse_device(p, p->main, in + b0 * in_len, out + b0 * out_len, nb, st);
             }
             return n;
         };
@@ -745,7 +967,7 @@ int run(sglgpu_plan* p, const double* in, double* out, size_t batch, int mem_kin
             // profiling (per-stage events) and only for streams other than the
             // legacy default stream.
             const auto key = std::make_tuple(forward ? 1 : 0, batch, (const void*)in, (void*)out, (void*)st,
-                                             (void*)p->G.p, (void*)p->S.p);
+                                             (void*)p->main.G.p, (void*)p->main.S.p);
             auto git = p->graphs.find(key);
             if (git != p->graphs.end() && !p->profiling) {
                 ck(cudaGraphLaunch(git->second.exec, st), "cudaGraphLaunch");
@@ -780,21 +1002,6 @@ int run(sglgpu_plan* p, const double* in, double* out, size_t batch, int mem_kin
             } else {
                 launches = body();
             }
-        } else {
-            p->in.ensure(in_len * chunk);
-            p->out.ensure(out_len * chunk);
-            for (size_t b0 = 0; b0 < batch; b0 += chunk) {
-                const int nb = (int)std::min(chunk, batch - b0);
-                ck(cudaMemcpyAsync(p->in.p, in + b0 * in_len, nb * in_len * sizeof(double),
-                                   cudaMemcpyHostToDevice, st),
-                   "H2D");
-                launches += forward ? forward_device(p, p->in.p, p->out.p, nb, st)
-                                    : inverse_device(p, p->in.p, p->out.p, nb, st);
-                ck(cudaMemcpyAsync(out + b0 * out_len, p->out.p, nb * out_len * sizeof(double),
-                                   cudaMemcpyDeviceToHost, st),
-                   "D2H");
-            }
-            ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
         }
         p->last_launches = launches;
     });
@@ -870,10 +1077,8 @@ int sglgpu_plan_destroy(sglgpu_plan* p) {
     }
     for (auto e : p->ev_pool) cudaEventDestroy(e);
     for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second.exec);
-    p->G.release();
-    p->S.release();
-    p->in.release();
-    p->out.release();
+    p->main.release();
+    for (auto& sl : p->slots) sl->release();
     delete p;
     return SGLGPU_OK;
 }
@@ -882,7 +1087,7 @@ int sglgpu_plan_bandlimit(const sglgpu_plan* p) { return p ? p->B : 0; }
 
 size_t sglgpu_plan_table_bytes(const sglgpu_plan* p) { return p ? p->table_bytes : 0; }
 
-int sglgpu_last_launch_count(const sglgpu_plan* p) { return p ? p->last_launches : 0; }
+int sglgpu_last_launch_count(const sglgpu_plan* p) { return p ? p->last_launches.load() : 0; }
 
 int sglgpu_profile_begin(sglgpu_plan* p) {
     return guarded([&] {
@@ -954,21 +1159,26 @@ int sglgpu_sample_basis(sglgpu_plan* p, int n, int l, int m, double* samples, in
         if (mem_kind != SGLGPU_MEM_HOST && mem_kind != SGLGPU_MEM_DEVICE)
             fail(SGLGPU_EINVAL, "sglgpu: unknown mem_kind");
         if (!samples) fail(SGLGPU_EINVAL, "sglgpu: null data pointer");
+        const size_t len = 2 * (size_t)sample_count(B);
+        if (mem_kind == SGLGPU_MEM_HOST) {
+            SlotGuard guard(p);
+            HostSlot& s = *guard.s;
+            set_device(p);
+            slot_init(s);
+            s.dout[0].ensure(len);
+            const int k = sglk::launch_sample_basis(B, n, l, m, s.dout[0].p, p->d_r, s.sc);
+            ck_launch(k, "sample_basis");
+            ck(cudaEventRecord(s.ec[0], s.sc), "event");
+            ck(cudaStreamWaitEvent(s.sd, s.ec[0], 0), "wait");
+            download(s, samples, s.dout[0].p, len, is_pinned(samples), s.sd);
+            ck(cudaStreamSynchronize(s.sd), "cudaStreamSynchronize");
+            p->last_launches = k;
+            return;
+        }
         std::lock_guard<std::mutex> lock(p->mu);
         set_device(p);
-        cudaStream_t st = static_cast<cudaStream_t>(stream);
-        const size_t len = 2 * (size_t)sample_count(B);
-        double* dst = samples;
-        if (mem_kind == SGLGPU_MEM_HOST) {
-            p->out.ensure(len);
-            dst = p->out.p;
-        }
-        const int k = sglk::launch_sample_basis(B, n, l, m, dst, p->d_r, st);
+        const int k = sglk::launch_sample_basis(B, n, l, m, samples, p->d_r, static_cast<cudaStream_t>(stream));
         ck_launch(k, "sample_basis");
-        if (mem_kind == SGLGPU_MEM_HOST) {
-            ck(cudaMemcpyAsync(samples, dst, len * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
-            ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
-        }
         p->last_launches = k;
     });
 }
@@ -997,12 +1207,12 @@ int sglgpu_spherical_forward(sglgpu_plan* p, const double* samples, size_t sampl
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         const int nb = (int)batch;
         sglk::Geo g{B, shell_count, nb, 2LL * nb * shell_count};
-        p->G.ensure(2 * (size_t)sglk::g_layout(g));
-        int n = sglk::launch_az_forward(g, samples, 2 * sample_stride, p->G.p, p->d_bcal, p->d_tw, st);
+        p->main.G.ensure(2 * (size_t)sglk::g_layout(g));
+        int n = sglk::launch_az_forward(g, samples, 2 * sample_stride, p->main.G.p, p->d_bcal, p->d_tw, st);
         ck_launch(n, "az_forward");
         auto lt = tiles_for(p, kLegFwd, nb, shell_count, 0, 2 * B);
         const sglk::SView sv{g.NB, shell_count, 0};
-        int k = sglk::launch_legendre_forward(g, sv, p->G.p, shells, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+        int k = sglk::launch_legendre_forward(g, sv, p->main.G.p, shells, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
         ck_launch(k, "legendre_forward");
         p->last_launches = n + k;
     });
@@ -1022,12 +1232,12 @@ int sglgpu_spherical_inverse(sglgpu_plan* p, const double* shells, double* sampl
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         const int nb = (int)batch;
         sglk::Geo g{B, shell_count, nb, 2LL * nb * shell_count};
-        p->G.ensure(2 * (size_t)sglk::g_layout(g));
+        p->main.G.ensure(2 * (size_t)sglk::g_layout(g));
         auto lt = tiles_for(p, kLegInv, nb, shell_count, 0, 2 * B);
         const sglk::SView sv{g.NB, shell_count, 0};
-        int k = sglk::launch_legendre_inverse(g, sv, shells, p->G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+        int k = sglk::launch_legendre_inverse(g, sv, shells, p->main.G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
         ck_launch(k, "legendre_inverse");
-        int n = sglk::launch_az_inverse(g, p->G.p, samples, 2 * sample_stride, p->d_tw, st);
+        int n = sglk::launch_az_inverse(g, p->main.G.p, samples, 2 * sample_stride, p->d_tw, st);
         ck_launch(n, "az_inverse");
         p->last_launches = n + k;
     });
@@ -1103,8 +1313,8 @@ int sglgpu_spherical_forward_to(sglgpu_plan* p, const double* samples, size_t sa
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         const int nb = (int)batch;
         sglk::Geo g{B, shell_count, nb, 2LL * nb * shell_count};
-        p->G.ensure(2 * (size_t)sglk::g_layout(g));
-        int n = sglk::launch_az_forward(g, samples, 2 * sample_stride, p->G.p, p->d_bcal, p->d_tw, st);
+        p->main.G.ensure(2 * (size_t)sglk::g_layout(g));
+        int n = sglk::launch_az_forward(g, samples, 2 * sample_stride, p->main.G.p, p->d_bcal, p->d_tw, st);
         ck_launch(n, "az_forward");
         sglk::PeerDest pd;
         pd.n = ndst;
@@ -1116,7 +1326,7 @@ int sglgpu_spherical_forward_to(sglgpu_plan* p, const double* samples, size_t sa
         pd.bound[ndst] = l_bounds[ndst];
         auto lt = tiles_for(p, kLegFwd, nb, shell_count, 0, 2 * B);
         const sglk::SView sv{g.NB, shell_count, 0};
-        int k = sglk::launch_legendre_forward_peers(g, sv, p->G.p, pd, p->d_leg, p->d_leg_off, lt.first, lt.second,
+        int k = sglk::launch_legendre_forward_peers(g, sv, p->main.G.p, pd, p->d_leg, p->d_leg_off, lt.first, lt.second,
                                                     st);
         ck_launch(k, "legendre_forward");
         p->last_launches = n + k;
