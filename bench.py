@@ -317,9 +317,10 @@ def main():
     ap.add_argument("--e2e-callers", type=int, default=2,
                     help="host threads issuing the e2e round trips concurrently (PCIe full duplex)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mode", default="split", choices=["split", "replicas"],
-                    help="N>1: split one transform by shells / (l, m) (strong scaling, default) "
-                         "or run independent replicas (weak scaling)")
+    ap.add_argument("--mode", default="auto", choices=["auto", "split", "replicas"],
+                    help="N>1: split one transform by shells / (l, m) (strong scaling; BASELINE configs C3/C4) "
+                         "or shard the batch as independent replicas (weak scaling; C2/C5); auto: split for one "
+                         "function per step, replicas for batches")
     ap.add_argument("--force-split", action="store_true", help="run the split path even at N=1 (testing)")
     ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
                     help="split mode: stage exchange fused into the kernels (NVLink peer stores) or NCCL all-to-all")
@@ -333,6 +334,11 @@ def main():
     if args.impl == "reference":
         reference_arm(args, rank, world)
         return
+    if args.mode == "auto":
+        args.mode = "split" if args.batch == 1 and not args.real else "replicas"
+    if world > 1:
+        # keep NCCL's communicator log on (rank count, transport: NVLink / NVLS) for the driver
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     if (world > 1 and args.mode == "split") or args.force_split:
         split_arm(args, rank, world, local)
         return
@@ -660,17 +666,94 @@ def split_arm(args, rank, world, local):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
     whole = 2 * wl.f_fwd(B) * nb / (ms * 1e-3) / 1e12
+
+    # ---- exchange accounting (this rank): bytes it sends to peers per step and
+    # the device time of the phases that carry them (a second pass of the same
+    # steps with CUDA events between the phases; max over ranks)
+    import paper_1604_05140_b200.distributed as D
+
+    s0r, _ = part.shell_range(rank)
+    nu0, nu1 = part.nu_range(rank)
+    row = 16 * nb * sc  # bytes of one nu row of this rank's shells
+    s_bytes = sum((part.nu_range(q)[1] - part.nu_range(q)[0]) * row for q in range(world) if q != rank)
+    l0r, l1r = part.l_ranges[rank]
+    omega_r = sum((2 * l + 1) * (B - l) for l in range(l0r, l1r))  # this rank's coefficients
+    exch = {"forward_shell_rows_bytes": s_bytes, "inverse_shell_rows_bytes": s_bytes}
+    if exchange == "fused":
+        exch["forward_coefficients_bytes"] = 16 * nb * omega_r * (world - 1)  # peer stores of its degrees
+    else:
+        exch["forward_coefficients_bytes"] = 16 * nb * Om  # all_reduce payload
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+    phase = np.zeros(6)
+    dist.barrier()
+    for s_ in range(args.steps):
+        c = cin[s_ % nrot]
+        evs[0].record(stream)
+        if exchange == "fused":
+            D.fused_inverse_radial(c, part, st, peers, rank)                    # radial inv + peer stores
+            evs[1].record(stream)
+            D._stream_barrier(dist, None, c.device)
+            evs[2].record(stream)
+            loc = D.fused_inverse_spherical(part, st, peers, rank, c.device)
+            D._stream_barrier(dist, None, c.device)
+            evs[3].record(stream)
+            D.fused_forward_spherical(loc.view(nb, -1), part, st, peers, rank, nb)  # spherical fwd + peer stores
+            evs[4].record(stream)
+            D._stream_barrier(dist, None, c.device)
+            evs[5].record(stream)
+            if world > 1:
+                D.fused_forward_radial_bcast(part, st, peers, rank, stream.cuda_stream)
+                D._stream_barrier(dist, None, c.device)
+            else:
+                co = torch.zeros((nb, Om), dtype=torch.complex128, device="cuda")
+                D.fused_forward_radial(part, st, peers, rank, co)
+            evs[6].record(stream)
+        else:
+            l0, l1 = part.l_ranges[rank]
+            blocks = st.radial_inverse(c, l0, l1, sc, nb) if l1 > l0 else torch.empty(0, dtype=torch.complex128,
+                                                                                       device="cuda")
+            evs[1].record(stream)
+            recv = [(part.nu_range(q)[1] - part.nu_range(q)[0]) * nb * sc for q in range(world)]
+            S_loc = D._a2a(dist, None, blocks, [(nu1 - nu0) * nb * sc] * world, recv)
+            evs[2].record(stream)
+            loc = st.spherical_inverse(S_loc, s0r, sc, nb)
+            S_f = st.spherical_forward(loc.view(nb, -1), s0r, sc, nb)
+            evs[3].record(stream)
+            blk = D._a2a(dist, None, S_f, recv, [(nu1 - nu0) * nb * sc] * world)
+            evs[4].record(stream)
+            co = torch.zeros((nb, Om), dtype=torch.complex128, device="cuda")
+            if l1 > l0:
+                st.radial_forward(blk, l0, l1, sc, nb, co)
+            evs[5].record(stream)
+            dist.all_reduce(torch.view_as_real(co))
+            evs[6].record(stream)
+        torch.cuda.synchronize()
+        for i in range(6):
+            phase[i] += evs[i].elapsed_time(evs[i + 1])
+    phase /= args.steps
+    tph = torch.tensor(phase, device="cuda", dtype=torch.float64)
+    dist.all_reduce(tph, op=dist.ReduceOp.MAX)
+    phase = tph.cpu().numpy()
+    names = (["radial_inverse+peer_stores", "barrier", "spherical_inverse(+barrier)", "spherical_forward+peer_stores",
+              "barrier", "radial_forward+coefficient_peer_stores(+barrier)"] if exchange == "fused" else
+             ["radial_inverse", "all_to_all(shells)", "spherical_inverse+spherical_forward", "all_to_all(shells)",
+              "radial_forward", "all_reduce(coefficients)"])
+    exch["phase_ms_max_over_ranks"] = {n: round(float(v), 5) for n, v in zip(names, phase)}
+    exch["phase_sum_ms"] = round(float(phase.sum()), 5)
+
     line = {
         "metric": f"fwd+inv SGL transforms/s at B={B} fp64", "value": value, "unit": "transforms/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: iid complex normal coefficients (numpy PCG64, seed 0)",
-        "config": {"workload": f"C3: B={B}, {nb} function(s) per step split over {world} GPUs "
-                               "(shells / degree ranges, " + ("exchange fused into the stage epilogues: NVLink "
-                               "peer stores" if exchange == "fused" else "NCCL all-to-all") + ")",
-                   "exchange": exchange + (f" ({why})" if why else ""),
-                   "B": B, "batch": nb, "parallelism": f"shell/(l,m) split x{world}",
-                   "l2": f"inputs rotated over {nrot} buffers; per-step grid {16 * Ps * nb / 2**20:.0f} MiB > L2"},
+        "config": workload_config(B, nb, False),
+        "setup": {"split": f"{nb} function(s) per step split over {world} GPUs (shells / degree ranges, " +
+                           ("exchange fused into the stage epilogues: NVLink peer stores" if exchange == "fused"
+                            else "NCCL all-to-all") + ")",
+                  "exchange": exchange + (f" ({why})" if why else ""),
+                  "parallelism": f"shell/(l,m) split x{world}",
+                  "l2": f"inputs rotated over {nrot} buffers; per-step grid {16 * Ps * nb / 2**20:.0f} MiB > L2"},
+        "exchange": exch,
         "e2e": {"value": nb / (e2e_ms / 1000.0), "unit": "transforms/s",
                 "h2d_bytes_per_step": 16 * (Om + sc * 4 * B * B) * nb,
                 "d2h_bytes_per_step": 16 * (sc * 4 * B * B + Om) * nb, "ms_per_step": e2e_ms,
