@@ -1114,6 +1114,9 @@ struct LegFwdPeers : LegFwd {
 struct LegFwdTma : LegFwd {
     static constexpr bool B_TMA = true;
     static constexpr int GEMM_MAXWM = 1;
+    // 5 CTAs / SM (96 registers, no spills; the cp.async-fed LegFwd would spill):
+    // 94.9 -> 92.0 us at B = 128 (round 2)
+    static constexpr int GEMM_MINB = SGL_MINB_LEGFWD > 0 ? SGL_MINB_LEGFWD : 5;
     alignas(64) CUtensorMap tmap;  // G viewed as [p][bin][group][j'][8 doubles]
 };
 // ... and its multi-GPU form (S rows to their owners' receive buffers).
@@ -1764,7 +1767,12 @@ int launch_az_inverse(const Geo& g, const double* G, double* samples, size_t sam
 template <class P>
 static int gemm_launch(const P& p, const TileMap* tiles, int ntiles, cudaStream_t s) {
     if (ntiles <= 0) return 0;
-    constexpr size_t smem = gemm_smem_bytes<P>();
+    // SGL_GEMM_SMEM_PAD: extra dynamic shared memory per CTA (occupancy experiments)
+    static const size_t pad = [] {
+        const char* e = std::getenv("SGL_GEMM_SMEM_PAD");
+        return e ? (size_t)std::atol(e) : (size_t)0;
+    }();
+    const size_t smem = gemm_smem_bytes<P>() + pad;
     static SmemAttrOnce attr;
     attr.ensure(gemm_dmma_kernel<P>, smem);
     gemm_dmma_kernel<P><<<ntiles, 128, smem, s>>>(p, *tiles);
