@@ -1,0 +1,7 @@
+#!/bin/bash
+timeout 300 python exp/i8_check.py 8 16 64 128 256 || exit 1
+for B in 128 256 64; do
+  echo "== B=$B"
+  B=$B SGL_I8=0 timeout 120 python exp/stage_time.py
+  for tpc in ${TPCS:-2 4 8}; do echo "tpc=$tpc"; B=$B SGL_I8=leginv SGL_I8_TPC=$tpc timeout 120 python exp/stage_time.py; done
+done

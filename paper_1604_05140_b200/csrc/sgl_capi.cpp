@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "sgl_kernels.cuh"
+#include "sgl_ozaki.cuh"
 #include "sgl_tables.hpp"
 
 namespace {
@@ -154,6 +155,15 @@ struct sglgpu_plan {
     long long* d_V_off = nullptr;
     double* d_r = nullptr;     // radial rule (separated cross-oracle only)
     double* d_amod = nullptr;
+    // INT8 tensor-core (fixed-point slice) tables, sgl_ozaki.cuh
+    struct OzTable {
+        uint8_t* img = nullptr;
+        long long* off = nullptr;
+        int* rexp = nullptr;
+        int* kpad = nullptr;
+        int mtiles = 1;
+    } oz_li;
+    std::map<std::tuple<long long, int, int>, std::pair<sglk::oz::Unit*, int>> oz_units;
     Work main;  // workspaces of device-memory calls and the stage entry points (under mu)
     std::vector<std::unique_ptr<HostSlot>> slots;  // host-memory calls (acquired under mu)
     std::condition_variable slot_cv;
@@ -324,6 +334,48 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
     const auto res = std::make_pair(tm, (int)n);
     p->tiles[key] = res;
     return res;
+}
+
+// INT8 tensor-core contractions (sgl_ozaki.cu): SGL_I8 = 0 (off), 1 (every kind
+// built so far) or a comma list of kinds ("leginv").
+bool i8_on(const char* kind) {
+    const char* e = std::getenv("SGL_I8");
+    if (!e) return false;
+    if (e[0] == '0' && e[1] == 0) return false;
+    if (e[0] == '1' && e[1] == 0) return true;
+    return std::strstr(e, kind) != nullptr;
+}
+
+int i8_tpc() {
+    const char* e = std::getenv("SGL_I8_TPC");
+    return e ? std::max(1, std::atoi(e)) : 4;
+}
+
+// Legendre inverse: the INT8 tensor-core kernel when enabled, else the DMMA GEMM.
+int leginv(sglgpu_plan* p, const sglk::Geo& g, const sglk::SView& sv, const double* S, double* G,
+           std::pair<sglk::TileMap*, int> lt, cudaStream_t st) {
+    if (p->oz_li.img && i8_on("leginv")) {
+        const int tpc = i8_tpc();
+        std::pair<sglk::oz::Unit*, int> un;
+        {
+            std::lock_guard<std::mutex> meta(p->meta_mu);
+            const auto key = std::make_tuple(g.NB, g.real, tpc);
+            auto it = p->oz_units.find(key);
+            if (it == p->oz_units.end()) {
+                const auto hu = sglk::oz::leginv_units(p->B, g.NB, g.real != 0, tpc);
+                sglk::oz::Unit* d = nullptr;
+                ck(cudaMalloc(&d, std::max<size_t>(1, hu.size()) * sizeof(sglk::oz::Unit)), "cudaMalloc(units)");
+                ck(cudaMemcpy(d, hu.data(), hu.size() * sizeof(sglk::oz::Unit), cudaMemcpyHostToDevice), "upload units");
+                it = p->oz_units.emplace(key, std::make_pair(d, (int)hu.size())).first;
+            }
+            un = it->second;
+        }
+        sglk::oz::LegInvI8 prm{g, sv, S, G, p->oz_li.img, p->oz_li.off, p->oz_li.rexp, p->oz_li.kpad, un.first, tpc,
+                               p->oz_li.mtiles};
+        if (const char* tr = std::getenv("SGL_I8_TRACE")) prm.trace = reinterpret_cast<long long*>(std::strtoull(tr, nullptr, 0));
+        return sglk::oz::launch_legendre_inverse_i8(prm, un.second, st);
+    }
+    return sglk::launch_legendre_inverse(g, sv, S, G, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
 }
 
 void set_device(sglgpu_plan* p) { ck(cudaSetDevice(p->device), "cudaSetDevice"); }
@@ -573,7 +625,7 @@ int inverse_device(sglgpu_plan* p, Work& w, const double* C, double* X, int nb, 
             const int i0 = c * SC;
             const sglk::SView v{2LL * 2 * B, 2 * B, i0};
             k = staged(p, 4, st, [&] {
-                return sglk::launch_legendre_inverse(gc, v, w.S.p, w.G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+                return leginv(p, gc, v, w.S.p, w.G.p, lt, st);
             });
             ck_launch(k, "legendre_inverse");
             n += k;
@@ -599,7 +651,7 @@ int inverse_device(sglgpu_plan* p, Work& w, const double* C, double* X, int nb, 
         ck_launch(k, "radial_inverse");
         n += k;
         k = staged(p, 4, st, [&] {
-            return sglk::launch_legendre_inverse(g, sv, w.S.p, w.G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+            return leginv(p, g, sv, w.S.p, w.G.p, lt, st);
         });
         ck_launch(k, "legendre_inverse");
         n += k;
@@ -659,7 +711,7 @@ int real_device(sglgpu_plan* p, Work& w, const double* in, double* out, int nb, 
             ck_launch(k, "radial_inverse");
             n += k;
             k = staged(p, 4, st, [&] {
-                return sglk::launch_legendre_inverse(g, sv, w.S.p, w.G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+                return leginv(p, g, sv, w.S.p, w.G.p, lt, st);
             });
             ck_launch(k, "legendre_inverse");
             n += k;
@@ -1051,6 +1103,14 @@ int sglgpu_plan_create(const sglgpu_plan_desc* desc, sglgpu_plan** out) {
             p->d_V_off = dev_upload(t.radial_inv_off);
             p->d_r = dev_upload(std::vector<double>(desc->r, desc->r + 2 * B));
             p->d_amod = dev_upload(std::vector<double>(desc->a_mod, desc->a_mod + 2 * B));
+            {
+                const auto im = sglk::oz::build_leginv_image(B, t.legendre, t.legendre_off);
+                p->oz_li.img = dev_upload(im.bytes);
+                p->oz_li.off = dev_upload(im.off);
+                p->oz_li.rexp = dev_upload(im.rexp);
+                p->oz_li.kpad = dev_upload(im.kpad);
+                p->oz_li.mtiles = im.mtiles;
+            }
         } catch (...) {
             sglgpu_plan_destroy(p);
             throw;
@@ -1068,8 +1128,10 @@ int sglgpu_plan_destroy(sglgpu_plan* p) {
     cudaSetDevice(p->device);
     cudaDeviceSynchronize();
     for (void* q : {(void*)p->d_tw, (void*)p->d_bcal, (void*)p->d_leg, (void*)p->d_leg_off, (void*)p->d_W,
-                    (void*)p->d_W_off, (void*)p->d_V, (void*)p->d_V_off, (void*)p->d_r, (void*)p->d_amod})
+                    (void*)p->d_W_off, (void*)p->d_V, (void*)p->d_V_off, (void*)p->d_r, (void*)p->d_amod,
+                    (void*)p->oz_li.img, (void*)p->oz_li.off, (void*)p->oz_li.rexp, (void*)p->oz_li.kpad})
         if (q) cudaFree(q);
+    for (auto& kv : p->oz_units) cudaFree(kv.second.first);
     for (auto& kv : p->tiles) delete kv.second.first;
     for (auto& [stage, a, b] : p->prof) {
         cudaEventDestroy(a);
@@ -1235,7 +1297,7 @@ int sglgpu_spherical_inverse(sglgpu_plan* p, const double* shells, double* sampl
         p->main.G.ensure(2 * (size_t)sglk::g_layout(g));
         auto lt = tiles_for(p, kLegInv, nb, shell_count, 0, 2 * B);
         const sglk::SView sv{g.NB, shell_count, 0};
-        int k = sglk::launch_legendre_inverse(g, sv, shells, p->main.G.p, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
+        int k = leginv(p, g, sv, shells, p->main.G.p, lt, st);
         ck_launch(k, "legendre_inverse");
         int n = sglk::launch_az_inverse(g, p->main.G.p, samples, 2 * sample_stride, p->d_tw, st);
         ck_launch(n, "az_inverse");

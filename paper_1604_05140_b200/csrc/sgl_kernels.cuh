@@ -8,7 +8,31 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <mutex>
+
 namespace sglk {
+
+// Opt-in to more than 48 KB of dynamic shared memory, once per kernel and
+// device: the attribute belongs to the current device's context, and plans may
+// live on several devices of one process (sglgpu_plan_desc::device) and be used
+// from several threads.
+struct SmemAttrOnce {
+    std::atomic<unsigned long long> done{0};  // bit d: set on device d
+    std::mutex mu;
+    template <class Kernel>
+    void ensure(Kernel k, size_t smem) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+        const unsigned long long bit = 1ULL << dev;
+        if (done.load(std::memory_order_acquire) & bit) return;
+        std::lock_guard<std::mutex> lock(mu);
+        if (done.load(std::memory_order_relaxed) & bit) return;
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess)
+            done.fetch_or(bit, std::memory_order_release);
+    }
+};
+
 
 // Tile descriptor for the grouped DMMA contraction: {problem, m0, n0, warp layout wm}.
 struct Tile {
@@ -110,6 +134,41 @@ struct SView {
     int sc;
     int i0;
 };
+
+// --- addressing of the Legendre problems (device)
+// Index math inside one call's G, S and coefficient arrays is 32-bit: the host
+// keeps every array a GEMM touches below 2^31 doubles (batch_chunk).
+__device__ __forceinline__ int s_col(const Geo& g, const SView& sv, int am, int n) {
+    const int NB = (int)g.NB;
+    const int sgn = n >= NB;
+    const int nn = n - (sgn ? NB : 0);
+    const int f = g.batch == 1 ? 0 : nn / (2 * g.SC), rem = nn - f * 2 * g.SC;  // no division for one function
+    return (sgn ? -am : am) * (int)sv.NB + f * 2 * sv.sc + 2 * sv.i0 + rem;
+}
+
+// Real offset of column n of a Legendre problem inside the blocked G (the row
+// part, j' * row stride, is separate): n = (sgn, flat shell s, re/im).
+__device__ __forceinline__ int g_col(const Geo& g, int p, int am, int n) {
+    const int NB = (int)g.NB;
+    const int sgn = n >= NB;
+    const int nn = n - (sgn ? NB : 0);
+    const int s = nn >> 1;
+    const int bin = sgn ? 2 * g.B - am : am;
+    const int gx = s >> g.lgib;
+    const int sl = s & ((1 << g.lgib) - 1);
+    return 2 * ((((gx * 2 + p) * g.nbins + bin) << g.lgib) + sl) + (nn & 1);
+}
+// Table offsets in closed form (no dependent global load at CTA start; the
+// host tables' offset arrays, sgl_tables.cpp, hold the same values -- pinned by
+// tests/test_tables_and_model.py): Legendre problem 2|m| + p starts after
+// sum_{|m'| < |m|} (B - |m'|) rows plus, for p = 1, the (B - |m| + 1) / 2 rows of
+// parity 0; radial degree l after sum_{l' < l} (B - l') rows of 2B.
+__device__ __forceinline__ int leg_table_off(int B, int pid) {
+    const int am = pid >> 1, p = pid & 1;
+    return (B + (B & 1)) * (am * B - am * (am - 1) / 2 + p * ((B - am + 1) / 2));
+}
+__device__ __forceinline__ int rad_table_off(int B, int l) { return 2 * B * (l * B - l * (l - 1) / 2); }
+__device__ __forceinline__ int g_rowstride(const Geo& g) { return (2 * (int)g.ngx * 2 * g.nbins) << g.lgib; }
 
 // Polar stage: per (|m|, parity) DMMA contraction against the normalized
 // Legendre table.  tab: rows Pbar_{l,|m|}(cos theta_j'), j' < B.

@@ -757,3 +757,27 @@ def test_fused_spherical_forward_matches_oracle(B, monkeypatch):
     f = sgl.fsglft_batch(plan, torch.from_numpy(x).cuda()).cpu().numpy()
     for b in range(2):
         assert normwise(f[b], orc.forward(x[b])) <= TOL
+
+
+@pytest.mark.parametrize("B", [3, 16, 64, 128, 256])
+def test_int8_tensor_core_legendre_inverse_matches_oracle(B, monkeypatch):
+    """The opt-in INT8 tensor-core Legendre inverse (SGL_I8=leginv: fp64 by
+    7-byte fixed-point slices, 28 tcgen05 kind::i8 GEMMs per 32-deep k step,
+    DESIGN.md section 4) matches the oracle per shell, for one function and a
+    batch of two (columns spanning functions), with every output finite."""
+    import torch
+
+    monkeypatch.setenv("SGL_I8", "leginv")
+    plan, orc = plan_for(B) if B <= 128 else (sgl.TransformPlan.compute(B), Oracle(B))
+    rng = np.random.default_rng(700 + B)
+    c = complex_normal(rng, (2, coefficient_count(B)))
+    if B == 256:  # C4's scaling, as in test_b256_matches_oracle_both_directions
+        c = _c4_coefficients(B, 700 + B, 2)
+    g = sgl.ifsglft_batch(plan, torch.from_numpy(c).cuda()).cpu().numpy()
+    assert np.isfinite(g).all()
+    for b in range(2 if B <= 64 else 1):
+        assert per_shell(g[b], orc.inverse(c[b]), B) <= TOL
+    monkeypatch.setenv("SGL_I8", "0")
+    g0 = sgl.ifsglft_batch(plan, torch.from_numpy(c).cuda()).cpu().numpy()
+    for b in range(2):
+        assert per_shell(g[b], g0[b], B) <= TOL

@@ -41,9 +41,28 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, 
         ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
+__device__ __forceinline__ void mma_i8_warp(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
+        ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n"
+        ::"r"(tmem_d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// mode 0: single-thread issue, SS; 1: warp issue (elect), SS; 2: warp issue, A from TMEM (TS)
 template <int N, int K>
-__global__ void __launch_bounds__(128, 1) umma_i8_kernel(const int8_t* A, const int8_t* Bm, int* D, int reps, int asg, int bsg) {
+__global__ void __launch_bounds__(128, 1) umma_i8_kernel(const int8_t* A, const int8_t* Bm, int* D, int reps, int asg, int bsg, int mode) {
     constexpr int M = 128;
+    constexpr int kCols = (N + K / 4) <= 32 ? 32 : (N + K / 4) <= 64 ? 64 : (N + K / 4) <= 128 ? 128 : (N + K / 4) <= 256 ? 256 : 512;
     extern __shared__ __align__(1024) uint8_t sm[];
     uint8_t* sa = sm;                 // M * K bytes
     uint8_t* sb = sm + M * K;         // N * K bytes
@@ -60,7 +79,7 @@ __global__ void __launch_bounds__(128, 1) umma_i8_kernel(const int8_t* A, const 
         sb[(k >> 4) * (N * 16) + r * 16 + (k & 15)] = (uint8_t)Bm[e];
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)), "r"(N >= 32 ? N : 32));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)), "r"(kCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (tid == 0) {
@@ -72,7 +91,23 @@ __global__ void __launch_bounds__(128, 1) umma_i8_kernel(const int8_t* A, const 
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t td = tmem_base;
-    if (tid == 0) {
+    if (mode == 2) {  // A -> TMEM columns [N, N + K/4): lane = row, 4 int8 per column
+        const int row = warp * 32 + (tid & 31);
+        const int8_t* ar = Ab + (size_t)row * K;
+#pragma unroll
+        for (int c0 = 0; c0 < K / 4; c0 += 8) {
+            uint32_t w[8];
+            for (int j = 0; j < 8; ++j) w[j] = *reinterpret_cast<const uint32_t*>(ar + 4 * (c0 + j));
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n"
+                         ::"r"(td + ((uint32_t)(warp * 32) << 16) + N + c0), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]),
+                           "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]));
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n");
+        asm volatile("tcgen05.fence::before_thread_sync;\n");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+    }
+    if (mode == 0 && tid == 0) {
         const uint32_t id = idesc_i8(M, N, asg, bsg);
         const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
         for (int r = 0; r < reps; ++r) {
@@ -84,6 +119,18 @@ __global__ void __launch_bounds__(128, 1) umma_i8_kernel(const int8_t* A, const 
             }
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&bar)));
+    }
+    if (mode != 0 && warp == 0) {
+        const uint32_t id = idesc_i8(M, N, asg, bsg);
+        const uint64_t da0 = sdesc(smem_u32(sa), M * 16, 128), db0 = sdesc(smem_u32(sb), N * 16, 128);
+        for (int r = 0; r < reps; ++r) {
+#pragma unroll
+            for (int ks = 0; ks < K / 32; ++ks) {
+                if (mode == 1) mma_i8_warp(td, da0 + ks * 2 * M, db0 + ks * 2 * N, id, (r | ks) ? 1u : 0u);
+                else mma_i8_ts(td, td + N + ks * 8, db0 + ks * 2 * N, id, (r | ks) ? 1u : 0u);
+            }
+        }
+        asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(&bar)));
     }
     // wait for the MMAs
     {
@@ -108,11 +155,11 @@ __global__ void __launch_bounds__(128, 1) umma_i8_kernel(const int8_t* A, const 
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(td), "r"(N >= 32 ? N : 32));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(td), "r"(kCols));
 }
 
 template <int N, int K>
-static int run(int asg, int bsg, int ctas, int reps_time) {
+static int run(int asg, int bsg, int ctas, int reps_time, int mode = 0) {
     constexpr int M = 128;
     std::vector<int8_t> A((size_t)ctas * M * K), Bm((size_t)N * K);
     srand(1);
@@ -127,7 +174,7 @@ static int run(int asg, int bsg, int ctas, int reps_time) {
     CK(cudaMemcpy(dB, Bm.data(), Bm.size(), cudaMemcpyHostToDevice));
     const size_t smem = (size_t)(M + N) * K;
     CK(cudaFuncSetAttribute(umma_i8_kernel<N, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    umma_i8_kernel<N, K><<<ctas, 128, smem>>>(dA, dB, dD, 1, asg, bsg);
+    umma_i8_kernel<N, K><<<ctas, 128, smem>>>(dA, dB, dD, 1, asg, bsg, mode);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     std::vector<int> D((size_t)ctas * M * N);
@@ -150,15 +197,15 @@ static int run(int asg, int bsg, int ctas, int reps_time) {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    umma_i8_kernel<N, K><<<ctas, 128, smem>>>(dA, dB, dD, reps_time, asg, bsg);
+    umma_i8_kernel<N, K><<<ctas, 128, smem>>>(dA, dB, dD, reps_time, asg, bsg, mode);
     CK(cudaEventRecord(e0));
-    umma_i8_kernel<N, K><<<ctas, 128, smem>>>(dA, dB, dD, reps_time, asg, bsg);
+    umma_i8_kernel<N, K><<<ctas, 128, smem>>>(dA, dB, dD, reps_time, asg, bsg, mode);
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, e0, e1));
     const double ops = 2.0 * M * N * K * (double)reps_time * ctas;
-    printf("M=128 N=%d K=%d a%s b%s: %s (%ld bad); %d CTAs x %d reps: %.3f ms, %.1f TOPS\n", N, K, asg ? "s8" : "u8",
+    printf("mode %d M=128 N=%d K=%d a%s b%s: %s (%ld bad); %d CTAs x %d reps: %.3f ms, %.1f TOPS\n", mode, N, K, asg ? "s8" : "u8",
            bsg ? "s8" : "u8", bad ? "WRONG" : "exact", bad, ctas, reps_time, ms, ops / ms / 1e9);
     cudaFree(dA);
     cudaFree(dB);
@@ -170,14 +217,15 @@ int main() {
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     int fails = 0;
-    fails += run<64, 128>(1, 1, 4, 1);
-    fails += run<64, 128>(0, 1, 4, 1);
-    fails += run<64, 128>(1, 0, 4, 1);
-    fails += run<64, 128>(0, 0, 4, 1);
-    fails += run<128, 128>(1, 1, sms, 2000);
-    fails += run<256, 128>(1, 1, sms, 1000);
-    fails += run<64, 128>(0, 1, sms, 4000);
-    fails += run<256, 128>(0, 0, 2 * sms, 1000);
+    for (int mode = 0; mode < 3; ++mode) {
+        fails += run<64, 128>(1, 0, 4, 1, mode);
+        fails += run<32, 64>(0, 1, 4, 1, mode);
+        fails += run<16, 128>(0, 0, sms, 8000, mode);
+        fails += run<32, 128>(0, 1, sms, 8000, mode);
+        fails += run<64, 128>(0, 1, sms, 4000, mode);
+        fails += run<128, 128>(1, 1, sms, 2000, mode);
+        fails += run<256, 128>(1, 1, sms, 1000, mode);
+    }
     printf("%s\n", fails ? "FAILED" : "all exact");
     return fails;
 }
