@@ -112,7 +112,7 @@ struct Work {
 // A plan keeps up to kHostSlots of them, so that host calls from several threads
 // run concurrently (PCIe is full duplex: one caller's downloads overlap
 // another's uploads).
-constexpr int kHostSlots = 2;
+constexpr int kHostSlots = 8;
 struct HostSlot {
     Work w;
     DevBuf din[2], dout[2];
