@@ -1057,6 +1057,9 @@ struct LegFwdPeers : LegFwd {
 // one cp.async.bulk.tensor per chunk, issued by one thread and completing on an
 // mbarrier, into a [group][k][8] shared layout that the 8 x 8 x 4 fragment reads
 // hit without bank conflicts; the A tiles keep cp.async.  32 x 128 tiles only.
+#ifndef SGL_LEGFWD_SPLIT
+#define SGL_LEGFWD_SPLIT 0  // measured: no gain (round 2)
+#endif
 struct LegFwdTma : LegFwd {
     static constexpr bool B_TMA = true;
     static constexpr int GEMM_MAXWM = 1;
@@ -1064,6 +1067,14 @@ struct LegFwdTma : LegFwd {
     // 94.9 -> 92.0 us at B = 128 (round 2)
     static constexpr int GEMM_MINB = SGL_MINB_LEGFWD > 0 ? SGL_MINB_LEGFWD : 5;
     alignas(64) CUtensorMap tmap;  // G viewed as [p][bin][group][j'][8 doubles]
+};
+// The same with each 8-double shell-group block landing as two 4-double halves,
+// [group][half][k][4] (4-shell groups only, a 5-D box {4, BK, 2, groups, 1}): a
+// half-warp's B fragment (4 k x 4 columns) is then 16 consecutive doubles instead
+// of two 32-byte windows of 64-byte rows that fall on the same banks (ncu,
+// round 2: the B-operand LDS.64 ran at 2x their ideal wavefronts).
+struct LegFwdTmaSplit : LegFwdTma {
+    static constexpr bool B_SPLIT = true;
 };
 // ... and its multi-GPU form (S rows to their owners' receive buffers).
 struct LegFwdTmaPeers : LegFwdTma {
@@ -1130,6 +1141,11 @@ template <class P>
 struct has_btma<P, std::void_t<decltype(P::B_TMA)>> : std::bool_constant<P::B_TMA> {};
 
 template <class P, class = void>
+struct has_bsplit : std::false_type {};
+template <class P>
+struct has_bsplit<P, std::void_t<decltype(P::B_SPLIT)>> : std::bool_constant<P::B_SPLIT> {};
+
+template <class P, class = void>
 struct has_straddle : std::false_type {};
 template <class P>
 struct has_straddle<P, std::void_t<decltype(P::STRADDLE)>> : std::bool_constant<P::STRADDLE> {};
@@ -1184,7 +1200,10 @@ __device__ __forceinline__ void mma_chunk(const double* as, const double* bs, do
         }
 #pragma unroll
         for (int fn = 0; fn < NA; ++fn)
-            bf[fn] = has_btma<P>::value ? bs[((wc >> 3) + fn) * (C::BK * 8) + (kk + (lane & 3)) * 8 + (lane >> 2)]
+            bf[fn] = has_bsplit<P>::value
+                         ? bs[((wc >> 3) + fn) * (C::BK * 8) + (lane >> 4) * (C::BK * 4) + (kk + (lane & 3)) * 4 +
+                              ((lane >> 2) & 3)]
+                     : has_btma<P>::value ? bs[((wc >> 3) + fn) * (C::BK * 8) + (kk + (lane & 3)) * 8 + (lane >> 2)]
                                         : bs[(kk + (lane & 3)) * C::LDB + wc + fn * 8 + (lane >> 2)];
 #pragma unroll
         for (int fm = 0; fm < FA; ++fm)
@@ -1294,6 +1313,9 @@ __device__ __forceinline__ void gemm_epilogue(const P& pr, int pid, int m0, int 
     }
 }
 
+#ifndef SGL_A_QUAD
+#define SGL_A_QUAD 0  // measured: no gain (round 2)
+#endif
 template <class P, int WM>
 __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* smem) {
     using C = GemmCfg<P, WM>;
@@ -1325,7 +1347,15 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
         for (int u = 0; u < AU; ++u) {
             const int e = tid + 128 * u;
             int row, k;
-            if (P::A_KCONTIG) {
+            if (P::A_KCONTIG && BK == 8 && SGL_A_QUAD) {
+                // eight 16-byte units per quarter-warp (one shared-memory wavefront):
+                // 4 rows x 2 units, whose row starts (96-byte stride) fall on
+                // distinct 32-byte bank windows -- 2 rows x 4 units would collide
+                const int q = e >> 3, w = e & 7;
+                row = (q >> 1) * 4 + (w >> 1);
+                k = 2 * (2 * (q & 1) + (w & 1));
+                a_so[u] = row * C::LDA + k;
+            } else if (P::A_KCONTIG) {
                 row = e / (BK / 2);
                 k = 2 * (e % (BK / 2));
                 a_so[u] = row * C::LDA + k;
@@ -1731,7 +1761,8 @@ static int gemm_launch(const P& p, const TileMap* tiles, int ntiles, cudaStream_
 // TMA descriptor of the blocked G as a 5-D tensor [p][bin][group][j'][8 doubles]
 // (innermost first: 8 doubles = 4 shells x re/im, j', group, bin, p) whose box
 // {8, BK, 16, 1, 1} is one 32 x 128 tile's k-chunk of B.
-static bool make_g_tensor_map(const Geo& g, const double* G, int bk, CUtensorMap* out, int box_groups = 0) {
+static bool make_g_tensor_map(const Geo& g, const double* G, int bk, CUtensorMap* out, int box_groups = 0,
+                              bool split = false) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -1746,9 +1777,13 @@ static bool make_g_tensor_map(const Geo& g, const double* G, int bk, CUtensorMap
     const cuuint64_t row = 2ULL * groups * 2 * g.nbins * W / 2;  // doubles per j' row (g_rowstride)
     // dims (innermost first): 8 doubles, j', block of 8 inside a group, group,
     // (p, bin) as one index p * nbins + bin (its stride is W doubles either way)
-    const cuuint64_t dims[5] = {8, (cuuint64_t)g.B, H, groups, 2ULL * g.nbins};
-    const cuuint64_t strides[4] = {row * 8, 64, 2ULL * g.nbins * W * 8, W * 8};
-    const cuuint32_t box[5] = {8, (cuuint32_t)bk, (cuuint32_t)H, (cuuint32_t)(box_groups > 0 ? box_groups : 128 / W), 1};
+    // split (4-shell groups): the H = 1 dimension becomes the two 4-double halves
+    // of the group, ordered outside j' in shared memory ([group][half][j'][4])
+    if (split && H != 1) return false;
+    const cuuint64_t dims[5] = {split ? 4ULL : 8ULL, (cuuint64_t)g.B, split ? 2ULL : H, groups, 2ULL * g.nbins};
+    const cuuint64_t strides[4] = {row * 8, split ? 32ULL : 64ULL, 2ULL * g.nbins * W * 8, W * 8};
+    const cuuint32_t box[5] = {split ? 4u : 8u, (cuuint32_t)bk, split ? 2u : (cuuint32_t)H,
+                               (cuuint32_t)(box_groups > 0 ? box_groups : 128 / W), 1};
     const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(G), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1934,6 +1969,11 @@ int launch_legendre_forward(const Geo& g, const SView& sv, const double* G, doub
     if (SGL_LEGFWD_TMA) {
         LegFwdTma q;
         static_cast<LegFwd&>(q) = p;
+        if (SGL_LEGFWD_SPLIT && g.lgib == 2) {
+            LegFwdTmaSplit qs;
+            static_cast<LegFwd&>(qs) = p;
+            if (make_g_tensor_map(g, G, LegFwd::GEMM_BK, &qs.tmap, 0, true)) return gemm_launch<LegFwdTmaSplit>(qs, tiles, ntiles, s);
+        }
         if (make_g_tensor_map(g, G, LegFwd::GEMM_BK, &q.tmap)) return gemm_launch<LegFwdTma>(q, tiles, ntiles, s);
     }
     return gemm_launch<LegFwd>(p, tiles, ntiles, s);
