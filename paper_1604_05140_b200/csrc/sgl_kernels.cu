@@ -1461,7 +1461,11 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
         const int a_adv = k0 * a_sk;
 #pragma unroll
         for (int u = 0; u < AU; ++u) {
+#ifdef SGL_TABLE_L2  // experiment (wrong results): every table read from one 64 KB, L2-resident block
+            const double* src = pr.A + (((a_ptr[u] - pr.A) + a_adv) & 8190);
+#else
             const double* src = a_ptr[u] + a_adv;
+#endif
             bool ok1, ok2;  // the unit's two elements
             if (kfull) {
                 ok1 = a_nb[u] >= 8;
