@@ -161,6 +161,7 @@ struct sglgpu_plan {
         long long* off = nullptr;
         int* rexp = nullptr;
         int* kpad = nullptr;
+        int* corr = nullptr;
         int mtiles = 1;
     } oz_li;
     std::map<std::tuple<long long, int, int>, std::pair<sglk::oz::Unit*, int>> oz_units;
@@ -352,17 +353,19 @@ int i8_tpc() {
 }
 
 // Legendre inverse: the INT8 tensor-core kernel when enabled, else the DMMA GEMM.
-int leginv(sglgpu_plan* p, const sglk::Geo& g, const sglk::SView& sv, const double* S, double* G,
+int leginv(sglgpu_plan* p, Work& w, const sglk::Geo& g, const sglk::SView& sv, const double* S, double* G,
            std::pair<sglk::TileMap*, int> lt, cudaStream_t st) {
-    if (p->oz_li.img && i8_on("leginv")) {
-        const int tpc = i8_tpc();
+    const bool ws = p->oz_li.img && i8_on("ws");
+    if (ws || (p->oz_li.img && i8_on("leginv"))) {
+        const int tpc = ws ? -1 : i8_tpc();
         std::pair<sglk::oz::Unit*, int> un;
         {
             std::lock_guard<std::mutex> meta(p->meta_mu);
             const auto key = std::make_tuple(g.NB, g.real, tpc);
             auto it = p->oz_units.find(key);
             if (it == p->oz_units.end()) {
-                const auto hu = sglk::oz::leginv_units(p->B, g.NB, g.real != 0, tpc);
+                const auto hu = ws ? sglk::oz::leginv_ws_units(p->B, g.NB, g.real != 0)
+                                   : sglk::oz::leginv_units(p->B, g.NB, g.real != 0, tpc);
                 sglk::oz::Unit* d = nullptr;
                 ck(cudaMalloc(&d, std::max<size_t>(1, hu.size()) * sizeof(sglk::oz::Unit)), "cudaMalloc(units)");
                 ck(cudaMemcpy(d, hu.data(), hu.size() * sizeof(sglk::oz::Unit), cudaMemcpyHostToDevice), "upload units");
@@ -373,7 +376,12 @@ int leginv(sglgpu_plan* p, const sglk::Geo& g, const sglk::SView& sv, const doub
         sglk::oz::LegInvI8 prm{g, sv, S, G, p->oz_li.img, p->oz_li.off, p->oz_li.rexp, p->oz_li.kpad, un.first, tpc,
                                p->oz_li.mtiles};
         if (const char* tr = std::getenv("SGL_I8_TRACE")) prm.trace = reinterpret_cast<long long*>(std::strtoull(tr, nullptr, 0));
-        return sglk::oz::launch_legendre_inverse_i8(prm, un.second, st);
+        prm.corr = p->oz_li.corr;
+        w.counters.ensure(1);  // the call's own unit ticket (host slots run concurrently)
+        prm.counter = reinterpret_cast<int*>(w.counters.p);
+        prm.grid = p->num_sms;
+        return ws ? sglk::oz::launch_legendre_inverse_ws(prm, un.second, st)
+                  : sglk::oz::launch_legendre_inverse_i8(prm, un.second, st);
     }
     return sglk::launch_legendre_inverse(g, sv, S, G, p->d_leg, p->d_leg_off, lt.first, lt.second, st);
 }
@@ -625,7 +633,7 @@ int inverse_device(sglgpu_plan* p, Work& w, const double* C, double* X, int nb, 
             const int i0 = c * SC;
             const sglk::SView v{2LL * 2 * B, 2 * B, i0};
             k = staged(p, 4, st, [&] {
-                return leginv(p, gc, v, w.S.p, w.G.p, lt, st);
+                return leginv(p, w, gc, v, w.S.p, w.G.p, lt, st);
             });
             ck_launch(k, "legendre_inverse");
             n += k;
@@ -651,7 +659,7 @@ int inverse_device(sglgpu_plan* p, Work& w, const double* C, double* X, int nb, 
         ck_launch(k, "radial_inverse");
         n += k;
         k = staged(p, 4, st, [&] {
-            return leginv(p, g, sv, w.S.p, w.G.p, lt, st);
+            return leginv(p, w, g, sv, w.S.p, w.G.p, lt, st);
         });
         ck_launch(k, "legendre_inverse");
         n += k;
@@ -711,7 +719,7 @@ int real_device(sglgpu_plan* p, Work& w, const double* in, double* out, int nb, 
             ck_launch(k, "radial_inverse");
             n += k;
             k = staged(p, 4, st, [&] {
-                return leginv(p, g, sv, w.S.p, w.G.p, lt, st);
+                return leginv(p, w, g, sv, w.S.p, w.G.p, lt, st);
             });
             ck_launch(k, "legendre_inverse");
             n += k;
@@ -1109,6 +1117,7 @@ int sglgpu_plan_create(const sglgpu_plan_desc* desc, sglgpu_plan** out) {
                 p->oz_li.off = dev_upload(im.off);
                 p->oz_li.rexp = dev_upload(im.rexp);
                 p->oz_li.kpad = dev_upload(im.kpad);
+                p->oz_li.corr = dev_upload(im.corr);
                 p->oz_li.mtiles = im.mtiles;
             }
         } catch (...) {
@@ -1129,7 +1138,7 @@ int sglgpu_plan_destroy(sglgpu_plan* p) {
     cudaDeviceSynchronize();
     for (void* q : {(void*)p->d_tw, (void*)p->d_bcal, (void*)p->d_leg, (void*)p->d_leg_off, (void*)p->d_W,
                     (void*)p->d_W_off, (void*)p->d_V, (void*)p->d_V_off, (void*)p->d_r, (void*)p->d_amod,
-                    (void*)p->oz_li.img, (void*)p->oz_li.off, (void*)p->oz_li.rexp, (void*)p->oz_li.kpad})
+                    (void*)p->oz_li.img, (void*)p->oz_li.off, (void*)p->oz_li.rexp, (void*)p->oz_li.kpad, (void*)p->oz_li.corr})
         if (q) cudaFree(q);
     for (auto& kv : p->oz_units) cudaFree(kv.second.first);
     for (auto& kv : p->tiles) delete kv.second.first;
@@ -1297,7 +1306,7 @@ int sglgpu_spherical_inverse(sglgpu_plan* p, const double* shells, double* sampl
         p->main.G.ensure(2 * (size_t)sglk::g_layout(g));
         auto lt = tiles_for(p, kLegInv, nb, shell_count, 0, 2 * B);
         const sglk::SView sv{g.NB, shell_count, 0};
-        int k = leginv(p, g, sv, shells, p->main.G.p, lt, st);
+        int k = leginv(p, p->main, g, sv, shells, p->main.G.p, lt, st);
         ck_launch(k, "legendre_inverse");
         int n = sglk::launch_az_inverse(g, p->main.G.p, samples, 2 * sample_stride, p->d_tw, st);
         ck_launch(n, "az_inverse");

@@ -129,6 +129,9 @@ __device__ __forceinline__ void tmem_ld16x256(uint32_t taddr, int (&v)[4]) {
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
                  : "r"(taddr));
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NLEFT>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NLEFT) : "memory"); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 // ------------------------------------------------------------------ number format
@@ -398,6 +401,332 @@ int launch_legendre_inverse_i8(const LegInvI8& prm, int nunits, cudaStream_t s) 
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
+// ------------------------------------------------------------------ Legendre inverse, warp-specialised
+__device__ __forceinline__ void bar_arrive(uint32_t a) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+
+// 16 lanes x 16 columns: v[0..3] as tmem_ld16x256 for columns 0..7, v[4..7] for 8..15
+__device__ __forceinline__ void tmem_ld16x256x2(uint32_t taddr, int (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+
+template <int KPMAX>
+__global__ void __launch_bounds__(512, 1) leginv_ws_kernel(const __grid_constant__ LegInvI8 P) {
+    constexpr int NR = kDigits * kWsN;      // 224 stacked data-digit rows
+    constexpr int SB = KPMAX * NR;          // bytes per data stage
+    constexpr int TM = kLevels * kWsN;      // 224 TMEM columns per buffer
+    constexpr int NPW = 7;                  // producer warps (9 .. 15)
+    constexpr int CPT = (KPMAX / 16 + NPW - 1) / NPW;  // 16-deep k chunks per producer thread
+    constexpr int FST = KPMAX > 64 ? 1 : 3;            // fp64 staging buffers (tiles in flight)
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint8_t* sA = sm;
+    uint8_t* sB = sm + kDigits * KPMAX * kTileM;
+    double* sF = reinterpret_cast<double*>(sB + 2 * SB);
+    __shared__ int colE[4][kWsN];
+    // 0 table, 1-2 data full, 3-4 data empty, 5-6 TMEM full, 7-8 TMEM empty
+    __shared__ __align__(8) unsigned long long bars[9];
+    __shared__ uint32_t tmem_base;
+    __shared__ int s_unit;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const Geo& g = P.g;
+    const int B = g.B, NB = (int)g.NB;
+    const int ntl = (NB + kWsN - 1) / kWsN;  // column tiles of a sign half
+    const int rs = g_rowstride(g);
+    auto bar = [&](int i) { return su32(&bars[i]); };
+    if (tid == 0) {
+        bar_init(bar(0), 1);
+        for (int s = 0; s < 2; ++s) {
+            bar_init(bar(1 + s), 1);
+            bar_init(bar(3 + s), 1);
+            bar_init(bar(5 + s), 1);
+            bar_init(bar(7 + s), 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 8) tmem_alloc(su32(&tmem_base), 512);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t td = tmem_base;
+    // persistent: units (problem, m-tile, sign half; heaviest first) from a global
+    // counter; T0 = tiles this CTA ran before the unit (barrier phases continue)
+    int T0 = 0, nunit = 0;
+    for (;;) {
+        if (tid == 0) s_unit = atomicAdd(P.counter, 1);
+        __syncthreads();
+        const int ui = s_unit;
+        if (ui >= P.nunits) break;
+        const Unit u = P.units[ui];
+        const int am = u.pid >> 1, p = u.pid & 1;
+        const int K = (B - am - p) > 0 ? (B - am - p + 1) / 2 : 0;
+        const int Kp = P.kpad[u.pid];
+        const int tix = u.pid * P.mtiles + u.mt;
+        const bool neg = u.half == 1 && (am & 1);  // the reference's sign of odd negative m
+        if (K == 0) {  // no degrees of this parity: G is zero there
+            for (int e = tid; e < kTileM * NB; e += blockDim.x) {
+                const int r = e / NB, c = e - r * NB, jp = u.mt * kTileM + r;
+                if (jp < B && (c & 1) == 0)
+                    *reinterpret_cast<double2*>(P.G + (long long)jp * rs + g_col(g, p, am, u.half * NB + c)) =
+                        make_double2(0.0, 0.0);
+            }
+        } else if (warp >= 9) {
+            // ---- producers: S tile -> column scales -> stacked unsigned digit planes.
+            // The fp64 tile is staged by cp.async (8-byte copies, one row of 32
+            // columns per warp instruction), FST - 1 tiles ahead.
+            if (tid == 288) bulk_load(su32(sA), P.img + P.img_off[tix], (uint32_t)(kDigits * Kp * kTileM), bar(0));
+            const int pt = tid - 288, c = pt & 31, wp = pt >> 5;
+            const int nkc = Kp / 16;
+            auto stage_tile = [&](int t) {  // cp.async of tile t's S rows into staging buffer (T0 + t) % FST
+                const int nloc0 = t * kWsN, ncols = min(kWsN, NB - nloc0), n0 = u.half * NB + nloc0;
+                if (c < ncols) {
+                    const double* src = P.S + s_col(g, P.sv, am, n0 + c);
+                    double* dst = sF + ((T0 + t) % FST) * (KPMAX * kWsN) + c;
+                    for (int k = wp; k < K; k += NPW) {
+                        const long long l = am + p + 2 * k;
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(su32(dst + k * kWsN)),
+                                     "l"(src + l * (l + 1) * P.sv.NB));
+                    }
+                }
+                cp_async_commit();
+            };
+            stage_tile(0);
+            if (FST == 3) {
+                if (1 < ntl) stage_tile(1);
+                else cp_async_commit();
+            }
+            for (int t = 0; t < ntl; ++t) {
+                const int T = T0 + t, s = T & 1;
+                const int ncols = min(kWsN, NB - t * kWsN);
+                if (FST == 3) {
+                    if (t + 2 < ntl) stage_tile(t + 2);
+                    else cp_async_commit();
+                    cp_async_wait_group<2>();
+                } else {
+                    cp_async_wait_group<0>();
+                }
+                if (T >= 2) bar_wait(bar(3 + s), ((T >> 1) - 1) & 1);  // the MMAs of tile T - 2 have read stage s
+                if (pt < kWsN) colE[T & 3][pt] = 0;
+                named_sync(1, 32 * NPW);
+                double v[CPT][16];
+                {
+                    int mE = 0;
+                    const double* fs = sF + (T % FST) * (KPMAX * kWsN) + c;
+#pragma unroll
+                    for (int ci = 0; ci < CPT; ++ci) {
+                        const int kc = wp + NPW * ci;
+#pragma unroll
+                        for (int r = 0; r < 16; ++r) {
+                            const int k = kc * 16 + r;
+                            const double x = (k < K && c < ncols) ? fs[k * kWsN] : 0.0;
+                            v[ci][r] = x;
+                            mE = max(mE, exp_bits(x));
+                        }
+                    }
+                    if (mE) atomicMax(&colE[T & 3][c], mE);
+                }
+                named_sync(1, 32 * NPW);
+                {
+                    // X = trunc(x 2^(55 - e)) + 2^55 (e = cE - 1022; the scale as the product of
+                    // two normal powers of two: exact down to subnormals), F2I.S64, PRMT planes
+                    const int cE = colE[T & 3][c];
+                    const int e = 1077 - cE, e2 = min(e, 1000);
+                    const double s2 = __longlong_as_double((long long)(e2 + 1023) << 52);
+                    const double s1 = __longlong_as_double((long long)(max(0, e - e2) + 1023) << 52);
+                    auto fx = [&](double x) { return __double2ll_rz(x * s1 * s2) + (1LL << 55); };
+#pragma unroll
+                    for (int ci = 0; ci < CPT; ++ci) {
+                        const int kc = wp + NPW * ci;
+                        if (kc >= nkc) continue;
+                        uint8_t* dst = sB + s * SB + kc * (NR * 16) + c * 16;
+#pragma unroll
+                        for (int qd = 0; qd < 4; ++qd) {
+                            const long long X0 = fx(v[ci][4 * qd]), X1 = fx(v[ci][4 * qd + 1]), X2 = fx(v[ci][4 * qd + 2]),
+                                            X3 = fx(v[ci][4 * qd + 3]);
+                            const uint32_t l0 = (uint32_t)X0, l1 = (uint32_t)X1, l2 = (uint32_t)X2, l3 = (uint32_t)X3;
+                            const uint32_t h0 = (uint32_t)(X0 >> 32), h1 = (uint32_t)(X1 >> 32), h2 = (uint32_t)(X2 >> 32),
+                                           h3 = (uint32_t)(X3 >> 32);
+#pragma unroll
+                            for (int bb = 0; bb < 4; ++bb) {
+                                const uint32_t sel = (uint32_t)(bb | ((bb + 4) << 4));
+                                reinterpret_cast<uint32_t*>(dst + (6 - bb) * (kWsN * 16))[qd] =
+                                    __byte_perm(__byte_perm(l0, l1, sel), __byte_perm(l2, l3, sel), 0x5410);
+                            }
+#pragma unroll
+                            for (int bb = 0; bb < 3; ++bb) {
+                                const uint32_t sel = (uint32_t)(bb | ((bb + 4) << 4));
+                                reinterpret_cast<uint32_t*>(dst + (2 - bb) * (kWsN * 16))[qd] =
+                                    __byte_perm(__byte_perm(h0, h1, sel), __byte_perm(h2, h3, sel), 0x5410);
+                            }
+                        }
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                named_sync(1, 32 * NPW);
+                if (pt == 0) bar_arrive(bar(1 + s));
+                if (FST == 1 && t + 1 < ntl) stage_tile(t + 1);
+            }
+        } else if (warp == 8) {
+            // ---- MMA issuer: per 32-deep k step, digit i of the table against the
+            // stacked data planes 0 .. 6 - i (N = 32 (7 - i)) into levels i .. 6
+            if (lane == 0) {
+                bar_wait(bar(0), nunit & 1);
+                const uint32_t aA = su32(sA), aB = su32(sB);
+                const uint32_t pa = (uint32_t)(Kp * kTileM);
+                for (int t = 0; t < ntl; ++t) {
+                    const int T = T0 + t, s = T & 1, b = T & 1;
+                    bar_wait(bar(1 + s), (T >> 1) & 1);
+                    if (T >= 2) bar_wait(bar(7 + b), ((T >> 1) - 1) & 1);
+                    fence_after();
+                    for (int ks = 0; ks < Kp / 32; ++ks) {
+                        const uint64_t db = sdesc(aB + s * SB + ks * 2 * (NR * 16), NR * 16, 128);
+#pragma unroll
+                        for (int i = 0; i < kDigits; ++i) {
+                            const uint64_t da = sdesc(aA + i * pa + ks * 2 * (kTileM * 16), kTileM * 16, 128);
+                            mma_i8_1(td + (uint32_t)(b * TM + i * kWsN), da, db,
+                                     idesc_i8(kTileM, (kDigits - i) * kWsN, i == 0, false), (ks | i) ? 1u : 0u);
+                        }
+                    }
+                    mma_commit_1(bar(3 + s));
+                    mma_commit_1(bar(5 + b));
+                }
+            }
+            __syncwarp();
+        } else {
+            // ---- epilogue: warp w drains TMEM lanes 32 (w % 4) + 16 (w / 4) .. + 15
+            // with 16x256b loads (four threads per row, 64-byte store runs) and
+            // releases the buffer after its last load
+            const int q = warp & 3, h = warp >> 2, t0 = lane & 3, t1 = lane >> 2;
+            // per row (w: +0 / +8): scale 2^e, and the magic constants of the int64 ->
+            // fp64 conversions with the bias correction folded in (hi: levels 0-2,
+            // lo: levels 3-6; exact in int64)
+            double rsc[2];
+            long long mhi[2], mlo[2];
+#pragma unroll
+            for (int w = 0; w < 2; ++w) {
+                const int row = q * 32 + h * 16 + t1 + 8 * w;
+                rsc[w] = pow2(P.rexp[tix * kTileM + row]);
+                const int* cr = P.corr + (size_t)tix * kDigits * kTileM + row;
+                mhi[w] = 0x4538000000000000LL - ((long long)cr[0] * 65536 + (long long)cr[kTileM] * 256 + cr[2 * kTileM]);
+                mlo[w] = 0x4338000000000000LL - ((long long)cr[3 * kTileM] * 16777216 + (long long)cr[4 * kTileM] * 65536 +
+                                                 (long long)cr[5 * kTileM] * 256 + cr[6 * kTileM]);
+            }
+            const int ja = u.mt * kTileM + q * 32 + h * 16 + t1;
+            double* outa = P.G + (long long)ja * rs;
+            double* outb = P.G + (long long)(ja + 8) * rs;
+            for (int t = 0; t < ntl; ++t) {
+                const int T = T0 + t, b = T & 1;
+                const int nloc0 = t * kWsN, ncols = min(kWsN, NB - nloc0), n0 = u.half * NB + nloc0;
+                bar_wait(bar(5 + b), (T >> 1) & 1);
+                fence_after();
+                const uint32_t ta = td + ((uint32_t)(q * 32 + h * 16) << 16) + (uint32_t)(b * TM);
+#pragma unroll
+                for (int cp = 0; cp < 2; ++cp) {
+                    int a[kLevels][8];
+#pragma unroll
+                    for (int lv = 0; lv < kLevels; ++lv) tmem_ld16x256x2(ta + (uint32_t)(lv * kWsN + cp * 16), a[lv]);
+                    tmem_wait_ld();
+                    if (cp == 1) {  // this warp's last TMEM load of the buffer
+                        fence_before();
+                        __syncwarp();
+                        if (lane == 0) bar_arrive(bar(7 + b));
+                    }
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        const int cc = cp * 16 + r * 8 + 2 * t0;
+                        double cs[2];
+#pragma unroll
+                        for (int y = 0; y < 2; ++y) {
+                            const int e = colE[T & 3][cc + y];
+                            const double sc = e ? pow2(e - 1084) : 0.0;
+                            cs[y] = neg ? -sc : sc;
+                        }
+                        double o[4];
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) {
+                            const int w = x >> 1, vi = r * 4 + x;  // x: (row w, column x & 1)
+                            if (SGL_OZ_EXP & 2) {
+                                o[x] = (double)(a[0][vi] + a[3][vi] + a[6][vi]);
+                                continue;
+                            }
+                            const long long hi = (long long)a[0][vi] * 65536 + (long long)a[1][vi] * 256 + a[2][vi] + mhi[w];
+                            const long long lo = (long long)a[3][vi] * 16777216 + (long long)a[4][vi] * 65536 +
+                                                 (long long)a[5][vi] * 256 + a[6][vi] + mlo[w];
+                            const double dh = __longlong_as_double(hi) - 29014219670751100192948224.0;
+                            const double dl = __longlong_as_double(lo) - 6755399441055744.0;
+                            o[x] = (dh + dl) * rsc[w] * cs[x & 1];
+                        }
+                        if ((SGL_OZ_EXP & 1) && o[0] != 1.2345e-300) continue;
+                        if (cc < ncols) {
+                            const int off = g_col(g, p, am, n0 + cc);
+                            if (ja < B) *reinterpret_cast<double2*>(outa + off) = make_double2(o[0], o[1]);
+                            if (ja + 8 < B) *reinterpret_cast<double2*>(outb + off) = make_double2(o[2], o[3]);
+                        }
+                    }
+                }
+            }
+        }
+        if (K > 0) {
+            T0 += ntl;
+            ++nunit;
+        }
+        fence_before();
+        __syncthreads();  // every MMA of the unit has completed (the epilogue drained them): the table may be reloaded
+        fence_after();
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 8) tmem_dealloc(td, 512);
+}
+
+size_t leginv_ws_smem(int B) {
+    const int kp = B > 128 ? 128 : 64;
+    const int fst = B > 128 ? 1 : 3;  // fp64 staging buffers (FST in the kernel)
+    return (size_t)kDigits * kp * kTileM + 2 * (size_t)kp * kDigits * kWsN + (size_t)fst * kp * kWsN * 8;
+}
+
+int launch_legendre_inverse_ws(const LegInvI8& prm_in, int nunits, cudaStream_t s) {
+    if (nunits <= 0) return 0;
+    LegInvI8 prm = prm_in;
+    prm.nunits = nunits;
+    if (cudaMemsetAsync(prm.counter, 0, sizeof(int), s) != cudaSuccess) return -1;
+    const size_t smem = leginv_ws_smem(prm.g.B);
+    if (prm.g.B > 128) {
+        static SmemAttrOnce attr;
+        attr.ensure(leginv_ws_kernel<128>, smem);
+        leginv_ws_kernel<128><<<std::min(nunits, prm.grid), 512, smem, s>>>(prm);
+    } else {
+        static SmemAttrOnce attr;
+        attr.ensure(leginv_ws_kernel<64>, smem);
+        leginv_ws_kernel<64><<<std::min(nunits, prm.grid), 512, smem, s>>>(prm);
+    }
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+std::vector<Unit> leginv_ws_units(int B, long long NB, bool real) {
+    const int mtiles = (B + kTileM - 1) / kTileM;
+    struct W {
+        int K;
+        Unit u;
+    };
+    std::vector<W> ws;
+    for (int pid = 0; pid < 2 * B; ++pid) {
+        const int am = pid >> 1, p = pid & 1, r = B - am - p;
+        const int K = r > 0 ? (r + 1) / 2 : 0;
+        const int halves = (am == 0 || real) ? 1 : 2;
+        for (int mt = 0; mt < mtiles; ++mt)
+            for (int h = 0; h < halves; ++h) ws.push_back({(K + 31) / 32, Unit{pid, mt, h, 0}});
+    }
+    std::stable_sort(ws.begin(), ws.end(), [](const W& a, const W& b) { return a.K > b.K; });
+    std::vector<Unit> us;
+    for (const W& w : ws) us.push_back(w.u);
+    (void)NB;
+    return us;
+}
+
 // ------------------------------------------------------------------ host: table images and units
 namespace {
 // 7 digit bytes of trunc(y * 2^(55 - e)) (digit 0 most significant, signed)
@@ -416,6 +745,7 @@ TableImage build_leginv_image(int B, const std::vector<double>& leg, const std::
     im.off.assign((size_t)np * im.mtiles, -1);
     im.kpad.assign(np, 0);
     im.rexp.assign((size_t)np * im.mtiles * kTileM, 0);
+    im.corr.assign((size_t)np * im.mtiles * kDigits * kTileM, 0);
     size_t total = 0;
     for (int pid = 0; pid < np; ++pid) {
         const int am = pid >> 1, p = pid & 1, r = B - am - p;
@@ -443,11 +773,14 @@ TableImage build_leginv_image(int B, const std::vector<double>& leg, const std::
                 if (mx > 0) std::frexp(mx, &e);
                 im.rexp[((size_t)pid * im.mtiles + mt) * kTileM + rr] = e;
                 if (mx == 0) continue;
+                int* corr = im.corr.data() + ((size_t)pid * im.mtiles + mt) * kDigits * kTileM + rr;
                 for (int k = 0; k < K; ++k) {
                     uint8_t d[kDigits];
                     digits_of(leg[leg_off[pid] + (long long)k * LS + jp], e, d);
-                    for (int i = 0; i < kDigits; ++i)
+                    for (int i = 0; i < kDigits; ++i) {
                         base[(size_t)i * Kp * kTileM + (size_t)(k / 16) * (kTileM * 16) + rr * 16 + (k % 16)] = d[i];
+                        corr[i * kTileM] += 128 * (i == 0 ? (int)(int8_t)d[i] : (int)d[i]);
+                    }
                 }
             }
         }

@@ -41,6 +41,7 @@ struct TableImage {
     std::vector<long long> off;  // per (problem * mtiles + mt): byte offset, -1: empty problem
     std::vector<int> kpad;       // per problem: K rounded up to 32
     std::vector<int> rexp;       // per (problem * mtiles + mt) * 128 + row: frexp exponent of the row maximum
+    std::vector<int> corr;       // per (problem * mtiles + mt) * 7 * 128 + digit * 128 + row: 128 * sum_k Y_digit[row][k]
     int mtiles = 1;
 };
 
@@ -65,7 +66,24 @@ struct LegInvI8 {
     int tpc;      // n-tiles per unit
     int mtiles;
     long long* trace = nullptr;  // experiments: per-CTA phase clocks [unit][tile < 8][phase < 8]
+    const int* corr = nullptr;   // warp-specialised kernel: bias corrections (TableImage::corr)
+    int* counter = nullptr;      // ... its unit ticket (zeroed by the launcher)
+    int nunits = 0;
+    int grid = 148;              // ... persistent CTAs (one per SM)
 };
+
+// Warp-specialised form (leginv_ws_kernel): 32-column tiles whose 7 data digit
+// planes are stacked along N (224 rows), so ONE int8 MMA per table digit i
+// covers all products (i, j <= 6 - i) -- 7 MMAs of N = 224 ... 32 per 32-deep
+// k step instead of 28 of N = 32 -- landing in TMEM levels i .. 6 by the column
+// offset i * 32; all data digits are unsigned (the top one biased by 128, undone by
+// a per-row constant in the epilogue).  Two TMEM buffers (2 x 224 columns), two
+// shared-memory stages: producers (8 warps), one MMA warp and 4 epilogue warps
+// overlap.  One CTA per (problem, m-tile, sign half).
+constexpr int kWsN = 32;
+std::vector<Unit> leginv_ws_units(int B, long long NB, bool real);
+size_t leginv_ws_smem(int B);
+int launch_legendre_inverse_ws(const LegInvI8& prm, int nunits, cudaStream_t s);
 
 // Host: the units of a Legendre-inverse launch (heaviest first) for NB reals per
 // nu row of S; returns the unit count.
