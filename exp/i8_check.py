@@ -13,7 +13,7 @@ for B in Bs:
     ct = torch.tensor(c, dtype=torch.complex128, device="cuda").reshape(1, n)
     os.environ["SGL_I8"] = "0"
     g0 = sgl.ifsglft_batch(plan, ct); torch.cuda.synchronize()
-    os.environ["SGL_I8"] = "leginv"
+    os.environ["SGL_I8"] = os.environ.get("I8MODE", "leginv")
     t = time.time(); g1 = sgl.ifsglft_batch(plan, ct); torch.cuda.synchronize(); dt = time.time() - t
     a, b = g0.cpu().numpy().ravel(), g1.cpu().numpy().ravel()
     msg = f"B={B}: i8 vs dmma per-shell {per_shell(b, a, B):.2e} finite {np.isfinite(b).all()}"

@@ -759,15 +759,16 @@ def test_fused_spherical_forward_matches_oracle(B, monkeypatch):
         assert normwise(f[b], orc.forward(x[b])) <= TOL
 
 
+@pytest.mark.parametrize("mode", ["leginv", "ws"])
 @pytest.mark.parametrize("B", [3, 16, 64, 128, 256])
-def test_int8_tensor_core_legendre_inverse_matches_oracle(B, monkeypatch):
+def test_int8_tensor_core_legendre_inverse_matches_oracle(B, mode, monkeypatch):
     """The opt-in INT8 tensor-core Legendre inverse (SGL_I8=leginv: fp64 by
     7-byte fixed-point slices, 28 tcgen05 kind::i8 GEMMs per 32-deep k step,
     DESIGN.md section 4) matches the oracle per shell, for one function and a
     batch of two (columns spanning functions), with every output finite."""
     import torch
 
-    monkeypatch.setenv("SGL_I8", "leginv")
+    monkeypatch.setenv("SGL_I8", mode)
     plan, orc = plan_for(B) if B <= 128 else (sgl.TransformPlan.compute(B), Oracle(B))
     rng = np.random.default_rng(700 + B)
     c = complex_normal(rng, (2, coefficient_count(B)))
