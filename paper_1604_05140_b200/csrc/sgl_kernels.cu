@@ -546,22 +546,28 @@ az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, doub
     }
     __syncthreads();
     const double b = __ldg(bcal + jp);
+    // one (shell, m) per iteration: both parities from the same Z[m], Z[-m]
 #pragma unroll 4
-    for (int idx = tid; idx < 2 * B * IGR; idx += S::THREADS) {
+    for (int idx = tid; idx < B * IGR; idx += S::THREADS) {
         const int sl = idx % IGR;
-        const int rowi = idx / IGR;  // p * B + m
-        const int p = rowi / B, m = rowi - p * B;
+        const int m = idx / IGR;
         const int s = s0 + sl;
         if (s >= nshell) continue;
         const double2 zm = rings[sl * S::STRIDE + phys(m)];
         const double2 zn = rings[sl * S::STRIDE + phys((N - m) & (N - 1))];
         const double2 x1 = make_double2(0.5 * (zm.x + zn.x), 0.5 * (zm.y - zn.y));
         const double2 x2 = make_double2(0.5 * (zm.y + zn.y), -0.5 * (zm.x - zn.x));
-        const double2 v = p ? csub(x1, x2) : cadd(x1, x2);
-        G[g_index(g, p, m, jp, s)] = cscale(b, v);
+        G[g_index(g, 0, m, jp, s)] = cscale(b, cadd(x1, x2));
+        G[g_index(g, 1, m, jp, s)] = cscale(b, csub(x1, x2));
     }
 }
 
+#ifndef SGL_AZR_REGSTAGE
+#define SGL_AZR_REGSTAGE 1
+#endif
+#ifndef SGL_AZR_ZPRE
+#define SGL_AZR_ZPRE 1
+#endif
 template <int N>
 __global__ void __launch_bounds__(FFTShape<N>::THREADS, FFTShape<N>::MINB)
 az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict__ X, size_t fstride,
@@ -579,6 +585,54 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
     const int jp = blockIdx.y;
     const int s0 = blockIdx.x * IGR;
     const int nshell = g.batch * g.SC;
+#if SGL_AZR_REGSTAGE
+    // all of this thread's G loads in flight before the first shared store (as in
+    // az_inverse_kernel); the cp.async form ran its shared-memory side at 8x the
+    // ideal wavefronts (ncu, round 2)
+    constexpr int PER = 2 * B * IGR / S::THREADS;
+    static_assert(PER * S::THREADS == 2 * B * IGR, "prologue must divide evenly");
+    double2 pv[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int idx = tid + q * S::THREADS;
+        const int sl = idx % IGR;
+        const int rowi = idx / IGR;  // p * B + m
+        const int p = rowi / B, m = rowi - p * B;
+        const int s = s0 + sl;
+        pv[q] = s < nshell ? ld_stream(G + g_index(g, p, m, jp, s)) : make_double2(0.0, 0.0);
+    }
+#if SGL_AZR_ZPRE
+    // the thread holds E (q) and O (q + PER / 2) of the same (shell, m): form the
+    // packed FFT input here, Z[m] = X1 + i X2 and Z[N - m] = conj X1 + i conj X2
+    // (X1 = E + O, X2 = E - O; Z[B] = 0), written in natural order so that the
+    // first FFT pass reads the ring like the complex path
+    static_assert(PER % 2 == 0, "E and O of one bin in one thread");
+#pragma unroll
+    for (int q = 0; q < PER / 2; ++q) {
+        const int idx = tid + q * S::THREADS;
+        const int sl = idx % IGR;
+        const int m = idx / IGR;  // rowi < B: p = 0
+        const double2 e = pv[q], o = pv[q + PER / 2];
+        const double2 x1 = cadd(e, o), x2 = csub(e, o);
+        double2* ring = eo + sl * EOS;
+        if (m == 0) {
+            ring[phys(0)] = make_double2(x1.x, x2.x);
+            ring[phys(B)] = make_double2(0.0, 0.0);
+        } else {
+            ring[phys(m)] = make_double2(x1.x - x2.y, x1.y + x2.x);
+            ring[phys(N - m)] = make_double2(x1.x + x2.y, x2.x - x1.y);
+        }
+    }
+#else
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int idx = tid + q * S::THREADS;
+        const int sl = idx % IGR;
+        const int rowi = idx / IGR;
+        eo[sl * EOS + rowi] = pv[q];
+    }
+#endif
+#else
 #pragma unroll 4
     for (int idx = tid; idx < 2 * B * IGR; idx += S::THREADS) {
         const int sl = idx % IGR;
@@ -593,6 +647,7 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
         }
     }
     cp_async_wait_all();
+#endif
     __syncthreads();
     {
         const int q = tid / S::T, tt = tid - q * S::T;
@@ -608,6 +663,7 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
         }
         double2* ring = rings + q * S::STRIDE;
         auto in = [&](int bin) {
+            if (SGL_AZR_REGSTAGE && SGL_AZR_ZPRE) return e_buf[phys(bin)];  // formed in the prologue
             if (bin == B) return make_double2(0.0, 0.0);
             const int m = bin < B ? bin : N - bin;
             const double2 e = e_buf[m], o = e_buf[B + m];
