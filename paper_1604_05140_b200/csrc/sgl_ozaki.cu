@@ -414,19 +414,20 @@ __device__ __forceinline__ void tmem_ld16x256x2(uint32_t taddr, int (&v)[8]) {
                  : "r"(taddr));
 }
 
-template <int KPMAX>
+template <int KPMAX, int NT>
 __global__ void __launch_bounds__(512, 1) leginv_ws_kernel(const __grid_constant__ LegInvI8 P) {
-    constexpr int NR = kDigits * kWsN;      // 224 stacked data-digit rows
+    constexpr int NR = kDigits * NT;        // stacked data-digit rows (224 / 448)
     constexpr int SB = KPMAX * NR;          // bytes per data stage
-    constexpr int TM = kLevels * kWsN;      // 224 TMEM columns per buffer
+    constexpr int TM = kLevels * NT;        // TMEM columns per buffer
+    constexpr int NBUF = 2 * TM <= 512 ? 2 : 1;  // TMEM buffers (64-column tiles: one, drained early)
     constexpr int NPW = 7;                  // producer warps (9 .. 15)
-    constexpr int CPT = (KPMAX / 16 + NPW - 1) / NPW;  // 16-deep k chunks per producer thread
+    constexpr int CPT = (NT * (KPMAX / 16) + 32 * NPW - 1) / (32 * NPW);  // (column, 16-deep k chunk) pairs per thread
     constexpr int FST = KPMAX > 64 ? 1 : 3;            // fp64 staging buffers (tiles in flight)
     extern __shared__ __align__(128) uint8_t sm[];
     uint8_t* sA = sm;
     uint8_t* sB = sm + kDigits * KPMAX * kTileM;
     double* sF = reinterpret_cast<double*>(sB + 2 * SB);
-    __shared__ int colE[4][kWsN];
+    __shared__ int colE[4][NT];
     // 0 table, 1-2 data full, 3-4 data empty, 5-6 TMEM full, 7-8 TMEM empty
     __shared__ __align__(8) unsigned long long bars[9];
     __shared__ uint32_t tmem_base;
@@ -434,7 +435,7 @@ __global__ void __launch_bounds__(512, 1) leginv_ws_kernel(const __grid_constant
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const Geo& g = P.g;
     const int B = g.B, NB = (int)g.NB;
-    const int ntl = (NB + kWsN - 1) / kWsN;  // column tiles of a sign half
+    const int ntl = (NB + NT - 1) / NT;  // column tiles of a sign half
     const int rs = g_rowstride(g);
     auto bar = [&](int i) { return su32(&bars[i]); };
     if (tid == 0) {
@@ -478,17 +479,21 @@ __global__ void __launch_bounds__(512, 1) leginv_ws_kernel(const __grid_constant
             // The fp64 tile is staged by cp.async (8-byte copies, one row of 32
             // columns per warp instruction), FST - 1 tiles ahead.
             if (tid == 288) bulk_load(su32(sA), P.img + P.img_off[tix], (uint32_t)(kDigits * Kp * kTileM), bar(0));
-            const int pt = tid - 288, c = pt & 31, wp = pt >> 5;
+            const int pt = tid - 288, wp = pt >> 5;
             const int nkc = Kp / 16;
             auto stage_tile = [&](int t) {  // cp.async of tile t's S rows into staging buffer (T0 + t) % FST
-                const int nloc0 = t * kWsN, ncols = min(kWsN, NB - nloc0), n0 = u.half * NB + nloc0;
-                if (c < ncols) {
-                    const double* src = P.S + s_col(g, P.sv, am, n0 + c);
-                    double* dst = sF + ((T0 + t) % FST) * (KPMAX * kWsN) + c;
-                    for (int k = wp; k < K; k += NPW) {
-                        const long long l = am + p + 2 * k;
-                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(su32(dst + k * kWsN)),
-                                     "l"(src + l * (l + 1) * P.sv.NB));
+                const int nloc0 = t * NT, ncols = min(NT, NB - nloc0), n0 = u.half * NB + nloc0;
+#pragma unroll
+                for (int cc = 0; cc < NT / 32; ++cc) {
+                    const int c = lane + 32 * cc;
+                    if (c < ncols) {
+                        const double* src = P.S + s_col(g, P.sv, am, n0 + c);
+                        double* dst = sF + ((T0 + t) % FST) * (KPMAX * NT) + c;
+                        for (int k = wp; k < K; k += NPW) {
+                            const long long l = am + p + 2 * k;
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(su32(dst + k * NT)),
+                                         "l"(src + l * (l + 1) * P.sv.NB));
+                        }
                     }
                 }
                 cp_async_commit();
@@ -500,7 +505,7 @@ __global__ void __launch_bounds__(512, 1) leginv_ws_kernel(const __grid_constant
             }
             for (int t = 0; t < ntl; ++t) {
                 const int T = T0 + t, s = T & 1;
-                const int ncols = min(kWsN, NB - t * kWsN);
+                const int ncols = min(NT, NB - t * NT);
                 if (FST == 3) {
                     if (t + 2 < ntl) stage_tile(t + 2);
                     else cp_async_commit();
@@ -509,27 +514,30 @@ __global__ void __launch_bounds__(512, 1) leginv_ws_kernel(const __grid_constant
                     cp_async_wait_group<0>();
                 }
                 if (T >= 2) bar_wait(bar(3 + s), ((T >> 1) - 1) & 1);  // the MMAs of tile T - 2 have read stage s
-                if (pt < kWsN) colE[T & 3][pt] = 0;
+                if (pt < NT) colE[T & 3][pt] = 0;
                 named_sync(1, 32 * NPW);
                 double v[CPT][16];
                 {
-                    int mE = 0;
-                    const double* fs = sF + (T % FST) * (KPMAX * kWsN) + c;
+                    const double* fs = sF + (T % FST) * (KPMAX * NT);
 #pragma unroll
                     for (int ci = 0; ci < CPT; ++ci) {
-                        const int kc = wp + NPW * ci;
+                        const int pr = pt + 32 * NPW * ci, c = pr % NT, kc = pr / NT;
+                        int mE = 0;
 #pragma unroll
                         for (int r = 0; r < 16; ++r) {
                             const int k = kc * 16 + r;
-                            const double x = (k < K && c < ncols) ? fs[k * kWsN] : 0.0;
+                            const double x = (k < K && c < ncols && kc < nkc) ? fs[k * NT + c] : 0.0;
                             v[ci][r] = x;
                             mE = max(mE, exp_bits(x));
                         }
+                        if (mE) atomicMax(&colE[T & 3][c], mE);
                     }
-                    if (mE) atomicMax(&colE[T & 3][c], mE);
                 }
                 named_sync(1, 32 * NPW);
-                {
+#pragma unroll
+                for (int ci = 0; ci < CPT; ++ci) {
+                    const int pr = pt + 32 * NPW * ci, c = pr % NT, kc = pr / NT;
+                    if (kc >= nkc) continue;
                     // X = trunc(x 2^(55 - e)) + 2^55 (e = cE - 1022; the scale as the product of
                     // two normal powers of two: exact down to subnormals), F2I.S64, PRMT planes
                     const int cE = colE[T & 3][c];
@@ -537,30 +545,25 @@ __global__ void __launch_bounds__(512, 1) leginv_ws_kernel(const __grid_constant
                     const double s2 = __longlong_as_double((long long)(e2 + 1023) << 52);
                     const double s1 = __longlong_as_double((long long)(max(0, e - e2) + 1023) << 52);
                     auto fx = [&](double x) { return __double2ll_rz(x * s1 * s2) + (1LL << 55); };
+                    uint8_t* dst = sB + s * SB + kc * (NR * 16) + c * 16;
 #pragma unroll
-                    for (int ci = 0; ci < CPT; ++ci) {
-                        const int kc = wp + NPW * ci;
-                        if (kc >= nkc) continue;
-                        uint8_t* dst = sB + s * SB + kc * (NR * 16) + c * 16;
+                    for (int qd = 0; qd < 4; ++qd) {
+                        const long long X0 = fx(v[ci][4 * qd]), X1 = fx(v[ci][4 * qd + 1]), X2 = fx(v[ci][4 * qd + 2]),
+                                        X3 = fx(v[ci][4 * qd + 3]);
+                        const uint32_t l0 = (uint32_t)X0, l1 = (uint32_t)X1, l2 = (uint32_t)X2, l3 = (uint32_t)X3;
+                        const uint32_t h0 = (uint32_t)(X0 >> 32), h1 = (uint32_t)(X1 >> 32), h2 = (uint32_t)(X2 >> 32),
+                                       h3 = (uint32_t)(X3 >> 32);
 #pragma unroll
-                        for (int qd = 0; qd < 4; ++qd) {
-                            const long long X0 = fx(v[ci][4 * qd]), X1 = fx(v[ci][4 * qd + 1]), X2 = fx(v[ci][4 * qd + 2]),
-                                            X3 = fx(v[ci][4 * qd + 3]);
-                            const uint32_t l0 = (uint32_t)X0, l1 = (uint32_t)X1, l2 = (uint32_t)X2, l3 = (uint32_t)X3;
-                            const uint32_t h0 = (uint32_t)(X0 >> 32), h1 = (uint32_t)(X1 >> 32), h2 = (uint32_t)(X2 >> 32),
-                                           h3 = (uint32_t)(X3 >> 32);
+                        for (int bb = 0; bb < 4; ++bb) {
+                            const uint32_t sel = (uint32_t)(bb | ((bb + 4) << 4));
+                            reinterpret_cast<uint32_t*>(dst + (6 - bb) * (NT * 16))[qd] =
+                                __byte_perm(__byte_perm(l0, l1, sel), __byte_perm(l2, l3, sel), 0x5410);
+                        }
 #pragma unroll
-                            for (int bb = 0; bb < 4; ++bb) {
-                                const uint32_t sel = (uint32_t)(bb | ((bb + 4) << 4));
-                                reinterpret_cast<uint32_t*>(dst + (6 - bb) * (kWsN * 16))[qd] =
-                                    __byte_perm(__byte_perm(l0, l1, sel), __byte_perm(l2, l3, sel), 0x5410);
-                            }
-#pragma unroll
-                            for (int bb = 0; bb < 3; ++bb) {
-                                const uint32_t sel = (uint32_t)(bb | ((bb + 4) << 4));
-                                reinterpret_cast<uint32_t*>(dst + (2 - bb) * (kWsN * 16))[qd] =
-                                    __byte_perm(__byte_perm(h0, h1, sel), __byte_perm(h2, h3, sel), 0x5410);
-                            }
+                        for (int bb = 0; bb < 3; ++bb) {
+                            const uint32_t sel = (uint32_t)(bb | ((bb + 4) << 4));
+                            reinterpret_cast<uint32_t*>(dst + (2 - bb) * (NT * 16))[qd] =
+                                __byte_perm(__byte_perm(h0, h1, sel), __byte_perm(h2, h3, sel), 0x5410);
                         }
                     }
                 }
@@ -577,17 +580,22 @@ __global__ void __launch_bounds__(512, 1) leginv_ws_kernel(const __grid_constant
                 const uint32_t aA = su32(sA), aB = su32(sB);
                 const uint32_t pa = (uint32_t)(Kp * kTileM);
                 for (int t = 0; t < ntl; ++t) {
-                    const int T = T0 + t, s = T & 1, b = T & 1;
+                    const int T = T0 + t, s = T & 1, b = T % NBUF;
                     bar_wait(bar(1 + s), (T >> 1) & 1);
-                    if (T >= 2) bar_wait(bar(7 + b), ((T >> 1) - 1) & 1);
+                    if (T >= NBUF) bar_wait(bar(7 + b), ((T / NBUF) - 1) & 1);
                     fence_after();
                     for (int ks = 0; ks < Kp / 32; ++ks) {
-                        const uint64_t db = sdesc(aB + s * SB + ks * 2 * (NR * 16), NR * 16, 128);
+                        const uint32_t b0 = aB + s * SB + ks * 2 * (NR * 16);
 #pragma unroll
                         for (int i = 0; i < kDigits; ++i) {
                             const uint64_t da = sdesc(aA + i * pa + ks * 2 * (kTileM * 16), kTileM * 16, 128);
-                            mma_i8_1(td + (uint32_t)(b * TM + i * kWsN), da, db,
-                                     idesc_i8(kTileM, (kDigits - i) * kWsN, i == 0, false), (ks | i) ? 1u : 0u);
+                            const int rows = (kDigits - i) * NT;
+#pragma unroll
+                            for (int a0 = 0; a0 < rows; a0 += 256) {
+                                const int n = min(256, rows - a0);
+                                mma_i8_1(td + (uint32_t)(b * TM + i * NT + a0), da, sdesc(b0 + a0 * 16, NR * 16, 128),
+                                         idesc_i8(kTileM, n, i == 0, false), (ks | i) ? 1u : 0u);
+                            }
                         }
                     }
                     mma_commit_1(bar(3 + s));
@@ -618,18 +626,18 @@ __global__ void __launch_bounds__(512, 1) leginv_ws_kernel(const __grid_constant
             double* outa = P.G + (long long)ja * rs;
             double* outb = P.G + (long long)(ja + 8) * rs;
             for (int t = 0; t < ntl; ++t) {
-                const int T = T0 + t, b = T & 1;
-                const int nloc0 = t * kWsN, ncols = min(kWsN, NB - nloc0), n0 = u.half * NB + nloc0;
-                bar_wait(bar(5 + b), (T >> 1) & 1);
+                const int T = T0 + t, b = T % NBUF;
+                const int nloc0 = t * NT, ncols = min(NT, NB - nloc0), n0 = u.half * NB + nloc0;
+                bar_wait(bar(5 + b), (T / NBUF) & 1);
                 fence_after();
                 const uint32_t ta = td + ((uint32_t)(q * 32 + h * 16) << 16) + (uint32_t)(b * TM);
 #pragma unroll
-                for (int cp = 0; cp < 2; ++cp) {
+                for (int cp = 0; cp < NT / 16; ++cp) {
                     int a[kLevels][8];
 #pragma unroll
-                    for (int lv = 0; lv < kLevels; ++lv) tmem_ld16x256x2(ta + (uint32_t)(lv * kWsN + cp * 16), a[lv]);
+                    for (int lv = 0; lv < kLevels; ++lv) tmem_ld16x256x2(ta + (uint32_t)(lv * NT + cp * 16), a[lv]);
                     tmem_wait_ld();
-                    if (cp == 1) {  // this warp's last TMEM load of the buffer
+                    if (cp == NT / 16 - 1) {  // this warp's last TMEM load of the buffer
                         fence_before();
                         __syncwarp();
                         if (lane == 0) bar_arrive(bar(7 + b));
@@ -682,10 +690,16 @@ __global__ void __launch_bounds__(512, 1) leginv_ws_kernel(const __grid_constant
     if (warp == 8) tmem_dealloc(td, 512);
 }
 
+int ws_tile_columns(int B) {
+    const char* e = std::getenv("SGL_I8_WSN");
+    return (B <= 128 && e && std::atoi(e) == 64) ? 64 : 32;
+}
+
 size_t leginv_ws_smem(int B) {
     const int kp = B > 128 ? 128 : 64;
     const int fst = B > 128 ? 1 : 3;  // fp64 staging buffers (FST in the kernel)
-    return (size_t)kDigits * kp * kTileM + 2 * (size_t)kp * kDigits * kWsN + (size_t)fst * kp * kWsN * 8;
+    const int nt = ws_tile_columns(B);
+    return (size_t)kDigits * kp * kTileM + 2 * (size_t)kp * kDigits * nt + (size_t)fst * kp * nt * 8;
 }
 
 int launch_legendre_inverse_ws(const LegInvI8& prm_in, int nunits, cudaStream_t s) {
@@ -694,14 +708,19 @@ int launch_legendre_inverse_ws(const LegInvI8& prm_in, int nunits, cudaStream_t 
     prm.nunits = nunits;
     if (cudaMemsetAsync(prm.counter, 0, sizeof(int), s) != cudaSuccess) return -1;
     const size_t smem = leginv_ws_smem(prm.g.B);
+    const int grid = std::min(nunits, prm.grid);
     if (prm.g.B > 128) {
         static SmemAttrOnce attr;
-        attr.ensure(leginv_ws_kernel<128>, smem);
-        leginv_ws_kernel<128><<<std::min(nunits, prm.grid), 512, smem, s>>>(prm);
+        attr.ensure(leginv_ws_kernel<128, 32>, smem);
+        leginv_ws_kernel<128, 32><<<grid, 512, smem, s>>>(prm);
+    } else if (ws_tile_columns(prm.g.B) == 64) {
+        static SmemAttrOnce attr;
+        attr.ensure(leginv_ws_kernel<64, 64>, smem);
+        leginv_ws_kernel<64, 64><<<grid, 512, smem, s>>>(prm);
     } else {
         static SmemAttrOnce attr;
-        attr.ensure(leginv_ws_kernel<64>, smem);
-        leginv_ws_kernel<64><<<std::min(nunits, prm.grid), 512, smem, s>>>(prm);
+        attr.ensure(leginv_ws_kernel<64, 32>, smem);
+        leginv_ws_kernel<64, 32><<<grid, 512, smem, s>>>(prm);
     }
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
