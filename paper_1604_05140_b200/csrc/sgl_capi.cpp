@@ -163,7 +163,8 @@ struct sglgpu_plan {
         int* kpad = nullptr;
         int* corr = nullptr;
         int mtiles = 1;
-    } oz_li;
+    } oz_li;  // built on the first INT8 call (ensure_oz_li), not at plan creation
+    size_t leg_count = 0;  // doubles of d_leg
     std::map<std::tuple<long long, int, int>, std::pair<sglk::oz::Unit*, int>> oz_units;
     Work main;  // workspaces of device-memory calls and the stage entry points (under mu)
     std::vector<std::unique_ptr<HostSlot>> slots;  // host-memory calls (acquired under mu)
@@ -354,11 +355,34 @@ int i8_tpc() {
     return e ? std::max(1, std::atoi(e)) : 4;
 }
 
+// The INT8 Legendre-inverse table image (sgl_ozaki.cu), built from the plan's
+// Legendre table on the first call that asks for it: the opt-in path costs
+// default users neither plan-creation time nor memory.  Called outside graph
+// capture (graphs are captured from the second call of a shape on).
+void ensure_oz_li(sglgpu_plan* p) {
+    std::lock_guard<std::mutex> meta(p->meta_mu);
+    if (p->oz_li.img) return;
+    const int B = p->B;
+    std::vector<double> leg(p->leg_count);
+    std::vector<long long> off(2 * B + 1);
+    ck(cudaMemcpy(leg.data(), p->d_leg, leg.size() * sizeof(double), cudaMemcpyDeviceToHost), "download(legendre)");
+    ck(cudaMemcpy(off.data(), p->d_leg_off, off.size() * sizeof(long long), cudaMemcpyDeviceToHost),
+       "download(legendre_off)");
+    const auto im = sglk::oz::build_leginv_image(B, leg, off);
+    p->oz_li.off = dev_upload(im.off);
+    p->oz_li.rexp = dev_upload(im.rexp);
+    p->oz_li.kpad = dev_upload(im.kpad);
+    p->oz_li.corr = dev_upload(im.corr);
+    p->oz_li.mtiles = im.mtiles;
+    p->oz_li.img = dev_upload(im.bytes);
+}
+
 // Legendre inverse: the INT8 tensor-core kernel when enabled, else the DMMA GEMM.
 int leginv(sglgpu_plan* p, Work& w, const sglk::Geo& g, const sglk::SView& sv, const double* S, double* G,
            std::pair<sglk::TileMap*, int> lt, cudaStream_t st) {
-    const bool ws = p->oz_li.img && i8_on("ws");
-    if (ws || (p->oz_li.img && i8_on("leginv"))) {
+    const bool ws = i8_on("ws");
+    if (ws || i8_on("leginv")) {
+        ensure_oz_li(p);
         const int tpc = ws ? -1 : i8_tpc();
         std::pair<sglk::oz::Unit*, int> un;
         {
@@ -1113,15 +1137,7 @@ int sglgpu_plan_create(const sglgpu_plan_desc* desc, sglgpu_plan** out) {
             p->d_V_off = dev_upload(t.radial_inv_off);
             p->d_r = dev_upload(std::vector<double>(desc->r, desc->r + 2 * B));
             p->d_amod = dev_upload(std::vector<double>(desc->a_mod, desc->a_mod + 2 * B));
-            {
-                const auto im = sglk::oz::build_leginv_image(B, t.legendre, t.legendre_off);
-                p->oz_li.img = dev_upload(im.bytes);
-                p->oz_li.off = dev_upload(im.off);
-                p->oz_li.rexp = dev_upload(im.rexp);
-                p->oz_li.kpad = dev_upload(im.kpad);
-                p->oz_li.corr = dev_upload(im.corr);
-                p->oz_li.mtiles = im.mtiles;
-            }
+            p->leg_count = t.legendre.size();
         } catch (...) {
             sglgpu_plan_destroy(p);
             throw;
