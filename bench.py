@@ -313,7 +313,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--B", type=int, default=128)
     ap.add_argument("--batch", type=int, default=1)
-    ap.add_argument("--e2e-steps", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=32)
     ap.add_argument("--e2e-callers", type=int, default=4,
                     help="host threads issuing the e2e round trips concurrently (PCIe full duplex)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
