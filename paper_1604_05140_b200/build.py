@@ -18,7 +18,7 @@ LIB = os.path.join(PKG, "libsglb200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CUDA_SOURCES = ["sgl_kernels.cu", "sgl_separated.cu", "sgl_ozaki.cu"]
+CUDA_SOURCES = ["sgl_kernels.cu", "sgl_separated.cu", "sgl_ozaki.cu", "sgl_small.cu"]
 CXX_SOURCES = ["sgl_tables.cpp", "sgl_capi.cpp", "sgl_api.cpp", "sgl_host.cpp"]
 
 

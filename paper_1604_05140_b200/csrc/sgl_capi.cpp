@@ -541,9 +541,28 @@ int fused_slice_shells(int B, int nb, int lgib) {
     return sls;
 }
 
+// The fused small-bandlimit path (sgl_small.cu) for 2B <= 32 and batches of at most
+// kSmallBatch functions (beyond that the staged path's wide kernels win: B = 16,
+// 4 functions 157k vs 116k transforms/s, 16 functions 306k vs 369k);
+// SGL_SMALL=0 turns it off.
+constexpr int kSmallBatch = 8;
+bool small_on(int B, int nb) {
+    if (!sglk::small_path_ok(B) || nb > kSmallBatch) return false;
+    const char* e = std::getenv("SGL_SMALL");
+    return !(e && e[0] == '0');
+}
+
 int forward_device(sglgpu_plan* p, Work& w, const double* X, double* C, int nb, cudaStream_t st) {
     const int B = p->B;
     const size_t psi2 = 2 * (size_t)sample_count(B), om2 = 2 * (size_t)coefficient_count(B);
+    if (small_on(B, nb)) {
+        const int k = staged(p, 6, st, [&] {
+            return sglk::launch_small_forward(B, nb, X, (long long)psi2 / 2, C, (long long)om2 / 2, p->d_leg, p->d_W,
+                                              p->d_bcal, p->d_tw, st);
+        });
+        ck_launch(k, "small_forward");
+        return k;
+    }
     const Slices sl = plan_slices(B, nb);
     w.S.ensure((size_t)4 * B * B * B * nb);
     int n = 0, k;
@@ -639,6 +658,14 @@ int forward_device(sglgpu_plan* p, Work& w, const double* X, double* C, int nb, 
 int inverse_device(sglgpu_plan* p, Work& w, const double* C, double* X, int nb, cudaStream_t st) {
     const int B = p->B;
     const size_t psi2 = 2 * (size_t)sample_count(B), om2 = 2 * (size_t)coefficient_count(B);
+    if (small_on(B, nb)) {
+        const int k = staged(p, 7, st, [&] {
+            return sglk::launch_small_inverse(B, nb, C, (long long)om2 / 2, X, (long long)psi2 / 2, p->d_leg, p->d_V,
+                                              p->d_tw, st);
+        });
+        ck_launch(k, "small_inverse");
+        return k;
+    }
     const Slices sl = plan_slices(B, nb);
     w.S.ensure((size_t)4 * B * B * B * nb);
     int n = 0, k;

@@ -31,6 +31,16 @@ struct SmemAttrOnce {
         if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess)
             done.fetch_or(bit, std::memory_order_release);
     }
+    template <class Kernel>
+    void ensure_attr(Kernel k, cudaFuncAttribute a, int v) {  // any other attribute, same once-per-device rule
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+        const unsigned long long bit = 1ULL << dev;
+        if (done.load(std::memory_order_acquire) & bit) return;
+        std::lock_guard<std::mutex> lock(mu);
+        if (done.load(std::memory_order_relaxed) & bit) return;
+        if (cudaFuncSetAttribute(k, a, v) == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+    }
 };
 
 
@@ -228,6 +238,15 @@ int launch_radial_forward(const Geo& g, const RadialBlocks& rb, const double* S,
 int launch_radial_inverse(const Geo& g, const RadialBlocks& rb, const double* C, double* S,
                           const double* V, const long long* v_off, const TileMap* tiles, int ntiles,
                           cudaStream_t s);
+
+// Small bandlimits (sgl_small.cu): the whole transform of 2B <= 32 in one launch
+// per direction (per-shell fusion of the three stages; the forward's radial sum
+// reduced across a cluster of CTAs).  Strides in complex elements per function.
+bool small_path_ok(int B);
+int launch_small_inverse(int B, int batch, const double* C, long long c_stride, double* X, long long x_stride,
+                         const double* leg, const double* V, const double* tw, cudaStream_t s);
+int launch_small_forward(int B, int batch, const double* X, long long x_stride, double* C, long long c_stride,
+                         const double* leg, const double* W, const double* bcal, const double* tw, cudaStream_t s);
 
 // On-device cross-oracle (sgl_separated.cu): the reference's separated transforms
 // with closed-form basis values, direct quadratures, no tables.  shells: scratch

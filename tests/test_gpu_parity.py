@@ -782,3 +782,26 @@ def test_int8_tensor_core_legendre_inverse_matches_oracle(B, mode, monkeypatch):
     g0 = sgl.ifsglft_batch(plan, torch.from_numpy(c).cuda()).cpu().numpy()
     for b in range(2):
         assert per_shell(g[b], g0[b], B) <= TOL
+
+
+@pytest.mark.parametrize("B,nb", [(1, 1), (2, 3), (4, 1), (8, 2), (16, 1), (16, 8)])
+def test_fused_small_bandlimit_path_matches_general_path_and_oracle(B, nb, monkeypatch):
+    """The one-launch-per-direction small-bandlimit kernels (2B <= 32, sgl_small.cu,
+    the default there) against the oracle and against the general staged path
+    (SGL_SMALL=0) on the same batch (up to the path's batch cap of 8 functions)."""
+    import torch
+
+    plan, orc = plan_for(B)
+    rng = np.random.default_rng(900 + 10 * B + nb)
+    c = torch.from_numpy(complex_normal(rng, (nb, coefficient_count(B)))).cuda()
+    x = torch.from_numpy(complex_normal(rng, (nb, sample_count(B)))).cuda()
+    g = sgl.ifsglft_batch(plan, c).cpu().numpy()
+    f = sgl.fsglft_batch(plan, x).cpu().numpy()
+    monkeypatch.setenv("SGL_SMALL", "0")
+    g0 = sgl.ifsglft_batch(plan, c).cpu().numpy()
+    f0 = sgl.fsglft_batch(plan, x).cpu().numpy()
+    cn, xn = c.cpu().numpy(), x.cpu().numpy()
+    for b in range(nb):
+        assert per_shell(g[b], orc.inverse(cn[b]), B) <= TOL
+        assert normwise(f[b], orc.forward(xn[b])) <= TOL
+        assert normwise(g[b], g0[b]) <= 1e-14 and normwise(f[b], f0[b]) <= 1e-14
