@@ -98,10 +98,28 @@ struct DevBuf {
 // the work-queue counters of the fused kernels.
 struct Work {
     DevBuf G, S, counters;
+    // pipelined spherical stage (SGL_PIPE): a second, high-priority stream for the
+    // azimuthal launches and the events that chain them to the Legendre launches
+    cudaStream_t st2 = nullptr;
+    cudaEvent_t pev[10] = {};
+    void ensure_pipe() {
+        if (st2) return;
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        const char* e = std::getenv("SGL_PIPE_PRIO");
+        const int pr = e && e[0] == '0' ? lo : hi;  // default: the azimuthal stream has priority
+        ck(cudaStreamCreateWithPriority(&st2, cudaStreamNonBlocking, pr), "cudaStreamCreateWithPriority");
+        for (cudaEvent_t& ev : pev) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+    }
     void release() {
         G.release();
         S.release();
         counters.release();
+        if (st2) {
+            cudaStreamDestroy(st2);
+            for (cudaEvent_t& ev : pev) cudaEventDestroy(ev);
+            st2 = nullptr;
+        }
     }
 };
 
@@ -169,7 +187,7 @@ struct sglgpu_plan {
     Work main;  // workspaces of device-memory calls and the stage entry points (under mu)
     std::vector<std::unique_ptr<HostSlot>> slots;  // host-memory calls (acquired under mu)
     std::condition_variable slot_cv;
-    std::map<std::tuple<int, int, int, int, int>, std::pair<sglk::TileMap*, int>> tiles;
+    std::map<std::tuple<int, int, int, int, int, int, int>, std::pair<sglk::TileMap*, int>> tiles;
     std::mutex mu;       // device-memory calls, stage entry points, slot acquisition
     std::mutex meta_mu;  // the tile-map cache and the profiling records
     std::atomic<int> last_launches{0};
@@ -228,9 +246,13 @@ void problem_shape(Kind kind, int B, int batch, long long NB, int pid, bool real
 // Tile table for one grouped contraction (problems heaviest tile first), cached
 // per shape.  Each problem gets the warp layout wm with the fewest
 // (32 wm) x (128 / wm) tiles; SGL_WM_LEG / SGL_WM_RAD force one.
+// sub_n > 0 restricts a Legendre launch to a sub-range of its tiles (the pipelined
+// spherical stage): row blocks [sub_lo, sub_lo + sub_n) of every problem for the
+// Legendre inverse (a slab of polar nodes), n-blocks [sub_lo, sub_lo + sub_n) of
+// every sign half for the Legendre forward (a range of shells).
 std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int SC, int lo, int hi,
-                                         bool real = false) {
-    const auto key = std::make_tuple((int)kind + (real ? 16 : 0), batch, SC, lo, hi);
+                                         bool real = false, int sub_lo = 0, int sub_n = 0) {
+    const auto key = std::make_tuple((int)kind + (real ? 16 : 0), batch, SC, lo, hi, sub_lo, sub_n);
     std::lock_guard<std::mutex> meta(p->meta_mu);
     auto it = p->tiles.find(key);
     if (it != p->tiles.end()) return it->second;
@@ -281,11 +303,20 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
                          : kind == kRadFwd ? SGL_MAXWM_RADFWD : SGL_MAXWM_RADINV;
         while ((1 << lwm) > max_wm) --lwm;
         const int bm = 32 << lwm, bn = 128 >> lwm;
-        const int tm = (M + bm - 1) / bm;
-        const long long tn = (half + bn - 1) / bn;
+        int tm = (M + bm - 1) / bm;
+        long long tn = (half + bn - 1) / bn;
         if (tn > (1 << 30) / 2) fail(SGLGPU_EINVAL, "tile table: problem too wide");
+        int mi0 = 0, ni0 = 0;
+        if (sub_n > 0 && kind == kLegInv) {
+            mi0 = sub_lo;
+            tm = std::min(sub_n, tm - sub_lo);
+        } else if (sub_n > 0 && kind == kLegFwd) {
+            ni0 = sub_lo;
+            tn = std::min<long long>(sub_n, tn - sub_lo);
+        }
+        if (tm <= 0 || tn <= 0) continue;
         const long long kk = std::max(K, 1);
-        ents.push_back({pid, lwm, halves, tm, (int)tn, 0, 0, 0,
+        ents.push_back({pid, lwm, halves, tm, (int)tn, 0, mi0, ni0,
                         (std::min(bm, M) + 7) / 8 * 8 * ((std::min<long long>(bn, half) + 7) / 8 * 8) * kk});
         ntiles += (long long)tm * halves * tn;
     }
@@ -303,6 +334,9 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
         if (ntiles < 2LL * 4 * p->num_sms) seq = 1;
         if (const char* e = std::getenv("SGL_SEQ")) seq = std::max(1, std::min(8, std::atoi(e)));
     }
+    if (kind == kRadInv && batch == 1 && !real) {  // RadInvSeq (one complex function)
+        if (const char* e = std::getenv("SGL_SEQ_RADINV")) seq = std::max(1, std::min(8, std::atoi(e)));
+    }
     if (seq == 1 && ntiles <= sglk::kMaxProblems) {  // one entry per tile, exact per-tile work
         std::vector<Entry> per;
         for (const Entry& e : ents) {
@@ -313,14 +347,37 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
             for (int mi = 0; mi < e.tm; ++mi)
                 for (int h = 0; h < e.halves; ++h)
                     for (int ni = 0; ni < e.tn; ++ni) {
-                        const long long rows = std::min(bm, M - mi * bm), cols = std::min<long long>(bn, half - (long long)ni * bn);
-                        per.push_back({e.pid, e.lwm, 1, 1, 1, h, mi, ni, (rows + 7) / 8 * 8 * ((cols + 7) / 8 * 8) * kk});
+                        const int gm = e.mi0 + mi, gn = e.ni0 + ni;
+                        const long long rows = std::min(bm, M - gm * bm), cols = std::min<long long>(bn, half - (long long)gn * bn);
+                        per.push_back({e.pid, e.lwm, 1, 1, 1, h, gm, gn, (rows + 7) / 8 * 8 * ((cols + 7) / 8 * 8) * kk});
                     }
         }
         ents.swap(per);
     }
+    // Legendre inverse, polar-slab-major order: all problems of row block mi (32
+    // nodes j') before the next block, so G is written slab by slab and the slab
+    // written last is still in L2 when the azimuthal inverse starts with it.
+    // SGL_LEGINV_ORDER: 0 = problem-major, 1 = slabs ascending, 2 = descending.
+    int slab_order = 0;
+    const bool per_tile = seq == 1 && ntiles <= sglk::kMaxProblems;  // expanded above
+    if (kind == kLegInv && !per_tile) {
+        if (const char* e = std::getenv("SGL_LEGINV_ORDER")) slab_order = std::atoi(e);
+        long long need = 0;
+        for (const Entry& e : ents) need += e.tm;
+        if (need > sglk::kMaxProblems) slab_order = 0;  // B = 256: 8 slabs x 512 problems
+        if (slab_order) {
+            std::vector<Entry> per;
+            for (const Entry& e : ents)
+                for (int mi = 0; mi < e.tm; ++mi)
+                    per.push_back({e.pid, e.lwm, e.halves, 1, e.tn, 0, e.mi0 + mi, e.ni0, e.work});
+            ents.swap(per);
+        }
+    }
     if ((int)ents.size() > sglk::kMaxProblems) fail(SGLGPU_EINVAL, "tile table: too many problems");
-    std::stable_sort(ents.begin(), ents.end(), [](const Entry& a, const Entry& b) { return a.work > b.work; });
+    std::stable_sort(ents.begin(), ents.end(), [slab_order](const Entry& a, const Entry& b) {
+        if (slab_order && a.mi0 != b.mi0) return slab_order == 1 ? a.mi0 < b.mi0 : a.mi0 > b.mi0;
+        return a.work > b.work;
+    });
     auto* tm = new sglk::TileMap{};
     long long n = 0;
     tm->nprob = (int)ents.size();
@@ -424,6 +481,18 @@ cudaEvent_t pool_event(sglgpu_plan* p) {
     cudaEvent_t e;
     ck(cudaEventCreate(&e), "cudaEventCreate");
     return e;
+}
+
+// Pipelined spherical stage of a single large transform (SGL_PIPE = slices, 0 = off):
+// the azimuthal kernels are HBM-bound and the Legendre kernels FP64-bound, so the
+// stage is cut into slices whose azimuthal and Legendre launches overlap on two
+// streams -- by shell range in the forward direction (az(k+1) || legendre(k)), by
+// slab of polar nodes in the inverse (legendre(k+1) || az(k)).
+int pipe_slices(int B, int nb) {
+    const char* e = std::getenv("SGL_PIPE");
+    const int ns = e ? std::atoi(e) : 0;
+    if (ns < 2 || nb != 1 || (B & (B - 1)) || B < 64) return 0;
+    return (B / 32) % ns == 0 ? ns : 0;
 }
 
 // Brackets one stage launch with events when profiling is on.
@@ -603,6 +672,35 @@ int forward_device(sglgpu_plan* p, Work& w, const double* X, double* C, int nb, 
         w.G.ensure(2 * (size_t)sglk::g_layout(gc));
         const sglk::SView sv{2LL * 2 * B, 2 * B, 0};
         auto lt = tiles_for(p, kLegFwd, 1, SC, 0, 2 * B);
+        if (const int ns = sl.count == 1 && !p->profiling ? pipe_slices(B, nb) : 0) {
+            w.ensure_pipe();
+            sglk::g_layout(gc);
+            const int gper = (int)(gc.ngx / ns);       // shell groups per slice
+            const int nper = (int)(gc.NB / 128 / ns);  // 128-column n-blocks per sign half and slice
+            if (gper > 0 && nper > 0 && (long long)gper * ns == gc.ngx && (long long)nper * ns * 128 == gc.NB) {
+                ck(cudaEventRecord(w.pev[8], st), "cudaEventRecord");
+                ck(cudaStreamWaitEvent(w.st2, w.pev[8], 0), "cudaStreamWaitEvent");
+                for (int c = 0; c < ns; ++c) {
+                    sglk::Geo ga = gc;
+                    ga.gx0 = c * gper;
+                    ga.gxn = gper;
+                    ck_launch(sglk::launch_az_forward(ga, X, psi2, w.G.p, p->d_bcal, p->d_tw, w.st2), "az_forward");
+                    ck(cudaEventRecord(w.pev[c], w.st2), "cudaEventRecord");
+                    ck(cudaStreamWaitEvent(st, w.pev[c], 0), "cudaStreamWaitEvent");
+                    auto ltc = tiles_for(p, kLegFwd, 1, SC, 0, 2 * B, false, c * nper, nper);
+                    ck_launch(sglk::launch_legendre_forward(gc, sv, w.G.p, w.S.p, p->d_leg, p->d_leg_off, ltc.first,
+                                                            ltc.second, st),
+                              "legendre_forward");
+                    n += 2;
+                }
+                sglk::Geo g{B, 2 * B, 1, 2LL * 2 * B};
+                auto rt = tiles_for(p, kRadFwd, 1, 2 * B, 0, B);
+                k = sglk::launch_radial_forward(g, sglk::RadialBlocks{2 * B, 0, 0}, w.S.p, C, p->d_W, p->d_W_off, rt.first,
+                                                rt.second, st);
+                ck_launch(k, "radial_forward");
+                return n + k;
+            }
+        }
         for (int c = 0; c < sl.count; ++c) {
             const int i0 = c * SC;
             k = staged(p, 0, st, [&] {
@@ -682,6 +780,25 @@ int inverse_device(sglgpu_plan* p, Work& w, const double* C, double* X, int nb, 
         sglk::Geo gc{B, SC, 1, 2LL * SC};
         w.G.ensure(2 * (size_t)sglk::g_layout(gc));
         auto lt = tiles_for(p, kLegInv, 1, SC, 0, 2 * B);
+        if (const int ns = sl.count == 1 && !p->profiling && !i8_on("ws") && !i8_on("leginv") ? pipe_slices(B, nb) : 0) {
+            w.ensure_pipe();
+            const int rb = B / 32 / ns;  // 32-node row blocks of the Legendre inverse per slab
+            const sglk::SView v{2LL * 2 * B, 2 * B, 0};
+            for (int c = 0; c < ns; ++c) {
+                auto ltc = tiles_for(p, kLegInv, 1, SC, 0, 2 * B, false, c * rb, rb);
+                ck_launch(leginv(p, w, gc, v, w.S.p, w.G.p, ltc, st), "legendre_inverse");
+                ck(cudaEventRecord(w.pev[c], st), "cudaEventRecord");
+                ck(cudaStreamWaitEvent(w.st2, w.pev[c], 0), "cudaStreamWaitEvent");
+                sglk::Geo ga = gc;
+                ga.jp0 = c * rb * 32;
+                ga.jpn = rb * 32;
+                ck_launch(sglk::launch_az_inverse(ga, w.G.p, X, psi2, p->d_tw, w.st2), "az_inverse");
+                n += 2;
+            }
+            ck(cudaEventRecord(w.pev[9], w.st2), "cudaEventRecord");
+            ck(cudaStreamWaitEvent(st, w.pev[9], 0), "cudaStreamWaitEvent");
+            return n;
+        }
         for (int c = 0; c < sl.count; ++c) {
             const int i0 = c * SC;
             const sglk::SView v{2LL * 2 * B, 2 * B, i0};

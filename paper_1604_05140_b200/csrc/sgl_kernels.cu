@@ -300,6 +300,29 @@ __device__ __forceinline__ void st_hint(double2* p, double2 v, unsigned long lon
                  : "memory");
 }
 
+// Round-trip L2 reuse (round 2): the grid the inverse writes last is what a
+// following forward reads first when the forward's CTAs run in reverse order
+// (SGL_AZF_REV), provided the inverse's stores stay in L2: SGL_AZI_STORE 0 =
+// st.global.cs (streaming), 1 = plain, 2 = L2 evict_last.  Measured at B = 128
+// (exp/l2order.sh, stage times): az_forward 95.8 -> 92.6 us reversed -> 91.0 with
+// plain stores -> 90.7 with evict_last (and the Legendre stages ~1 us faster).
+// The same trick for G (SGL_AZI_REV or the polar-slab-major tile order of the
+// Legendre inverse, SGL_LEGINV_ORDER in sgl_capi.cpp) costs the Legendre inverse
+// 3.3 us and gains the azimuthal inverse 1.7: off.  SGL_AZI_LOAD 1 = the G
+// loads marked L2 evict_first (no change).
+#ifndef SGL_AZF_REV
+#define SGL_AZF_REV 1
+#endif
+#ifndef SGL_AZI_REV
+#define SGL_AZI_REV 0
+#endif
+#ifndef SGL_AZI_STORE
+#define SGL_AZI_STORE 2
+#endif
+#ifndef SGL_AZI_LOAD
+#define SGL_AZI_LOAD 0
+#endif
+
 // ------------------------------------------------------------------ async copy helpers
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
@@ -416,7 +439,9 @@ __global__ void __launch_bounds__(FFTShape<N>::THREADS, FFTShape<N>::MINB)
 az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2* __restrict__ G,
                   const double* __restrict__ bcal, const double2* __restrict__ twg) {
     extern __shared__ double2 smem[];
-    az_fwd_item<N>(g, X, fstride, G, bcal, twg, blockIdx.x * FFTShape<N>::IG, blockIdx.y, smem);
+    const int bx = (SGL_AZF_REV ? gridDim.x - 1 - blockIdx.x : blockIdx.x) + g.gx0;
+    const int by = (SGL_AZF_REV ? gridDim.y - 1 - blockIdx.y : blockIdx.y) + g.jp0;
+    az_fwd_item<N>(g, X, fstride, G, bcal, twg, bx * FFTShape<N>::IG, by, smem);
 }
 
 // ------------------------------------------------------------------ azimuthal inverse
@@ -436,8 +461,8 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
     // per-pass tables in shared memory 125 us)
     double2* rings = smem;  // twiddles: per-pass tables from global (93 us; a shared-memory copy 104 us)
     const int tid = threadIdx.x;
-    const int jp = blockIdx.y;
-    const int s0 = blockIdx.x * S::IG;
+    const int jp = (SGL_AZI_REV ? gridDim.y - 1 - blockIdx.y : blockIdx.y) + g.jp0;
+    const int s0 = ((SGL_AZI_REV ? gridDim.x - 1 - blockIdx.x : blockIdx.x) + g.gx0) * S::IG;
     const int nshell = g.batch * g.SC;
     // prologue: all of this thread's G loads in flight before the first shared
     // store (a partially unrolled load -> store loop kept only 4 in flight)
@@ -456,7 +481,7 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
                                          : make_double2(0.0, 0.0);
 #else
         pv[q] = (bin != B && s < nshell)
-                    ? (SGL_L2HINTS ? ld_stream_hint(G + g_index(g, p, bin, jp, s), policy_evict_first())
+                    ? ((SGL_L2HINTS || SGL_AZI_LOAD) ? ld_stream_hint(G + g_index(g, p, bin, jp, s), policy_evict_first())
                                    : ld_stream(G + g_index(g, p, bin, jp, s)))
                     : make_double2(0.0, 0.0);
 #endif
@@ -492,7 +517,10 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
                 return mirror ? csub(e, o) : cadd(e, o);
             },
             [&](int x, double2 v) {
-                if (ok) __stcs(dst + x, v);
+                if (!ok) return;
+                if (SGL_AZI_STORE == 0) __stcs(dst + x, v);
+                else if (SGL_AZI_STORE == 1) dst[x] = v;
+                else st_hint(dst + x, v, policy_evict_last());
             });
     }
 }
@@ -1160,6 +1188,13 @@ struct LegFwdSlice : LegFwd {
 struct LegInvSeq : LegInv {  // CTAs run TileMap::seq consecutive n-blocks
     static constexpr bool GEMM_SEQ = true;
 };
+// Radial inverse of ONE complex function whose CTAs run consecutive n-blocks of a
+// degree (the coefficient columns 2 (l^2 + l + m) + c are then affine in n): the
+// short-K problems of high degree amortize the CTA prologue over the sequence.
+struct RadInvSeq : RadInv {
+    static constexpr bool GEMM_SEQ = true;
+    static constexpr bool B_COL_AFFINE = true;
+};
 // Radial forward of one rank's degree range under the multi-GPU split whose
 // coefficients are stored into every rank's coefficient vector (pd.base[q]; the
 // degree ranges are disjoint, so each entry is written by exactly one rank): the
@@ -1732,7 +1767,7 @@ static int az_fwd_launch(const Geo& g, const double* X, size_t fstride, double* 
     static SmemAttrOnce attr;
     attr.ensure(az_forward_kernel<N>, smem);
     const int nshell = g.batch * g.SC;
-    dim3 grid((nshell + S::IG - 1) / S::IG, g.B);
+    dim3 grid(g.gxn ? g.gxn : (nshell + S::IG - 1) / S::IG, g.jpn ? g.jpn : g.B);
     az_forward_kernel<N><<<grid, S::THREADS, smem, s>>>(g, reinterpret_cast<const double2*>(X), fstride / 2,
                                                          reinterpret_cast<double2*>(G), bcal,
                                                          reinterpret_cast<const double2*>(tw));
@@ -1748,7 +1783,7 @@ static int az_inv_launch(const Geo& g, const double* G, double* X, size_t fstrid
     static SmemAttrOnce attr;
     attr.ensure(az_inverse_kernel<N>, smem);
     const int nshell = g.batch * g.SC;
-    dim3 grid((nshell + S::IG - 1) / S::IG, g.B);
+    dim3 grid(g.gxn ? g.gxn : (nshell + S::IG - 1) / S::IG, g.jpn ? g.jpn : g.B);
     az_inverse_kernel<N><<<grid, S::THREADS, smem, s>>>(g, reinterpret_cast<const double2*>(G),
                                                          reinterpret_cast<double2*>(X), fstride / 2,
                                                          reinterpret_cast<const double2*>(tw));
@@ -2086,6 +2121,11 @@ int launch_radial_inverse(const Geo& g, const RadialBlocks& rb, const double* C,
                           const double* V, const long long* v_off, const TileMap* tiles, int ntiles,
                           cudaStream_t s) {
     RadInv p{g, V, v_off, C, S, degree_offset(g.B + 1), ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
+    if (ntiles > 0 && tiles->seq > 1 && g.batch == 1 && !g.real) {
+        RadInvSeq q;
+        static_cast<RadInv&>(q) = p;
+        return gemm_launch<RadInvSeq>(q, tiles, ntiles, s);
+    }
     return gemm_launch<RadInv>(p, tiles, ntiles, s);
 }
 

@@ -107,6 +107,9 @@ struct Geo {
     int lgib = 0;        // log2(shells per group) = log2 of the azimuthal kernel's tile
     int nbins = 0;       // bins per (p, shell): 2B (complex path, bin B unused) or B (real path)
     long long ngx = 0;   // shell groups = ceil(batch * SC / 2^lgib)
+    // Sub-range of the azimuthal launch (the pipelined spherical stage, sgl_capi.cpp):
+    // polar nodes j' in [jp0, jp0 + jpn) and shell groups [gx0, gx0 + gxn); 0 counts = all.
+    int jp0 = 0, jpn = 0, gx0 = 0, gxn = 0;
 };
 
 // Complex index of G(p, bin, j', flat shell s).
