@@ -2,11 +2,11 @@
 import sys, os, numpy as np, torch
 sys.path.insert(0, os.getcwd())
 import paper_1604_05140_b200 as sgl
-B = int(os.environ.get("B", 128)); steps = 50
+B = int(os.environ.get("B", 128)); steps = int(os.environ.get("STEPS", 50))
 plan = sgl.TransformPlan.compute(B, device=0)
 L = sgl.lib()
 n = sgl.coefficient_count(B)
-c = torch.randn(1, n, dtype=torch.complex128, device="cuda")
+c = torch.randn(int(os.environ.get("BATCH", 1)), n, dtype=torch.complex128, device="cuda")
 g = sgl.ifsglft_batch(plan, c); b = sgl.fsglft_batch(plan, g)
 ms = np.zeros(8); cnt = np.zeros(8, dtype=np.int32)
 assert L.sglgpu_profile_begin(plan.handle) == 0

@@ -310,6 +310,18 @@ __device__ __forceinline__ void st_hint(double2* p, double2 v, unsigned long lon
 // Legendre inverse, SGL_LEGINV_ORDER in sgl_capi.cpp) costs the Legendre inverse
 // 3.3 us and gains the azimuthal inverse 1.7: off.  SGL_AZI_LOAD 1 = the G
 // loads marked L2 evict_first (no change).
+// N = 512 (B = 256): the radix-2 pass of the (2, 16, 16) ring FFT fused into the
+// kernels' own shared-memory traffic -- forward as radices (16, 16) with the
+// final radix-2 butterfly done by the epilogue on its ring reads, inverse with
+// the leading radix-2 butterfly done in the prologue's registers (a thread holds
+// bins k and k + 256 of its rows): one shared-memory pass and one CTA barrier
+// fewer per direction.
+#ifndef SGL_AZ512_FUSE2
+#define SGL_AZ512_FUSE2 1
+#endif
+#ifndef SGL_AZI_EO_PRE
+#define SGL_AZI_EO_PRE 1
+#endif
 #ifndef SGL_AZF_REV
 #define SGL_AZF_REV 1
 #endif
@@ -388,6 +400,48 @@ __device__ __forceinline__ void az_fwd_item(const Geo& g, const double2* __restr
     constexpr int B = N / 2;
     const int tid = threadIdx.x;
     const int nshell = g.batch * g.SC;
+    if constexpr (N == 512 && SGL_AZ512_FUSE2) {
+        static_assert(N != 512 || (S::T == 32 && S::TWN == 1022), "N = 512 twiddle layout (sgl_tables.cpp)");
+        const int q = tid / S::T, tt = tid - q * S::T;
+        const int s = s0 + (q >> 1);
+        const int j = (q & 1) ? (N - 1 - jp) : jp;
+        const double2* src = X;
+        const bool ok = s < nshell;
+        if (ok) {
+            const int f = s / g.SC, i = s - f * g.SC;
+            src = X + (size_t)f * fstride + ((size_t)i * N + j) * N;
+        }
+        double2* ring = rings + q * S::STRIDE;
+        auto rd = [&](int x) { return ring[phys(x)]; };
+        auto wr = [&](int x, double2 v) { ring[phys(x)] = v; };
+        stockham_pass<N, 16, -1, false>(1, tt, twg, [&](int x) { return ok ? ld_stream(src + x) : make_double2(0.0, 0.0); },
+                                        wr);
+        __syncthreads();
+        stockham_pass<N, 16, -1, true>(16, tt, twg + S::TWN, rd, wr);
+        __syncthreads();
+        // epilogue: final radix-2 butterfly X[k] = y[k] + w^k y[k + 256], X[k + 256] = y[k] - w^k y[k + 256]
+        // (linear, so applied to the E/O fold of the ring pair), b_cal, blocked G rows
+        const double b = __ldg(bcal + jp);
+#pragma unroll 2
+        for (int idx = tid; idx < B * S::IG; idx += S::THREADS) {
+            const int sl = idx % S::IG, k = idx / S::IG;
+            const int sh = s0 + sl;
+            if (sh >= nshell) continue;
+            const double2* rj = rings + (2 * sl) * S::STRIDE;
+            const double2* rm = rj + S::STRIDE;
+            const double2 yj0 = rj[phys(k)], yj1 = rj[phys(k + B)], ym0 = rm[phys(k)], ym1 = rm[phys(k + B)];
+            const double2 w = __ldg(twg + k);
+            const double2 a0 = cadd(yj0, ym0), a1 = csub(yj0, ym0);
+            const double2 b0 = cmul(w, cadd(yj1, ym1)), b1 = cmul(w, csub(yj1, ym1));
+            G[g_index(g, 0, k, jp, sh)] = cscale(b, cadd(a0, b0));
+            G[g_index(g, 1, k, jp, sh)] = cscale(b, cadd(a1, b1));
+            if (k != 0) {  // bin B (Nyquist) is not part of G
+                G[g_index(g, 0, k + B, jp, sh)] = cscale(b, csub(a0, b0));
+                G[g_index(g, 1, k + B, jp, sh)] = cscale(b, csub(a1, b1));
+            }
+        }
+        return;
+    }
     {
         // twiddles come straight from the (L1-resident) per-pass global tables;
         // the ring loads go straight to registers (staging small-N rings through
@@ -486,6 +540,72 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
                     : make_double2(0.0, 0.0);
 #endif
     }
+    // ring values in the prologue's registers: a thread's loads q and q + PER / 2
+    // are E (p = 0) and O (p = 1) of the same (shell, bin), so ring j' = E + O and
+    // its mirror 2B-1-j' = E - O are formed here and every FFT pass reads its own
+    // ring only (SGL_AZI_EO_PRE, N >= 256: az_inverse 92.3 -> 89.8 us at B = 128,
+    // 914 -> 862 us at B = 256; at N <= 128 the two-ring stores conflict in shared
+    // memory -- B = 64 x 64: 733 -> 750 us -- so there the first pass still reads
+    // both parity buffers)
+    constexpr int HP = PER / 2;
+    static_assert(HP * S::THREADS == N * S::IG, "parity partner of load q is load q + PER / 2");
+    const int fq = tid / S::T, tt = tid - fq * S::T;  // FFT role: ring fq of the CTA, thread tt of the ring
+    const int fs = s0 + (fq >> 1);
+    const bool ok = fs < nshell;
+    double2* dst = X;
+    if (ok) {
+        const int f = fs / g.SC, i = fs - f * g.SC;
+        const int j = (fq & 1) ? (N - 1 - jp) : jp;
+        dst = X + (size_t)f * fstride + ((size_t)i * N + j) * N;
+    }
+    double2* ring = rings + fq * S::STRIDE;
+    auto st_out = [&](int x, double2 v) {
+        if (!ok) return;
+        if (SGL_AZI_STORE == 0) __stcs(dst + x, v);
+        else if (SGL_AZI_STORE == 1) dst[x] = v;
+        else st_hint(dst + x, v, policy_evict_last());
+    };
+    if constexpr (N == 512 && SGL_AZ512_FUSE2) {
+        // ... and the leading radix-2 butterfly of the (2, 16, 16) FFT: loads q and
+        // q + HQ are bins k and k + 256 of the same row
+        constexpr int HQ = (B * S::IG) / S::THREADS;
+        static_assert(HQ * S::THREADS == B * S::IG && PER == 4 * HQ, "prologue pairing");
+#pragma unroll
+        for (int q = 0; q < HQ; ++q) {
+            const int idx = tid + q * S::THREADS;
+            const int sl = idx % S::IG, k = idx / S::IG;  // k < B
+            const double2 xj0 = cadd(pv[q], pv[q + HP]), xm0 = csub(pv[q], pv[q + HP]);
+            const double2 xj1 = cadd(pv[q + HQ], pv[q + HQ + HP]), xm1 = csub(pv[q + HQ], pv[q + HQ + HP]);
+            double2* rj = rings + (2 * sl) * S::STRIDE;
+            double2* rm = rj + S::STRIDE;
+            // ring pairs sit 32 bytes apart (mod 128): odd shells store the odd
+            // element first so that a warp's 16-byte stores cover all banks
+            const int odd = sl & 1;
+            const double2 sj = cadd(xj0, xj1), dj = csub(xj0, xj1), sm = cadd(xm0, xm1), dm = csub(xm0, xm1);
+            rj[phys(2 * k + odd)] = odd ? dj : sj;
+            rj[phys(2 * k + 1 - odd)] = odd ? sj : dj;
+            rm[phys(2 * k + odd)] = odd ? dm : sm;
+            rm[phys(2 * k + 1 - odd)] = odd ? sm : dm;
+        }
+        __syncthreads();
+        stockham_pass<N, 16, +1, true>(2, tt, twg + N, [&](int x) { return ring[phys(x)]; },
+                                       [&](int x, double2 v) { ring[phys(x)] = v; });
+        __syncthreads();
+        stockham_pass<N, 16, +1, false>(32, tt, twg + N + 15 * 2, [&](int x) { return ring[phys(x)]; }, st_out);
+        return;
+    }
+    if constexpr (SGL_AZI_EO_PRE && N >= 256) {
+#pragma unroll
+    for (int q = 0; q < HP; ++q) {
+        const int idx = tid + q * S::THREADS;
+        const int sl = idx % S::IG, bin = idx / S::IG;
+        rings[(2 * sl) * S::STRIDE + phys(bin)] = cadd(pv[q], pv[q + HP]);
+        rings[(2 * sl + 1) * S::STRIDE + phys(bin)] = csub(pv[q], pv[q + HP]);
+    }
+    __syncthreads();
+    ring_fft_io<N, +1, true>(ring, tt, twg, [&](int x) { return ring[phys(x)]; }, st_out);
+    return;
+    }
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
         const int idx = tid + q * S::THREADS;
@@ -496,32 +616,16 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
     }
     __syncthreads();
     {
-        const int q = tid / S::T, tt = tid - q * S::T;
-        const int sl = q >> 1;
-        const int s = s0 + sl;
-        const bool mirror = q & 1;
-        const int j = mirror ? (N - 1 - jp) : jp;
-        double2* ring = rings + q * S::STRIDE;
-        const double2* e_buf = rings + (2 * sl) * S::STRIDE;
-        const double2* o_buf = rings + (2 * sl + 1) * S::STRIDE;
-        double2* dst = X;
-        const bool ok = s < nshell;
-        if (ok) {
-            const int f = s / g.SC, i = s - f * g.SC;
-            dst = X + (size_t)f * fstride + ((size_t)i * N + j) * N;
-        }
+        const bool mirror = fq & 1;
+        const double2* e_buf = rings + (fq & ~1) * S::STRIDE;
+        const double2* o_buf = e_buf + S::STRIDE;
         ring_fft_io<N, +1, true>(
             ring, tt, twg,
             [&](int x) {
                 const double2 e = e_buf[phys(x)], o = o_buf[phys(x)];
                 return mirror ? csub(e, o) : cadd(e, o);
             },
-            [&](int x, double2 v) {
-                if (!ok) return;
-                if (SGL_AZI_STORE == 0) __stcs(dst + x, v);
-                else if (SGL_AZI_STORE == 1) dst[x] = v;
-                else st_hint(dst + x, v, policy_evict_last());
-            });
+            st_out);
     }
 }
 

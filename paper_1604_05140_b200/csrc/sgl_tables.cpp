@@ -69,6 +69,17 @@ Tables build_tables(int B, const double* r, const double* a_mod, const double* b
                     t.twiddle.push_back((double)sinl(ang));
                 }
     }
+    // N = 512 forward (radices 16, 16 and a final radix 2 fused into the azimuthal
+    // kernel's epilogue, sgl_kernels.cu SGL_AZ512_FUSE2): the radix-16 pass with
+    // Ns = 16, appended after the (2, 16, 16) tables the inverse uses.
+    if (n2 == 512)
+        for (int rr = 1; rr < 16; ++rr)
+            for (int k = 0; k < 16; ++k) {
+                const long long x = ((long long)rr * k * (n2 / (16 * 16))) % n2;
+                const long double ang = -2.0L * kPiL * x / n2;
+                t.twiddle.push_back((double)cosl(ang));
+                t.twiddle.push_back((double)sinl(ang));
+            }
     t.bcal.assign(bcal, bcal + n2);
 
     // ---- normalized Legendre table, rows grouped by (|m|, parity); rows padded
