@@ -176,9 +176,15 @@ __device__ __forceinline__ void pair_sync() {
 // j R + r of a first-pass butterfly depends on j alone, so any butterfly-to-thread
 // assignment is valid there.
 struct NoPairLoad {};
-template <int N, int R, int SIGN, bool IN_PLACE, class Ld, class St, class Ld2 = NoPairLoad>
+// NS2 (radix 16 after a radix-2 pass, Ns = 2): the pass's twiddles are 1 (k = 0)
+// or e^{-+2 pi i r / 32} (k = 1) -- compile-time constants selected per thread
+// instead of 15 table loads (the N = 512 inverse was throttled on its global
+// load/store queue: lg_throttle in ncu).
+template <int N, int R, int SIGN, bool IN_PLACE, class Ld, class St, class Ld2 = NoPairLoad, bool NS2 = false>
 __device__ __forceinline__ void stockham_pass(int Ns, int t, const double2* twp, Ld&& ld, St&& st,
                                               Ld2&& ld2 = NoPairLoad{}) {
+    constexpr double kC32[16] = {1.00000000000000000000, 0.98078528040323043058, 0.92387953251128673848, 0.83146961230254523567, 0.70710678118654757274, 0.55557023301960228867, 0.38268343236508983729, 0.19509032201612833135, 0.00000000000000006123, -0.19509032201612819257, -0.38268343236508972627, -0.55557023301960195560, -0.70710678118654746172, -0.83146961230254534669, -0.92387953251128673848, -0.98078528040323043058};
+    constexpr double kS32[16] = {0.00000000000000000000, 0.19509032201612824808, 0.38268343236508978178, 0.55557023301960217765, 0.70710678118654746172, 0.83146961230254523567, 0.92387953251128673848, 0.98078528040323043058, 1.00000000000000000000, 0.98078528040323043058, 0.92387953251128673848, 0.83146961230254545772, 0.70710678118654757274, 0.55557023301960217765, 0.38268343236508989280, 0.19509032201612860891};
     constexpr int T = FFTShape<N>::T;
     constexpr int NBF = N / R;          // butterflies in this pass
     constexpr int PER = NBF / T;        // butterflies per thread
@@ -203,7 +209,13 @@ __device__ __forceinline__ void stockham_pass(int Ns, int t, const double2* twp,
     for (int b = 0; b < PER; ++b) {
         const int j = bj(b);
         const int k = j & (Ns - 1);
-        if (Ns > 1) {
+        if constexpr (NS2 && R == 16) {
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                const double2 w = make_double2(k ? kC32[r] : 1.0, k ? (SIGN > 0 ? kS32[r] : -kS32[r]) : 0.0);
+                v[b][r] = cmul(v[b][r], w);
+            }
+        } else if (Ns > 1) {
 #pragma unroll
             for (int r = 1; r < R; ++r) {
                 double2 w = twp[(r - 1) * Ns + k];
@@ -318,6 +330,9 @@ __device__ __forceinline__ void st_hint(double2* p, double2 v, unsigned long lon
 // fewer per direction.
 #ifndef SGL_AZ512_FUSE2
 #define SGL_AZ512_FUSE2 1
+#endif
+#ifndef SGL_AZ512_NS2
+#define SGL_AZ512_NS2 1
 #endif
 #ifndef SGL_AZI_EO_PRE
 #define SGL_AZI_EO_PRE 1
@@ -588,10 +603,12 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
             rm[phys(2 * k + 1 - odd)] = odd ? sm : dm;
         }
         __syncthreads();
-        stockham_pass<N, 16, +1, true>(2, tt, twg + N, [&](int x) { return ring[phys(x)]; },
-                                       [&](int x, double2 v) { ring[phys(x)] = v; });
+        auto rd_ring = [&](int x) { return ring[phys(x)]; };
+        auto wr_ring = [&](int x, double2 v) { ring[phys(x)] = v; };
+        stockham_pass<N, 16, +1, true, decltype(rd_ring)&, decltype(wr_ring)&, NoPairLoad, SGL_AZ512_NS2 != 0>(
+            2, tt, twg + N, rd_ring, wr_ring);
         __syncthreads();
-        stockham_pass<N, 16, +1, false>(32, tt, twg + N + 15 * 2, [&](int x) { return ring[phys(x)]; }, st_out);
+        stockham_pass<N, 16, +1, false>(32, tt, twg + N + 15 * 2, rd_ring, st_out);
         return;
     }
     if constexpr (SGL_AZI_EO_PRE && N >= 256) {
