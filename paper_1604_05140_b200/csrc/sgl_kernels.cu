@@ -646,6 +646,37 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
     }
 }
 
+// 256-bit global accesses (sm_100a: LDG / STG .ENL2.256) and a 4 x 4 transpose of
+// doubles across the 4 lanes of a ring (N = 64: T = 4), for the real-valued
+// kernels at B = 32 (config C5), whose 8-byte samples otherwise move 32 bytes per
+// ring and instruction.
+__device__ __forceinline__ void ld_v4_cs(const double* p, double (&v)[4]) {
+    asm volatile("ld.global.cs.v4.f64 {%0, %1, %2, %3}, [%4];\n" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void st_v4_cs(double* p, const double (&v)[4]) {
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]) : "memory");
+}
+// in: lane t of an aligned 4-lane group holds M[t][b] in m[b]; out: m[b] = M[b][t]
+__device__ __forceinline__ void transpose4_lanes(double (&m)[4], int t) {
+    {
+        const bool hi = t & 1;
+        double s0 = hi ? m[0] : m[1], s1 = hi ? m[2] : m[3];
+        s0 = __shfl_xor_sync(0xffffffffu, s0, 1);
+        s1 = __shfl_xor_sync(0xffffffffu, s1, 1);
+        if (hi) { m[0] = s0; m[2] = s1; } else { m[1] = s0; m[3] = s1; }
+    }
+    {
+        const bool hi = t & 2;
+        double s0 = hi ? m[0] : m[2], s1 = hi ? m[1] : m[3];
+        s0 = __shfl_xor_sync(0xffffffffu, s0, 2);
+        s1 = __shfl_xor_sync(0xffffffffu, s1, 2);
+        if (hi) { m[0] = s0; m[1] = s1; } else { m[2] = s0; m[3] = s1; }
+    }
+}
+#ifndef SGL_AZR_V4
+#define SGL_AZR_V4 1
+#endif
+
 // ------------------------------------------------------------------ real-valued azimuthal stage
 // Real samples: the rings j' and 2B-1-j' of a shell are packed into one complex
 // ring z = x1 + i x2 and transformed with ONE complex FFT; with Z = FFT(z),
@@ -653,7 +684,7 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
 // and for real data only m >= 0 is needed (G[-m] = conj G[m]).  Half the bytes
 // in (8 B per sample) and half the FFTs of the complex path.  CTA: 2*IG shells,
 // one packed ring each (same thread count and shared memory as the complex path).
-template <int N>
+template <int N, bool V4 = false>
 __global__ void __launch_bounds__(FFTShape<N>::THREADS, FFTShape<N>::MINB)
 az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, double2* __restrict__ G,
                        const double* __restrict__ bcal, const double2* __restrict__ twg) {
@@ -689,9 +720,35 @@ az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, doub
                 z0 = z1 = make_double2(0.0, 0.0);
             }
         };
+        if constexpr (V4) {
+            // head pass (radix 4, thread tt runs butterflies 4 tt .. 4 tt + 3) on 32-byte
+            // loads: 4 consecutive samples of both rings per radix input
+            static_assert(S::T == 4 && S::R0 == 4 && N == 64, "N = 64: radix 4 then radix 16, 4 threads per ring");
+            double2 v[4][4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                double a[4] = {0.0, 0.0, 0.0, 0.0}, c[4] = {0.0, 0.0, 0.0, 0.0};
+                if (ok) {
+                    ld_v4_cs(src1 + 4 * tt + 16 * r, a);
+                    ld_v4_cs(src2 + 4 * tt + 16 * r, c);
+                }
+#pragma unroll
+                for (int bb = 0; bb < 4; ++bb) v[bb][r] = make_double2(a[bb], c[bb]);
+            }
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+                dft_reg<4, -1>(v[bb]);
+#pragma unroll
+                for (int r = 0; r < 4; ++r) ring[phys((4 * tt + bb) * 4 + r)] = v[bb][r];
+            }
+            pair_sync<N>();
+            stockham_pass<N, 16, -1, true>(4, tt, twg + N, [&](int x) { return ring[phys(x)]; },
+                                           [&](int x, double2 w) { ring[phys(x)] = w; });
+        } else {
         ring_fft_io<N, -1, false>(
             ring, tt, twg, [&](int x) { return ok ? make_double2(__ldcs(src1 + x), __ldcs(src2 + x)) : make_double2(0.0, 0.0); },
             [&](int x, double2 v) { ring[phys(x)] = v; }, ld2);
+        }
     }
     __syncthreads();
     const double b = __ldg(bcal + jp);
@@ -717,7 +774,7 @@ az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, doub
 #ifndef SGL_AZR_ZPRE
 #define SGL_AZR_ZPRE 1
 #endif
-template <int N>
+template <int N, bool V4 = false>
 __global__ void __launch_bounds__(FFTShape<N>::THREADS, FFTShape<N>::MINB)
 az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict__ X, size_t fstride,
                        const double2* __restrict__ twg) {
@@ -821,12 +878,45 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
             if (bin < B) return make_double2(x1.x - x2.y, x1.y + x2.x);  // X1 + i X2
             return make_double2(x1.x + x2.y, x2.x - x1.y);                // conj X1 + i conj X2
         };
+        if constexpr (V4) {
+            // radix-4 head pass in place, then the radix-16 pass (Ns = 4) by hand: thread tt
+            // ends with samples x = tt + 4 r; a 4 x 4 transpose across the ring's 4 lanes
+            // gives it 4 consecutive samples per block, stored as 32 bytes per ring
+            stockham_pass<N, 4, +1, true>(1, tt, twg, in, [&](int x, double2 w) { ring[phys(x)] = w; });
+            pair_sync<N>();
+            double2 v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = ring[phys(tt + 4 * r)];
+#pragma unroll
+            for (int r = 1; r < 16; ++r) {
+                double2 w = twg[N + (r - 1) * 4 + tt];
+                w.y = -w.y;
+                v[r] = cmul(v[r], w);
+            }
+            dft_reg<16, +1>(v);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                double m1[4], m2[4];
+#pragma unroll
+                for (int bb = 0; bb < 4; ++bb) {
+                    m1[bb] = v[4 * a + bb].x;
+                    m2[bb] = v[4 * a + bb].y;
+                }
+                transpose4_lanes(m1, tt);
+                transpose4_lanes(m2, tt);
+                if (ok) {
+                    st_v4_cs(dst1 + 16 * a + 4 * tt, m1);
+                    st_v4_cs(dst2 + 16 * a + 4 * tt, m2);
+                }
+            }
+        } else {
         ring_fft_io<N, +1, true>(ring, tt, twg, in, [&](int x, double2 v) {
             if (ok) {
                 __stcs(dst1 + x, v.x);
                 __stcs(dst2 + x, v.y);
             }
         });
+        }
     }
 }
 
@@ -836,10 +926,20 @@ static int az_fwd_real_launch(const Geo& g, const double* X, size_t fstride, dou
     using S = FFTShape<N>;
     constexpr int IGR = 2 * S::IG;
     const size_t smem = sizeof(double2) * (IGR * S::STRIDE);
-    static SmemAttrOnce attr;
-    attr.ensure(az_forward_real_kernel<N>, smem);
     const int nshell = g.batch * g.SC;
     dim3 grid((nshell + IGR - 1) / IGR, g.B);
+    if constexpr (N == 64 && SGL_AZR_V4) {
+        // 32-byte sample accesses need 32-byte aligned rings (any cudaMalloc / torch buffer)
+        if (reinterpret_cast<uintptr_t>(X) % 32 == 0 && fstride % 4 == 0) {
+            static SmemAttrOnce attr4;
+            attr4.ensure(az_forward_real_kernel<N, true>, smem);
+            az_forward_real_kernel<N, true><<<grid, S::THREADS, smem, s>>>(g, X, fstride, reinterpret_cast<double2*>(G),
+                                                                          bcal, reinterpret_cast<const double2*>(tw));
+            return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+        }
+    }
+    static SmemAttrOnce attr;
+    attr.ensure(az_forward_real_kernel<N>, smem);
     az_forward_real_kernel<N><<<grid, S::THREADS, smem, s>>>(g, X, fstride, reinterpret_cast<double2*>(G), bcal,
                                                               reinterpret_cast<const double2*>(tw));
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
@@ -851,10 +951,19 @@ static int az_inv_real_launch(const Geo& g, const double* G, double* X, size_t f
     using S = FFTShape<N>;
     constexpr int IGR = 2 * S::IG;
     const size_t smem = sizeof(double2) * (IGR * S::STRIDE);  // E/O rows live in the ring buffers
-    static SmemAttrOnce attr;
-    attr.ensure(az_inverse_real_kernel<N>, smem);
     const int nshell = g.batch * g.SC;
     dim3 grid((nshell + IGR - 1) / IGR, g.B);
+    if constexpr (N == 64 && SGL_AZR_V4) {
+        if (reinterpret_cast<uintptr_t>(X) % 32 == 0 && fstride % 4 == 0) {
+            static SmemAttrOnce attr4;
+            attr4.ensure(az_inverse_real_kernel<N, true>, smem);
+            az_inverse_real_kernel<N, true><<<grid, S::THREADS, smem, s>>>(g, reinterpret_cast<const double2*>(G), X,
+                                                                          fstride, reinterpret_cast<const double2*>(tw));
+            return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+        }
+    }
+    static SmemAttrOnce attr;
+    attr.ensure(az_inverse_real_kernel<N>, smem);
     az_inverse_real_kernel<N><<<grid, S::THREADS, smem, s>>>(g, reinterpret_cast<const double2*>(G), X, fstride,
                                                               reinterpret_cast<const double2*>(tw));
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
