@@ -395,6 +395,15 @@ __device__ __forceinline__ void tma_load_5d(unsigned dst, const void* tmap, unsi
 #endif
 }
 
+// G block of one azimuthal CTA: the CTA's shells are exactly one shell group
+// (2^lgib shells, g_layout), so element (p, bin, s0 + sl) of polar node jp sits at
+// block + (p * nbins + bin) * 2^lgib + sl -- for the kernels' idx = row * shells + sl
+// enumeration simply block[idx] (the general g_index costs ~25 integer
+// instructions per element, half of the real inverse kernel's instruction count).
+__device__ __forceinline__ long long g_block(const Geo& g, int jp, int s0) {
+    return ((((long long)jp * g.ngx + (s0 >> g.lgib)) * 2) * g.nbins) << g.lgib;
+}
+
 // ------------------------------------------------------------------ azimuthal forward
 // grid.x = ceil(nshell / IG), grid.y = B (j' = polar node in the northern half).
 // CTA holds rings (s, j') and (s, 2B-1-j') for IG consecutive flat shells s.
@@ -437,6 +446,7 @@ __device__ __forceinline__ void az_fwd_item(const Geo& g, const double2* __restr
         // epilogue: final radix-2 butterfly X[k] = y[k] + w^k y[k + 256], X[k + 256] = y[k] - w^k y[k + 256]
         // (linear, so applied to the E/O fold of the ring pair), b_cal, blocked G rows
         const double b = __ldg(bcal + jp);
+        double2* const Gblk = G + g_block(g, jp, s0);
 #pragma unroll 2
         for (int idx = tid; idx < B * S::IG; idx += S::THREADS) {
             const int sl = idx % S::IG, k = idx / S::IG;
@@ -448,11 +458,12 @@ __device__ __forceinline__ void az_fwd_item(const Geo& g, const double2* __restr
             const double2 w = __ldg(twg + k);
             const double2 a0 = cadd(yj0, ym0), a1 = csub(yj0, ym0);
             const double2 b0 = cmul(w, cadd(yj1, ym1)), b1 = cmul(w, csub(yj1, ym1));
-            G[g_index(g, 0, k, jp, sh)] = cscale(b, cadd(a0, b0));
-            G[g_index(g, 1, k, jp, sh)] = cscale(b, cadd(a1, b1));
+            double2* Gb = Gblk + idx;  // (p, bin) row at (p * N + bin) * IG
+            Gb[0] = cscale(b, cadd(a0, b0));
+            Gb[N * S::IG] = cscale(b, cadd(a1, b1));
             if (k != 0) {  // bin B (Nyquist) is not part of G
-                G[g_index(g, 0, k + B, jp, sh)] = cscale(b, csub(a0, b0));
-                G[g_index(g, 1, k + B, jp, sh)] = cscale(b, csub(a1, b1));
+                Gb[B * S::IG] = cscale(b, csub(a0, b0));
+                Gb[(N + B) * S::IG] = cscale(b, csub(a1, b1));
             }
         }
         return;
@@ -482,24 +493,31 @@ __device__ __forceinline__ void az_fwd_item(const Geo& g, const double2* __restr
     }
     __syncthreads();
     // epilogue: E/O fold, b_cal, scatter rows G[p][|m|][j'][sgn][s]
+    // both parities of a (shell, bin) from one pair of ring reads; the shell of
+    // idx = tid + it THREADS is a per-thread constant and the CTA's G block is
+    // contiguous (g_block): rows p = 0 at block[idx], p = 1 one half block further
     const unsigned long long gpol = SGL_L2HINTS ? policy_evict_last() : 0ull;
     const double b = __ldg(bcal + jp);
+    double2* const Gblk = G + g_block(g, jp, s0);
+    static_assert(S::THREADS % S::IG == 0 && (N * S::IG) % S::THREADS == 0, "epilogue enumeration");
+    const int sl = tid % S::IG;
+    if (s0 + sl >= nshell) return;
+    const double2* r1 = rings + (2 * sl) * S::STRIDE;
+    const double2* r2 = r1 + S::STRIDE;
 #pragma unroll 4
-    for (int idx = tid; idx < 2 * N * S::IG; idx += S::THREADS) {
-        const int sl = idx % S::IG;
-        const int rowi = idx / S::IG;  // p * N + bin
-        const int p = rowi / N, bin = rowi - p * N;
-        const int s = s0 + sl;
-        if (bin == B || s >= nshell) continue;
-        const double2 f1 = rings[(2 * sl) * S::STRIDE + phys(bin)];
-        const double2 f2 = rings[(2 * sl + 1) * S::STRIDE + phys(bin)];
-        const double2 v = p ? csub(f1, f2) : cadd(f1, f2);
-#ifdef SGL_G_WRAP  // timing-only experiment: G stores wrap inside an L2-sized window (wrong results)
-        G[g_index(g, p, bin, jp, s) % (SGL_G_WRAP * 65536LL)] = cscale(b, v);
-#else
-        if (SGL_L2HINTS) st_hint(G + g_index(g, p, bin, jp, s), cscale(b, v), gpol);
-        else G[g_index(g, p, bin, jp, s)] = cscale(b, v);
-#endif
+    for (int it = 0; it < N * S::IG / S::THREADS; ++it) {
+        const int idx = tid + it * S::THREADS;
+        const int bin = tid / S::IG + it * (S::THREADS / S::IG);
+        if (bin == B) continue;
+        const double2 f1 = r1[phys(bin)], f2 = r2[phys(bin)];
+        const double2 ve = cscale(b, cadd(f1, f2)), vo = cscale(b, csub(f1, f2));
+        if (SGL_L2HINTS) {
+            st_hint(Gblk + idx, ve, gpol);
+            st_hint(Gblk + idx + N * S::IG, vo, gpol);
+        } else {
+            Gblk[idx] = ve;
+            Gblk[idx + N * S::IG] = vo;
+        }
     }
 }
 
@@ -538,20 +556,21 @@ az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X,
     constexpr int PER = 2 * N * S::IG / S::THREADS;
     static_assert(PER * S::THREADS == 2 * N * S::IG, "prologue must divide evenly");
     double2 pv[PER];
+    // idx = tid + q THREADS enumerates the CTA's contiguous G block [p][bin][shell]
+    // (g_block): the shell is a per-thread constant, the address an immediate offset
+    static_assert(S::THREADS % S::IG == 0 && (N & (N - 1)) == 0, "shell of a prologue load is per-thread");
+    const bool sok = s0 + tid % S::IG < nshell;
+    const double2* Gb = G + g_block(g, jp, s0) + tid;
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
-        const int idx = tid + q * S::THREADS;
-        const int sl = idx % S::IG;
-        const int rowi = idx / S::IG;  // p * N + bin
-        const int p = rowi / N, bin = rowi - p * N;
-        const int s = s0 + sl;
+        const int bin = (tid / S::IG + q * (S::THREADS / S::IG)) & (N - 1);
 #ifdef SGL_G_WRAP
-        pv[q] = (bin != B && s < nshell) ? ld_stream(G + g_index(g, p, bin, jp, s) % (SGL_G_WRAP * 65536LL))
-                                         : make_double2(0.0, 0.0);
+        pv[q] = (bin != B && sok) ? ld_stream(G + (g_block(g, jp, s0) + tid + q * S::THREADS) % (SGL_G_WRAP * 65536LL))
+                                  : make_double2(0.0, 0.0);
 #else
-        pv[q] = (bin != B && s < nshell)
-                    ? ((SGL_L2HINTS || SGL_AZI_LOAD) ? ld_stream_hint(G + g_index(g, p, bin, jp, s), policy_evict_first())
-                                   : ld_stream(G + g_index(g, p, bin, jp, s)))
+        pv[q] = (bin != B && sok)
+                    ? ((SGL_L2HINTS || SGL_AZI_LOAD) ? ld_stream_hint(Gb + q * S::THREADS, policy_evict_first())
+                                                     : ld_stream(Gb + q * S::THREADS))
                     : make_double2(0.0, 0.0);
 #endif
     }
@@ -676,6 +695,25 @@ __device__ __forceinline__ void transpose4_lanes(double (&m)[4], int t) {
 #ifndef SGL_AZR_V4
 #define SGL_AZR_V4 1
 #endif
+// Ring of FFT role q (4 threads per ring, N = 64): shared memory serves 16-byte
+// accesses a quarter-warp at a time, i.e. two rings' threads together, and rings
+// one padded stride apart (69 = 5 mod 8 slots of 16 bytes) overlap in one slot --
+// every FFT-pass LDS / STS ran at 2x its ideal wavefronts (ncu, round 2).  Roles
+// 2a and 2a + 1 take rings 4 apart instead (20 = 4 mod 8 slots: disjoint halves of
+// the 128-byte line); the prologue / epilogue, whose lanes run over consecutive
+// rings, are unaffected.
+#ifndef SGL_AZR_RINGPERM
+#define SGL_AZR_RINGPERM 1
+#endif
+template <int T>
+__device__ __forceinline__ int ring_of_role(int q) {
+    if constexpr (T == 4 && SGL_AZR_RINGPERM) {
+        const int a = q >> 1;
+        return ((a >> 2) << 3) + (a & 3) + 4 * (q & 1);
+    } else {
+        return q;
+    }
+}
 
 // ------------------------------------------------------------------ real-valued azimuthal stage
 // Real samples: the rings j' and 2B-1-j' of a shell are packed into one complex
@@ -698,7 +736,8 @@ az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, doub
     const int s0 = blockIdx.x * IGR;
     const int nshell = g.batch * g.SC;
     {
-        const int q = tid / S::T, tt = tid - q * S::T;
+        const int tt = tid % S::T;
+        const int q = ring_of_role<S::T>(tid / S::T);
         const int s = s0 + q;
         const double* src1 = X;
         const double* src2 = X;
@@ -752,6 +791,7 @@ az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, doub
     }
     __syncthreads();
     const double b = __ldg(bcal + jp);
+    double2* const Gblk = G + g_block(g, jp, s0);
     // one (shell, m) per iteration: both parities from the same Z[m], Z[-m]
 #pragma unroll 4
     for (int idx = tid; idx < B * IGR; idx += S::THREADS) {
@@ -763,8 +803,9 @@ az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, doub
         const double2 zn = rings[sl * S::STRIDE + phys((N - m) & (N - 1))];
         const double2 x1 = make_double2(0.5 * (zm.x + zn.x), 0.5 * (zm.y - zn.y));
         const double2 x2 = make_double2(0.5 * (zm.y + zn.y), -0.5 * (zm.x - zn.x));
-        G[g_index(g, 0, m, jp, s)] = cscale(b, cadd(x1, x2));
-        G[g_index(g, 1, m, jp, s)] = cscale(b, csub(x1, x2));
+        double2* Gb = Gblk + idx;
+        Gb[0] = cscale(b, cadd(x1, x2));
+        Gb[B * IGR] = cscale(b, csub(x1, x2));
     }
 }
 
@@ -774,8 +815,11 @@ az_forward_real_kernel(Geo g, const double* __restrict__ X, size_t fstride, doub
 #ifndef SGL_AZR_ZPRE
 #define SGL_AZR_ZPRE 1
 #endif
+#ifndef SGL_AZRI_MINB64
+#define SGL_AZRI_MINB64 4  // CTAs/SM of the real inverse at N = 64
+#endif
 template <int N, bool V4 = false>
-__global__ void __launch_bounds__(FFTShape<N>::THREADS, FFTShape<N>::MINB)
+__global__ void __launch_bounds__(FFTShape<N>::THREADS, (N == 64 ? SGL_AZRI_MINB64 : FFTShape<N>::MINB))
 az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict__ X, size_t fstride,
                        const double2* __restrict__ twg) {
     using S = FFTShape<N>;
@@ -798,14 +842,19 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
     constexpr int PER = 2 * B * IGR / S::THREADS;
     static_assert(PER * S::THREADS == 2 * B * IGR, "prologue must divide evenly");
     double2 pv[PER];
+    // idx = tid + q THREADS enumerates the CTA's contiguous G block [p][m][shell]
+    // (g_block): the shell (idx % IGR) is a per-thread constant, the address an
+    // immediate offset from one pointer
+    static_assert(S::THREADS % IGR == 0, "shell of a prologue load is per-thread");
+    const bool sok = s0 + tid % IGR < nshell;
+    const double2* Gb = G + g_block(g, jp, s0) + tid;
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
-        const int idx = tid + q * S::THREADS;
-        const int sl = idx % IGR;
-        const int rowi = idx / IGR;  // p * B + m
-        const int p = rowi / B, m = rowi - p * B;
-        const int s = s0 + sl;
-        pv[q] = s < nshell ? ld_stream(G + g_index(g, p, m, jp, s)) : make_double2(0.0, 0.0);
+#ifdef SGL_AZR_DBG_NOLD  // timing-only (wrong results): no G loads
+        pv[q] = make_double2((double)(tid + q), (double)(q - tid));
+#else
+        pv[q] = sok ? ld_stream(Gb + q * S::THREADS) : make_double2(0.0, 0.0);
+#endif
     }
 #if SGL_AZR_ZPRE
     // the thread holds E (q) and O (q + PER / 2) of the same (shell, m): form the
@@ -814,13 +863,12 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
     // first FFT pass reads the ring like the complex path
     static_assert(PER % 2 == 0, "E and O of one bin in one thread");
 #pragma unroll
+    double2* const zring = eo + (tid % IGR) * EOS;
     for (int q = 0; q < PER / 2; ++q) {
-        const int idx = tid + q * S::THREADS;
-        const int sl = idx % IGR;
-        const int m = idx / IGR;  // rowi < B: p = 0
+        const int m = tid / IGR + q * (S::THREADS / IGR);  // row < B: p = 0
         const double2 e = pv[q], o = pv[q + PER / 2];
         const double2 x1 = cadd(e, o), x2 = csub(e, o);
-        double2* ring = eo + sl * EOS;
+        double2* ring = zring;
         if (m == 0) {
             ring[phys(0)] = make_double2(x1.x, x2.x);
             ring[phys(B)] = make_double2(0.0, 0.0);
@@ -856,7 +904,8 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
 #endif
     __syncthreads();
     {
-        const int q = tid / S::T, tt = tid - q * S::T;
+        const int tt = tid % S::T;
+        const int q = ring_of_role<S::T>(tid / S::T);
         const int s = s0 + q;
         const double2* e_buf = eo + q * EOS;
         double* dst1 = X;
@@ -866,6 +915,10 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
             const int f = s / g.SC, i = s - f * g.SC;
             dst1 = X + f * fstride + ((size_t)i * N + jp) * N;
             dst2 = X + f * fstride + ((size_t)i * N + (N - 1 - jp)) * N;
+#ifdef SGL_AZR_DBG_CONTIG  // timing-only (wrong results): each CTA writes one contiguous block
+            dst1 = X + (((size_t)blockIdx.y * gridDim.x + blockIdx.x) * IGR * 2 + 2 * q) * N;
+            dst2 = dst1 + N;
+#endif
         }
         double2* ring = rings + q * S::STRIDE;
         auto in = [&](int bin) {
@@ -904,7 +957,11 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
                 }
                 transpose4_lanes(m1, tt);
                 transpose4_lanes(m2, tt);
+#ifdef SGL_AZR_DBG_NOST  // timing-only (wrong results): stores only if a value is NaN
+                if (ok && m1[0] != m1[0]) {
+#else
                 if (ok) {
+#endif
                     st_v4_cs(dst1 + 16 * a + 4 * tt, m1);
                     st_v4_cs(dst2 + 16 * a + 4 * tt, m2);
                 }
