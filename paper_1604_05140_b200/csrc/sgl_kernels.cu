@@ -932,38 +932,45 @@ az_inverse_real_kernel(Geo g, const double2* __restrict__ G, double* __restrict_
             return make_double2(x1.x + x2.y, x2.x - x1.y);                // conj X1 + i conj X2
         };
         if constexpr (V4) {
-            // radix-4 head pass in place, then the radix-16 pass (Ns = 4) by hand: thread tt
-            // ends with samples x = tt + 4 r; a 4 x 4 transpose across the ring's 4 lanes
-            // gives it 4 consecutive samples per block, stored as 32 bytes per ring
-            stockham_pass<N, 4, +1, true>(1, tt, twg, in, [&](int x, double2 w) { ring[phys(x)] = w; });
-            pair_sync<N>();
+            // radices (16, 4) instead of the generic (4, 16): the last pass's thread tt runs
+            // the radix-4 butterflies j = 4 tt .. 4 tt + 3, whose outputs j + 16 r are 4
+            // consecutive samples per r -- 32-byte stores per ring, no transposition.
+            // Pass 1 (radix 16, thread tt = butterfly tt): element y[16 u + 4 v + b] is
+            // parked at 16 b + 4 u + ((u + v) & 3), which keeps both its writes (4 threads
+            // u) and pass 2's reads (4 threads v) on 4 distinct 16-byte slots of one half
+            // of the 128-byte line; the quarter-warp's other ring sits on the other half.
             double2 v[16];
 #pragma unroll
-            for (int r = 0; r < 16; ++r) v[r] = ring[phys(tt + 4 * r)];
-#pragma unroll
-            for (int r = 1; r < 16; ++r) {
-                double2 w = twg[N + (r - 1) * 4 + tt];
-                w.y = -w.y;
-                v[r] = cmul(v[r], w);
-            }
+            for (int r = 0; r < 16; ++r) v[r] = in(tt + 4 * r);
             dft_reg<16, +1>(v);
+            pair_sync<N>();  // every read of the natural-order ring before the in-place writes
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                double m1[4], m2[4];
+            for (int r = 0; r < 16; ++r) ring[16 * (r & 3) + 4 * tt + ((tt + (r >> 2)) & 3)] = v[r];
+            pair_sync<N>();
+            double2 u4[4][4];
 #pragma unroll
-                for (int bb = 0; bb < 4; ++bb) {
-                    m1[bb] = v[4 * a + bb].x;
-                    m2[bb] = v[4 * a + bb].y;
+            for (int bb = 0; bb < 4; ++bb) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) u4[bb][r] = ring[16 * bb + 4 * r + ((r + tt) & 3)];
+#pragma unroll
+                for (int r = 1; r < 4; ++r) {
+                    double2 w = twg[r * (4 * tt + bb)];  // e^{-2 pi i r k / 64}, k = 4 tt + bb
+                    w.y = -w.y;
+                    u4[bb][r] = cmul(u4[bb][r], w);
                 }
-                transpose4_lanes(m1, tt);
-                transpose4_lanes(m2, tt);
+                dft_reg<4, +1>(u4[bb]);
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const double m1[4] = {u4[0][r].x, u4[1][r].x, u4[2][r].x, u4[3][r].x};
+                const double m2[4] = {u4[0][r].y, u4[1][r].y, u4[2][r].y, u4[3][r].y};
 #ifdef SGL_AZR_DBG_NOST  // timing-only (wrong results): stores only if a value is NaN
                 if (ok && m1[0] != m1[0]) {
 #else
                 if (ok) {
 #endif
-                    st_v4_cs(dst1 + 16 * a + 4 * tt, m1);
-                    st_v4_cs(dst2 + 16 * a + 4 * tt, m2);
+                    st_v4_cs(dst1 + 16 * r + 4 * tt, m1);
+                    st_v4_cs(dst2 + 16 * r + 4 * tt, m2);
                 }
             }
         } else {
