@@ -1701,6 +1701,9 @@ __device__ __forceinline__ void gemm_epilogue(const P& pr, int pid, int m0, int 
 #ifndef SGL_A_QUAD
 #define SGL_A_QUAD 0  // measured: no gain (round 2)
 #endif
+#ifndef SGL_GEMM_FASTISSUE
+#define SGL_GEMM_FASTISSUE 1
+#endif
 template <class P, int WM>
 __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* smem) {
     using C = GemmCfg<P, WM>;
@@ -1807,6 +1810,28 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
         a_nb[u] = o1 ? (o2 ? 16 : 8) : 0;
     }
 
+    // Fast chunk issue (SGL_GEMM_FASTISSUE): when every transfer of this warp is a
+    // full 16-byte unit inside M and N -- interior tiles, the vast majority -- a
+    // chunk inside K is issued without predicates, selects or zero-fill sizes,
+    // straight from precomputed 32-bit shared-memory destinations (the general path
+    // spends ~20 instructions per cp.async).  Warp-uniform, so no divergence.
+    unsigned a_dst[AU], b_dst[C::BQ];
+    bool fast_issue = false;
+    if constexpr (SGL_GEMM_FASTISSUE) {
+        bool all = true;
+#pragma unroll
+        for (int u = 0; u < AU; ++u) {
+            all = all && a_nb[u] == 16;
+            a_dst[u] = static_cast<unsigned>(__cvta_generic_to_shared(smem + a_so[u]));
+        }
+#pragma unroll
+        for (int q = 0; q < C::BQ; ++q)
+            b_dst[q] = static_cast<unsigned>(__cvta_generic_to_shared(smem + C::A_STAGE + b_so[q]));
+        if constexpr (SEQ) all = all && n0 + t.nseq * BN <= N;
+        else all = all && b_ok == (1u << C::BQ) - 1u;
+        fast_issue = __all_sync(0xffffffffu, all);
+    }
+
     // SEQ: the CTA runs t.nseq consecutive n-blocks of the problem as one
     // pipelined sequence of chunks v = tile * nch + c (A is the same for all of
     // them; B columns shift by BN per tile), so each tile's epilogue overlaps the
@@ -1844,6 +1869,22 @@ __device__ __forceinline__ void gemm_tile(const P& pr, const Tile& t, double* sm
         const int k0 = c * BK;
         const bool kfull = k0 + BK <= K;
         const int a_adv = k0 * a_sk;
+        if constexpr (SGL_GEMM_FASTISSUE && !has_btma<P>::value) {
+            if (fast_issue && kfull) {
+                const unsigned so = (unsigned)((v % ST) * C::STAGE * (int)sizeof(double));
+#pragma unroll
+                for (int u = 0; u < AU; ++u)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(a_dst[u] + so), "l"(a_ptr[u] + a_adv));
+                const int b_adv = k0 * (int)b_step;
+#pragma unroll
+                for (int q = 0; q < C::BQ; ++q) {
+                    const double* src = (TAB ? b_ptr[q] + ktab[k0 + b_k[q]] : b_ptr[q] + b_adv) + cs;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(b_dst[q] + so), "l"(src));
+                }
+                cp_async_commit();
+                return;
+            }
+        }
 #pragma unroll
         for (int u = 0; u < AU; ++u) {
 #ifdef SGL_TABLE_L2  // experiment (wrong results): every table read from one 64 KB, L2-resident block
@@ -2024,6 +2065,138 @@ __global__ void __launch_bounds__(128, P::GEMM_MINB) gemm_dmma_kernel(const __gr
         case 2: if constexpr (P::GEMM_MAXWM >= 2) gemm_tile<P, 2>(pr, t, gsm); break;
         default: if constexpr (P::GEMM_MAXWM >= 4) gemm_tile<P, 4>(pr, t, gsm); break;
     }
+}
+
+// ------------------------------------------------------------------ Legendre inverse, warp-private pipelines
+// The Legendre inverse's problems are short in K (<= B/2 degrees of one parity) and
+// wide in N, so the general engine's per-chunk CTA barrier and per-chunk A reload
+// weigh heavily.  Here a CTA (one 32-row block of a problem, a sequence of 128-column
+// n-blocks) loads its whole A panel -- 32 table rows x K -- once, and each warp then
+// runs its own 32 x 32 pipeline: it copies its own 32 columns of S chunk by chunk
+// (cp.async ring private to the warp), waits on its own copies (wait_group +
+// __syncwarp) and never meets the other warps again: no CTA barrier after the panel,
+// warps drift freely across chunks and tiles, one A transfer per problem row block.
+// Used when every n-block is full (NB % 128 == 0), B % 32 == 0 and K <= KMAX.
+#ifndef SGL_LEGINV_WP
+#define SGL_LEGINV_WP 1
+#endif
+template <int KMAX>
+struct LegInvWp {
+    static constexpr int ST = 4, BK = 8, LDA = 36, LDB = 36;
+    static constexpr int A_PANEL = KMAX * LDA;        // doubles: [k][row], rows padded to 36
+    static constexpr int B_STAGE = BK * LDB;          // doubles per warp and stage
+    static constexpr size_t smem_bytes() { return sizeof(double) * (A_PANEL + 4 * ST * B_STAGE); }
+};
+
+template <int KMAX>
+__global__ void __launch_bounds__(128, 4) leginv_wp_kernel(const __grid_constant__ LegInv pr, const __grid_constant__ TileMap tm) {
+    using W = LegInvWp<KMAX>;
+    constexpr int ST = W::ST, BK = W::BK, LDA = W::LDA, LDB = W::LDB;
+    extern __shared__ __align__(128) double gsm[];
+    double* As = gsm;
+    double* Bw = gsm + W::A_PANEL + (threadIdx.x >> 5) * (ST * W::B_STAGE);
+    const Tile t = decode_tile<true>(tm, pr.g.NB, blockIdx.x);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int pid = t.prob, m0 = t.m0, n0 = t.n0;
+    const int M = pr.M(pid), N = pr.nlim(pid, n0), K = pr.K(pid);
+    const int nch = K > 0 ? (K + BK - 1) / BK : 1;
+    const int kr = nch * BK;
+
+    // ---- A panel (table rows m0 .. m0 + 31, all K degrees; zero past K) and the row-offset table
+    {
+        const double* a0 = pr.A + pr.rowA(pid, m0);
+        const int a_sk = pr.a_sk(pid);
+        for (int e = tid; e < kr * 16; e += 128) {  // 16-byte units: k = e / 16, rows 2 (e % 16), +1
+            const int k = e >> 4, r = (e & 15) * 2;
+            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(As + k * LDA + r));
+            const bool ok = k < K;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(ok ? a0 + (long long)k * a_sk + r : pr.A),
+                         "r"(ok ? 16 : 0));
+        }
+        cp_async_commit();
+    }
+    // ---- this warp's B pipeline: chunk v = (tile tv, k-chunk c); lane copies rows r0 + 2 i, unit u
+    const int r0 = lane >> 4, u = lane & 15;
+    const double* bcol = pr.Bm + pr.colB(pid, n0) + 32 * warp + 2 * u;
+    const unsigned bdst = static_cast<unsigned>(__cvta_generic_to_shared(Bw + r0 * LDB + 2 * u));
+    const int nv = t.nseq * nch;
+    const int l0 = pr.am(pid) + (pid & 1), snb = (int)pr.sv.NB;
+    int is_tile = 0, is_chunk = 0;
+    auto issue = [&](int v) {
+        const int k0 = is_chunk * BK, cs = is_tile * 128;
+        if (++is_chunk == nch) {
+            is_chunk = 0;
+            ++is_tile;
+        }
+        const unsigned so = (unsigned)((v % ST) * W::B_STAGE * (int)sizeof(double));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int k = k0 + r0 + 2 * i;
+            const bool ok = k < K;
+            // row of degree l = |m| + p + 2 k of the nu-major S: l (l + 1) NB reals (LegInv::rowB)
+            const int l = l0 + 2 * k;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(bdst + so + (unsigned)(2 * i * LDB * 8)),
+                         "l"(ok ? bcol + l * (l + 1) * snb + cs : pr.Bm), "r"(ok ? 16 : 0));
+        }
+        cp_async_commit();
+    };
+    // the first B chunks are in flight while the panel arrives
+#pragma unroll
+    for (int v = 0; v < ST - 1; ++v) {
+        if (v < nv) issue(v);
+        else cp_async_commit();
+    }
+    cp_async_wait_group<ST - 1>();  // this thread's share of the panel (the oldest group)
+    __syncthreads();                // panel visible to all warps: the only CTA barrier
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    int c = 0, tv = 0;
+    for (int v = 0; v < nv; ++v) {
+        cp_async_wait_group<ST - 2>();
+        __syncwarp();
+        if (v + ST - 1 < nv) issue(v + ST - 1);
+        else cp_async_commit();
+        const double* as = As + c * BK * LDA;
+        const double* bs = Bw + (v % ST) * W::B_STAGE;
+        const int ksteps = min(BK, K - c * BK);
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            if (kk >= ksteps) break;
+            double af[4], bf[4];
+#pragma unroll
+            for (int fm = 0; fm < 4; ++fm) af[fm] = as[(kk + (lane & 3)) * LDA + fm * 8 + (lane >> 2)];
+#pragma unroll
+            for (int fn = 0; fn < 4; ++fn) bf[fn] = bs[(kk + (lane & 3)) * LDB + fn * 8 + (lane >> 2)];
+#pragma unroll
+            for (int fm = 0; fm < 4; ++fm)
+#pragma unroll
+                for (int fn = 0; fn < 4; ++fn) dmma884(acc[fm][fn], af[fm], bf[fn]);
+        }
+        if (++c == nch) {
+            gemm_epilogue<LegInv, 1>(pr, pid, m0, n0 + tv * 128, M, N, acc, 0, 32 * warp, lane);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            c = 0;
+            ++tv;
+        }
+    }
+    cp_async_wait_group<0>();
+}
+
+bool leginv_wp_ok(const Geo& g) { return g.NB % 128 == 0 && g.B % 32 == 0 && g.B >= 64 && g.B <= 128; }
+
+template <int KMAX>
+static int leginv_wp_launch(const LegInv& p, const TileMap* tiles, int ntiles, cudaStream_t s) {
+    const size_t smem = LegInvWp<KMAX>::smem_bytes();
+    static SmemAttrOnce attr;
+    attr.ensure(leginv_wp_kernel<KMAX>, smem);
+    leginv_wp_kernel<KMAX><<<ntiles, 128, smem, s>>>(p, *tiles);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 // ------------------------------------------------------------------ G layout
@@ -2386,6 +2559,17 @@ int launch_legendre_forward_peers(const Geo& g, const SView& sv, const double* G
 int launch_legendre_inverse(const Geo& g, const SView& sv, const double* S, double* G, const double* tab,
                             const long long* tab_off, const TileMap* tiles, int ntiles, cudaStream_t s) {
     LegInv p{g, tab, tab_off, S, G, sv};
+    {
+        // warp-private pipelines: full n-blocks, full 32-row blocks, K <= 64 (B <= 128)
+        static const int wp = [] {
+            const char* e = std::getenv("SGL_LEGINV_WP");
+            return e ? std::atoi(e) : SGL_LEGINV_WP;
+        }();
+        // (B = 32: K <= 16, two chunks per tile -- the panel and its barrier do not pay: 444 -> 488 us
+        // for 512 functions; B = 64 x 64: 570 -> 561 us; B = 128: 101.9 -> 97.4 us)
+        if (wp && leginv_wp_ok(g))
+            return g.B <= 64 ? leginv_wp_launch<32>(p, tiles, ntiles, s) : leginv_wp_launch<64>(p, tiles, ntiles, s);
+    }
     if (ntiles > 0 && tiles->seq > 1) {
         LegInvSeq q;
         static_cast<LegInv&>(q) = p;

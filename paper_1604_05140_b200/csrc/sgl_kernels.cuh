@@ -123,6 +123,10 @@ __host__ __device__ inline long long g_index(const Geo& g, int p, int bin, int j
 // fields of g.  Returns the number of complex values G needs.
 long long g_layout(Geo& g);
 
+// Does the Legendre inverse of this geometry run on the warp-private kernel
+// (leginv_wp_kernel)?  The tile builder uses longer n-block sequences for it.
+bool leginv_wp_ok(const Geo& g);
+
 // Azimuthal stage (forward): FFT of length 2B per ring (sign -1, kernels.cpp:478),
 // b_cal weighting, equatorial fold E/O and scatter to the m-major intermediate
 //   G[p][|m|][j'][sgn][f][i]  (complex), p = parity, j' < B, sgn = (m < 0).
