@@ -2115,30 +2115,51 @@ __global__ void __launch_bounds__(128, 4) leginv_wp_kernel(const __grid_constant
         }
         cp_async_commit();
     }
-    // ---- this warp's B pipeline: chunk v = (tile tv, k-chunk c); lane copies rows r0 + 2 i, unit u
+    // ---- this warp's B pipeline: chunk v = (tile tv, k-chunk c); lane copies rows r0 + 2 i, unit u.
+    // Row k of the chunk is degree l = l0 + 2 k of the nu-major S, at l (l + 1) NB reals
+    // (LegInv::rowB); the lane's four rows are l, l + 4, l + 8, l + 12 with l = la, and la
+    // advances by 16 per chunk: off(l) and e = (2 l + 1) NB are carried incrementally,
+    //   off(l + 16) = off(l) + 16 e + 256 NB,  off(l + 4 i) = off(l) + 4 i e + 16 i^2 NB.
     const int r0 = lane >> 4, u = lane & 15;
     const double* bcol = pr.Bm + pr.colB(pid, n0) + 32 * warp + 2 * u;
     const unsigned bdst = static_cast<unsigned>(__cvta_generic_to_shared(Bw + r0 * LDB + 2 * u));
     const int nv = t.nseq * nch;
-    const int l0 = pr.am(pid) + (pid & 1), snb = (int)pr.sv.NB;
-    int is_tile = 0, is_chunk = 0;
+    const int snb = (int)pr.sv.NB;
+    const int la0 = pr.am(pid) + (pid & 1) + 2 * r0;
+    const int off_init = la0 * (la0 + 1) * snb, e_init = (2 * la0 + 1) * snb;
+    int off = off_init, e = e_init;
+    int is_chunk = 0;
+    const double* bcs = bcol;  // + 128 per finished tile
     auto issue = [&](int v) {
-        const int k0 = is_chunk * BK, cs = is_tile * 128;
-        if (++is_chunk == nch) {
-            is_chunk = 0;
-            ++is_tile;
-        }
-        const unsigned so = (unsigned)((v % ST) * W::B_STAGE * (int)sizeof(double));
+        const unsigned so = bdst + (unsigned)((v % ST) * W::B_STAGE * (int)sizeof(double));
+        const int o1 = off + 4 * e + 16 * snb, o2 = off + 8 * e + 64 * snb, o3 = off + 12 * e + 144 * snb;
+        const bool tail = is_chunk == nch - 1;
+        if (!tail || K == kr) {  // every row of the chunk inside K (uniform)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(so), "l"(bcs + off));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(so + 2u * LDB * 8u), "l"(bcs + o1));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(so + 4u * LDB * 8u), "l"(bcs + o2));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(so + 6u * LDB * 8u), "l"(bcs + o3));
+        } else {
+            const int kb = is_chunk * BK + r0;
+            const int oo[4] = {off, o1, o2, o3};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int k = k0 + r0 + 2 * i;
-            const bool ok = k < K;
-            // row of degree l = |m| + p + 2 k of the nu-major S: l (l + 1) NB reals (LegInv::rowB)
-            const int l = l0 + 2 * k;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(bdst + so + (unsigned)(2 * i * LDB * 8)),
-                         "l"(ok ? bcol + l * (l + 1) * snb + cs : pr.Bm), "r"(ok ? 16 : 0));
+            for (int i = 0; i < 4; ++i) {
+                const bool ok = kb + 2 * i < K;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(so + (unsigned)(2 * i * LDB * 8)),
+                             "l"(ok ? bcs + oo[i] : pr.Bm), "r"(ok ? 16 : 0));
+            }
         }
         cp_async_commit();
+        if (tail) {  // next chunk starts the next n-block
+            is_chunk = 0;
+            off = off_init;
+            e = e_init;
+            bcs += 128;
+        } else {
+            ++is_chunk;
+            off += 16 * e + 256 * snb;
+            e += 32 * snb;
+        }
     };
     // the first B chunks are in flight while the panel arrives
 #pragma unroll
@@ -2176,7 +2197,32 @@ __global__ void __launch_bounds__(128, 4) leginv_wp_kernel(const __grid_constant
                 for (int fn = 0; fn < 4; ++fn) dmma884(acc[fm][fn], af[fm], bf[fn]);
         }
         if (++c == nch) {
-            gemm_epilogue<LegInv, 1>(pr, pid, m0, n0 + tv * 128, M, N, acc, 0, 32 * warp, lane);
+            // epilogue of a full interior tile: the column offsets of the blocked G once per
+            // tile (colC4), the (-1)^m of the -m half as a uniform sign flip, rows one G
+            // row stride apart -- no bounds checks (M, N full by construction)
+            {
+                const int ncol = n0 + tv * 128 + 32 * warp;
+                int cofs[4];
+                pr.colC4(pid, ncol + 2 * (lane & 3), cofs);
+                if (pr.negC(pid, ncol)) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {  // sign-bit flips: no FP64 pipe work
+                            acc[i][j][0] = __longlong_as_double(__double_as_longlong(acc[i][j][0]) ^ (1LL << 63));
+                            acc[i][j][1] = __longlong_as_double(__double_as_longlong(acc[i][j][1]) ^ (1LL << 63));
+                        }
+                }
+                const int rs = g_rowstride(pr.g);
+                double* out = pr.C + (long long)(m0 + (lane >> 2)) * rs;
+#pragma unroll
+                for (int fm = 0; fm < 4; ++fm) {
+#pragma unroll
+                    for (int fn = 0; fn < 4; ++fn)
+                        *reinterpret_cast<double2*>(out + cofs[fn]) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
+                    out += 8 * rs;
+                }
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
