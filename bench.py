@@ -34,14 +34,15 @@ sys.path.insert(0, REPO)
 sys.path.insert(0, os.path.join(REPO, "tests"))
 
 FP64_PEAK_TFLOPS = 37.1  # measured DMMA m8n8k4 peak on this pool's B200 (profiles/fp64_peak_r01.txt)
-TRAFFIC_FILE = "r02e_traffic.json"  # per-kernel DRAM bytes of the committed ncu capture (B = 128, one function)
+TRAFFIC_FILE = "r02f_traffic.json"  # per-kernel DRAM bytes of the committed ncu capture (B = 128, one function)
 
 
 def KERNEL_NAMES(B):  # noqa: N802 -- ncu names of each stage's kernels
     return {0: [f"void az_forward_kernel<{2 * B}>"],
             1: ["void gemm_dmma_kernel<LegFwdTma>", "void gemm_dmma_kernel<LegFwd>"],
             2: ["void gemm_dmma_kernel<RadFwd>"], 3: ["void gemm_dmma_kernel<RadInv>"],
-            4: ["void gemm_dmma_kernel<LegInvSeq>", "void gemm_dmma_kernel<LegInv>"],
+            4: ["void leginv_wp_kernel<64>", "void leginv_wp_kernel<32>", "void gemm_dmma_kernel<LegInvSeq>",
+                "void gemm_dmma_kernel<LegInv>"],
             5: [f"void az_inverse_kernel<{2 * B}>"],
             6: [f"void sph_fwd_fused_kernel<{2 * B}>"], 7: [f"void sph_inv_fused_kernel<{2 * B}>"]}
 

@@ -250,9 +250,11 @@ void problem_shape(Kind kind, int B, int batch, long long NB, int pid, bool real
 // spherical stage): row blocks [sub_lo, sub_lo + sub_n) of every problem for the
 // Legendre inverse (a slab of polar nodes), n-blocks [sub_lo, sub_lo + sub_n) of
 // every sign half for the Legendre forward (a range of shells).
+// wp: the caller runs the whole-transform radial forward (one S block, every degree), for
+// which batched small bandlimits use the warp-private kernel (n-block sequences).
 std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, int SC, int lo, int hi,
-                                         bool real = false, int sub_lo = 0, int sub_n = 0) {
-    const auto key = std::make_tuple((int)kind + (real ? 16 : 0), batch, SC, lo, hi, sub_lo, sub_n);
+                                         bool real = false, int sub_lo = 0, int sub_n = 0, bool wp = false) {
+    const auto key = std::make_tuple((int)kind + (real ? 16 : 0) + (wp ? 32 : 0), batch, SC, lo, hi, sub_lo, sub_n);
     std::lock_guard<std::mutex> meta(p->meta_mu);
     auto it = p->tiles.find(key);
     if (it != p->tiles.end()) return it->second;
@@ -273,6 +275,19 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
         int pid, lwm, halves, tm, tn, h0, mi0, ni0;
         long long work;  // per tile, for heaviest-first ordering
     };
+    // radial forward on warp-private pipelines: batched small bandlimits, several waves deep
+    bool radfwd_wp = false;
+    if (kind == kRadFwd && wp && SC == 2 * B && lo == 0 && hi == B) {
+        const char* e = std::getenv("SGL_RADFWD_WP");
+        sglk::Geo gq{B, SC, batch, NB};
+        long long cols = 0;
+        for (int l = 0; l < B; ++l) cols += ((real ? l + 1 : 2 * l + 1) * 2LL * batch + 127) / 128 * ((B - l + 31) / 32);
+        // opt-in: measured equal or slower (B = 64 x 64: 209 vs 209 us, real B = 32 x 4096: 864 -> 877,
+        // sequences of 2 / 8: 835 / 950) -- at K = 2B <= 128 these tiles are bound by their epilogue
+        // (the omega-order scatter with its per-column divisions), not by barriers or chunk issue
+        radfwd_wp = (e && std::atoi(e)) && sglk::radfwd_wp_ok(gq, sglk::RadialBlocks{2 * B, 0, 0}) &&
+                    cols >= 8LL * 4 * p->num_sms;
+    }
     std::vector<Entry> ents;
     long long ntiles = 0;
     for (int pid = plo; pid < phi; ++pid) {
@@ -299,6 +314,7 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
         // radial forward at B >= 256: 64 x 64 tiles (measured: 493 -> 477 us at B = 256; no gain at B = 128)
         if (kind == kRadFwd && B >= 256 && !wm_force) lwm = 1;
         if (wm_force == 1 || wm_force == 2 || wm_force == 4) lwm = wm_force == 1 ? 0 : wm_force == 2 ? 1 : 2;
+        if (radfwd_wp) lwm = 0;  // 32 x 128 tiles: one warp per 32 columns
         const int max_wm = kind == kLegFwdS ? 1 : kind == kLegFwd ? SGL_MAXWM_LEGFWD : kind == kLegInv ? SGL_MAXWM_LEGINV
                          : kind == kRadFwd ? SGL_MAXWM_RADFWD : SGL_MAXWM_RADINV;
         while ((1 << lwm) > max_wm) --lwm;
@@ -340,6 +356,10 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
         // function (~1k tiles) runs 18.7 -> 17.1 us without them
         if (ntiles < 2LL * 4 * p->num_sms) seq = 1;
         if (const char* e = std::getenv("SGL_SEQ")) seq = std::max(1, std::min(8, std::atoi(e)));
+    }
+    if (radfwd_wp) {
+        seq = 4;
+        if (const char* e = std::getenv("SGL_SEQ_RADFWD")) seq = std::max(2, std::min(8, std::atoi(e)));
     }
     if (kind == kRadInv && batch == 1 && !real) {  // RadInvSeq (one complex function)
         if (const char* e = std::getenv("SGL_SEQ_RADINV")) seq = std::max(1, std::min(8, std::atoi(e)));
@@ -739,7 +759,7 @@ int forward_device(sglgpu_plan* p, Work& w, const double* X, double* C, int nb, 
         w.G.ensure(2 * (size_t)sglk::g_layout(g));
         const sglk::SView sv{g.NB, 2 * B, 0};
         auto lt = tiles_for(p, kLegFwd, fb, 2 * B, 0, 2 * B);
-        auto rt = tiles_for(p, kRadFwd, fb, 2 * B, 0, B);
+        auto rt = tiles_for(p, kRadFwd, fb, 2 * B, 0, B, false, 0, 0, true);
         k = staged(p, 0, st, [&] {
             return sglk::launch_az_forward(g, X + (size_t)f0 * psi2, psi2, w.G.p, p->d_bcal, p->d_tw, st);
         });
@@ -868,7 +888,7 @@ int real_device(sglgpu_plan* p, Work& w, const double* in, double* out, int nb, 
         const sglk::SView sv{g.NB, 2 * B, 0};
         if (forward) {
             auto lt = tiles_for(p, kLegFwd, fb, 2 * B, 0, 2 * B, true);
-            auto rt = tiles_for(p, kRadFwd, fb, 2 * B, 0, B, true);
+            auto rt = tiles_for(p, kRadFwd, fb, 2 * B, 0, B, true, 0, 0, true);
             k = staged(p, 0, st, [&] {
                 return sglk::launch_az_forward_real(g, in + (size_t)f0 * psi, psi, w.G.p, p->d_bcal, p->d_tw, st);
             });

@@ -2245,6 +2245,152 @@ static int leginv_wp_launch(const LegInv& p, const TileMap* tiles, int ntiles, c
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
+// ------------------------------------------------------------------ radial forward, warp-private pipelines
+// Batched transforms at small bandlimits (B <= 64: configs C2, C5): a degree's radial
+// problem is M = B - l <= 64 rows against K = 2B shells and a very wide N (all orders of
+// all functions), and in the general engine its tiles -- half-empty in M, 8 to 16 chunks
+// deep -- are dominated by per-tile and per-chunk overhead (radial_forward at 18% of the
+// DMMA peak for B = 32 x 4096).  As in leginv_wp_kernel: a CTA takes one 32-row block of
+// a degree and a sequence of 128-column n-blocks, loads its A panel (32 rows of W_l, all
+// K shells) once, and each warp streams its own 32 columns of S through a private
+// cp.async ring with no CTA barrier after the panel.  The (order, function) column pairs
+// of a warp are 16 runs of S, each contiguous over the shells (re, im interleaved):
+// lane (k, pair) copies 16 bytes of 8 lanes' 128-byte run.  Opt-in (SGL_RADFWD_WP=1):
+// measured equal or slower than the general engine (sgl_capi.cpp, tiles_for).
+template <int KMAX>
+struct RadFwdWp {
+    static constexpr int ST = 4, BK = 8, LDA = KMAX + 4, LDB = 36;
+    static constexpr int A_PANEL = 32 * LDA;  // doubles: [row][k]
+    static constexpr int B_STAGE = BK * LDB;
+    static constexpr size_t smem_bytes() { return sizeof(double) * (A_PANEL + 4 * ST * B_STAGE); }
+};
+
+template <int FA>
+__device__ __forceinline__ void radfwd_wp_chunk(const double* as, const double* bs, double (&acc)[4][4][2], int lane,
+                                                int lda, int ldb) {
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 4) {
+        double af[FA], bf[4];
+#pragma unroll
+        for (int fm = 0; fm < FA; ++fm) af[fm] = as[(fm * 8 + (lane >> 2)) * lda + kk + (lane & 3)];
+#pragma unroll
+        for (int fn = 0; fn < 4; ++fn) bf[fn] = bs[(kk + (lane & 3)) * ldb + fn * 8 + (lane >> 2)];
+#pragma unroll
+        for (int fm = 0; fm < FA; ++fm)
+#pragma unroll
+            for (int fn = 0; fn < 4; ++fn) dmma884(acc[fm][fn], af[fm], bf[fn]);
+    }
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(128, (KMAX <= 64 ? 4 : 3))
+radfwd_wp_kernel(const __grid_constant__ RadFwd pr, const __grid_constant__ TileMap tm) {
+    using W = RadFwdWp<KMAX>;
+    constexpr int ST = W::ST, BK = W::BK, LDA = W::LDA, LDB = W::LDB;
+    extern __shared__ __align__(128) double gsm[];
+    double* As = gsm;
+    double* Bw = gsm + W::A_PANEL + (threadIdx.x >> 5) * (ST * W::B_STAGE);
+    const Tile t = decode_tile<true>(tm, pr.g.NB, blockIdx.x);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int l = t.prob, m0 = t.m0, n0 = t.n0;
+    const int M = pr.M(l), N = pr.N(l), K = pr.K(l);  // K = 2B, a multiple of 8, <= KMAX
+    const int nch = K / BK;
+    {
+        // A panel: rows m0 .. m0 + 31 of W_l (zero past M), K shells each, in 16-byte units
+        const double* a0 = pr.A + pr.rowA(l, m0);
+        const int ku = K / 2, a_sr = pr.a_sr(l);
+        for (int e = tid; e < 32 * ku; e += 128) {
+            const int r = e / ku, k2 = 2 * (e - r * ku);
+            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(As + r * LDA + k2));
+            const bool ok = m0 + r < M;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(ok ? a0 + (long long)r * a_sr + k2 : pr.A),
+                         "r"(ok ? 16 : 0));
+        }
+        cp_async_commit();
+    }
+    // this warp's B pipeline: lane = (shell kq of the chunk, pair group pq); its 4 copies per
+    // chunk are column pairs pq + 4 i of the warp's 16 (S is contiguous over shells per pair)
+    const int kq = lane & 7, pq = lane >> 3;
+    const unsigned bdst = static_cast<unsigned>(__cvta_generic_to_shared(Bw + kq * LDB + 2 * pq));
+    const int nv = t.nseq * nch;
+    int is_chunk = 0, is_tile = 0;
+    const double* bp[4];
+    auto issue = [&](int v) {
+        if (is_chunk == 0) {  // new n-block: the lane's four column-pair pointers (null past N)
+            const int ncol = n0 + is_tile * 128 + 32 * warp + 2 * pq;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int col = ncol + 8 * i;
+                bp[i] = col < N ? pr.Bm + pr.colB(l, col) + 2 * kq : nullptr;
+            }
+        }
+        const unsigned so = bdst + (unsigned)((v % ST) * W::B_STAGE * (int)sizeof(double));
+        const int adv = is_chunk * (2 * BK);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const bool ok = bp[i] != nullptr;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(so + (unsigned)(8 * i * 8)),
+                         "l"(ok ? bp[i] + adv : pr.Bm), "r"(ok ? 16 : 0));
+        }
+        cp_async_commit();
+        if (++is_chunk == nch) {
+            is_chunk = 0;
+            ++is_tile;
+        }
+    };
+#pragma unroll
+    for (int v = 0; v < ST - 1; ++v) {
+        if (v < nv) issue(v);
+        else cp_async_commit();
+    }
+    cp_async_wait_group<ST - 1>();
+    __syncthreads();  // panel visible: the only CTA barrier
+    const int fa = max(0, min(4, (M - m0 + 7) >> 3));
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    int c = 0, tv = 0;
+    for (int v = 0; v < nv; ++v) {
+        cp_async_wait_group<ST - 2>();
+        __syncwarp();
+        if (v + ST - 1 < nv) issue(v + ST - 1);
+        else cp_async_commit();
+        const double* as = As + c * BK;
+        const double* bs = Bw + (v % ST) * W::B_STAGE;
+        switch (fa) {  // 8-row fragments past M skipped (warp-uniform, straight-line MMAs)
+            case 4: radfwd_wp_chunk<4>(as, bs, acc, lane, LDA, LDB); break;
+            case 3: radfwd_wp_chunk<3>(as, bs, acc, lane, LDA, LDB); break;
+            case 2: radfwd_wp_chunk<2>(as, bs, acc, lane, LDA, LDB); break;
+            default: radfwd_wp_chunk<1>(as, bs, acc, lane, LDA, LDB); break;
+        }
+        if (++c == nch) {
+            gemm_epilogue<RadFwd, 1>(pr, l, m0, n0 + tv * 128, M, N, acc, 0, 32 * warp, lane);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            c = 0;
+            ++tv;
+        }
+    }
+    cp_async_wait_group<0>();
+}
+
+bool radfwd_wp_ok(const Geo& g, const RadialBlocks& rb) {
+    return g.B % 4 == 0 && g.B <= 64 && rb.blk_stride == 0 && rb.sc_blk == 2 * g.B;
+}
+
+template <int KMAX>
+static int radfwd_wp_launch(const RadFwd& p, const TileMap* tiles, int ntiles, cudaStream_t s) {
+    const size_t smem = RadFwdWp<KMAX>::smem_bytes();
+    static SmemAttrOnce attr;
+    attr.ensure(radfwd_wp_kernel<KMAX>, smem);
+    radfwd_wp_kernel<KMAX><<<ntiles, 128, smem, s>>>(p, *tiles);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
 // ------------------------------------------------------------------ G layout
 long long g_layout(Geo& g) {
     const int N = 2 * g.B;
@@ -2628,6 +2774,8 @@ int launch_radial_forward(const Geo& g, const RadialBlocks& rb, const double* S,
                           const double* W, const long long* w_off, const TileMap* tiles, int ntiles,
                           cudaStream_t s) {
     RadFwd p{g, W, w_off, S, C, degree_offset(g.B + 1), ShellBlocks{rb.sc_blk, rb.blk_stride, rb.nu0}};
+    if (ntiles > 0 && tiles->seq > 1)  // the tile builder asks for sequences only where radfwd_wp_ok holds
+        return g.B <= 32 ? radfwd_wp_launch<64>(p, tiles, ntiles, s) : radfwd_wp_launch<128>(p, tiles, ntiles, s);
     return gemm_launch<RadFwd>(p, tiles, ntiles, s);
 }
 

@@ -215,6 +215,10 @@ struct RadialBlocks {
     long long blk_stride;
     long long nu0;
 };
+// Does the radial forward of this geometry run on the warp-private kernel
+// (radfwd_wp_kernel: batched small bandlimits)?  The tile builder then emits n-block
+// sequences of 32 x 128 tiles (TileMap::seq > 1), which select that kernel.
+bool radfwd_wp_ok(const Geo& g, const RadialBlocks& rb);
 // Peer destinations for the multi-GPU exchange fused into a stage's epilogue
 // (NVLink peer stores instead of an all-to-all): output row r goes to base[q]
 // for the q with bound[q] <= key(r) < bound[q + 1] (key: l for the Legendre

@@ -13,6 +13,6 @@ for cfg in "C1 --B 16 --batch 1" "C2 --B 64 --batch 64" "C3 --B 128 --batch 1" "
       --e2e-steps 1 --e2e-callers 1 > gpurun_out/${R}_ncu_launch_${name}.log 2>&1
 done
 cp gpurun_out/${R}_launches_C3.csv gpurun_out/${R}_launches.csv
-ncu --set full --import-source on --clock-control none -k regex:"az_|gemm_dmma" -c 6 \
+ncu --set full --import-source on --clock-control none -k regex:"az_|gemm_dmma|leginv_wp|radfwd_wp" -c 6 \
     -o gpurun_out/${R}_full -f python tools/profile_step.py --steps 1 > gpurun_out/${R}_ncu_full.log 2>&1
 echo profile done
