@@ -2076,7 +2076,7 @@ __global__ void __launch_bounds__(128, P::GEMM_MINB) gemm_dmma_kernel(const __gr
 // (cp.async ring private to the warp), waits on its own copies (wait_group +
 // __syncwarp) and never meets the other warps again: no CTA barrier after the panel,
 // warps drift freely across chunks and tiles, one A transfer per problem row block.
-// Used when every n-block is full (NB % 128 == 0), B % 32 == 0 and K <= KMAX.
+// Used when every n-block is full (NB % 128 == 0), B % 32 == 0 and 64 <= B <= 256.
 #ifndef SGL_LEGINV_WP
 #define SGL_LEGINV_WP 1
 #endif
@@ -2234,7 +2234,12 @@ __global__ void __launch_bounds__(128, 4) leginv_wp_kernel(const __grid_constant
     cp_async_wait_group<0>();
 }
 
-bool leginv_wp_ok(const Geo& g) { return g.NB % 128 == 0 && g.B % 32 == 0 && g.B >= 64 && g.B <= 128; }
+bool leginv_wp_ok(const Geo& g) {
+    // B = 256 runs the K <= 128 instantiation at 3 CTAs/SM: 1243 -> 1206 us (SGL_LEGINV_WP_BMAX=128: off)
+    const char* e = std::getenv("SGL_LEGINV_WP_BMAX");
+    const int bmax = e ? std::atoi(e) : 256;
+    return g.NB % 128 == 0 && g.B % 32 == 0 && g.B >= 64 && g.B <= bmax;
+}
 
 template <int KMAX>
 static int leginv_wp_launch(const LegInv& p, const TileMap* tiles, int ntiles, cudaStream_t s) {
@@ -2753,14 +2758,14 @@ int launch_legendre_inverse(const Geo& g, const SView& sv, const double* S, doub
     LegInv p{g, tab, tab_off, S, G, sv};
     {
         // warp-private pipelines: full n-blocks, full 32-row blocks, K <= 64 (B <= 128)
-        static const int wp = [] {
-            const char* e = std::getenv("SGL_LEGINV_WP");
-            return e ? std::atoi(e) : SGL_LEGINV_WP;
-        }();
+        const char* e = std::getenv("SGL_LEGINV_WP");  // read per call (the tests flip it)
+        const int wp = e ? std::atoi(e) : SGL_LEGINV_WP;
         // (B = 32: K <= 16, two chunks per tile -- the panel and its barrier do not pay: 444 -> 488 us
         // for 512 functions; B = 64 x 64: 570 -> 561 us; B = 128: 101.9 -> 97.4 us)
-        if (wp && leginv_wp_ok(g))
-            return g.B <= 64 ? leginv_wp_launch<32>(p, tiles, ntiles, s) : leginv_wp_launch<64>(p, tiles, ntiles, s);
+        if (wp && ntiles > 0 && leginv_wp_ok(g))
+            return g.B <= 64    ? leginv_wp_launch<32>(p, tiles, ntiles, s)
+                   : g.B <= 128 ? leginv_wp_launch<64>(p, tiles, ntiles, s)
+                                : leginv_wp_launch<128>(p, tiles, ntiles, s);
     }
     if (ntiles > 0 && tiles->seq > 1) {
         LegInvSeq q;

@@ -805,3 +805,48 @@ def test_fused_small_bandlimit_path_matches_general_path_and_oracle(B, nb, monke
         assert per_shell(g[b], orc.inverse(cn[b]), B) <= TOL
         assert normwise(f[b], orc.forward(xn[b])) <= TOL
         assert normwise(g[b], g0[b]) <= 1e-14 and normwise(f[b], f0[b]) <= 1e-14
+
+
+@pytest.mark.parametrize("B,nb", [(64, 2), (128, 1), (256, 1)])
+def test_warp_private_legendre_inverse_matches_general_engine_and_oracle(B, nb, monkeypatch):
+    """The default Legendre inverse for 64 <= B <= 256 (leginv_wp_kernel: A panel once per
+    CTA, warp-private cp.async rings) against the general GEMM engine
+    (SGL_LEGINV_WP=0) on the same coefficients, and against the oracle per shell."""
+    import torch
+
+    plan, orc = plan_for(B) if B <= 128 else (sgl.TransformPlan.compute(B), Oracle(B))
+    c = _c4_coefficients(B, 1100 + B, nb) if B == 256 else complex_normal(np.random.default_rng(1100 + B),
+                                                                          (nb, coefficient_count(B)))
+    ct = torch.from_numpy(c).cuda()
+    g = sgl.ifsglft_batch(plan, ct).cpu().numpy()
+    assert np.isfinite(g).all()
+    monkeypatch.setenv("SGL_LEGINV_WP", "0")
+    g0 = sgl.ifsglft_batch(plan, ct).cpu().numpy()
+    for b in range(nb):
+        assert per_shell(g[b], g0[b], B) <= 1e-13
+    assert per_shell(g[0], orc.inverse(c[0]), B) <= TOL
+
+
+def test_real_path_with_sample_buffers_that_are_not_32_byte_aligned():
+    """At B = 32 the real-valued azimuthal kernels use 256-bit sample loads / stores when
+    the sample pointer is 32-byte aligned; a buffer at a 16-byte offset takes the 16-byte
+    kernels and must give the same samples and coefficients."""
+    import torch
+
+    B, nb = 32, 3
+    plan, orc = plan_for(B)
+    rng = np.random.default_rng(1200)
+    c = torch.from_numpy(_real_coeffs(B, nb, rng)).cuda()
+    x = sgl.ifsglft_real_batch(plan, c)
+    assert x.data_ptr() % 32 == 0
+    big = torch.empty(x.numel() + 2, dtype=x.dtype, device=x.device)
+    x_off = big[2:].view_as(x)
+    assert x_off.data_ptr() % 32 == 16
+    sgl.ifsglft_real_batch(plan, c, out=x_off)
+    assert torch.equal(x, x_off) or normwise(x_off.cpu().numpy().ravel(), x.cpu().numpy().ravel()) <= 1e-14
+    f = sgl.fsglft_real_batch(plan, x).cpu().numpy()
+    f_off = sgl.fsglft_real_batch(plan, x_off).cpu().numpy()
+    cn = c.cpu().numpy()
+    for b in range(nb):
+        assert normwise(f_off[b], f[b]) <= 1e-14
+        assert normwise(f[b], cn[b]) <= TOL
