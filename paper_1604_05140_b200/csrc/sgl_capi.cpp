@@ -357,6 +357,14 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
         if (ntiles < 2LL * 4 * p->num_sms) seq = 1;
         if (const char* e = std::getenv("SGL_SEQ")) seq = std::max(1, std::min(8, std::atoi(e)));
     }
+    if (kind == kLegFwd && wp && sub_n == 0) {  // whole-transform Legendre forward on warp-private pipelines
+        sglk::Geo gq{B, SC, batch, NB};
+        gq.real = real ? 1 : 0;
+        if (sglk::legfwd_wp_ok(gq)) {
+            seq = 4;
+            if (const char* e = std::getenv("SGL_SEQ_LEGFWD")) seq = std::max(2, std::min(8, std::atoi(e)));
+        }
+    }
     if (radfwd_wp) {
         seq = 4;
         if (const char* e = std::getenv("SGL_SEQ_RADFWD")) seq = std::max(2, std::min(8, std::atoi(e)));
@@ -698,7 +706,7 @@ int forward_device(sglgpu_plan* p, Work& w, const double* X, double* C, int nb, 
         sglk::Geo gc{B, SC, 1, 2LL * SC};
         w.G.ensure(2 * (size_t)sglk::g_layout(gc));
         const sglk::SView sv{2LL * 2 * B, 2 * B, 0};
-        auto lt = tiles_for(p, kLegFwd, 1, SC, 0, 2 * B);
+        auto lt = tiles_for(p, kLegFwd, 1, SC, 0, 2 * B, false, 0, 0, true);
         if (const int ns = sl.count == 1 && !p->profiling ? pipe_slices(B, nb) : 0) {
             w.ensure_pipe();
             sglk::g_layout(gc);
@@ -758,7 +766,7 @@ int forward_device(sglgpu_plan* p, Work& w, const double* X, double* C, int nb, 
         sglk::Geo g{B, 2 * B, fb, 2LL * fb * 2 * B};
         w.G.ensure(2 * (size_t)sglk::g_layout(g));
         const sglk::SView sv{g.NB, 2 * B, 0};
-        auto lt = tiles_for(p, kLegFwd, fb, 2 * B, 0, 2 * B);
+        auto lt = tiles_for(p, kLegFwd, fb, 2 * B, 0, 2 * B, false, 0, 0, true);
         auto rt = tiles_for(p, kRadFwd, fb, 2 * B, 0, B, false, 0, 0, true);
         k = staged(p, 0, st, [&] {
             return sglk::launch_az_forward(g, X + (size_t)f0 * psi2, psi2, w.G.p, p->d_bcal, p->d_tw, st);
@@ -887,7 +895,7 @@ int real_device(sglgpu_plan* p, Work& w, const double* in, double* out, int nb, 
         w.G.ensure(2 * (size_t)sglk::g_layout(g));
         const sglk::SView sv{g.NB, 2 * B, 0};
         if (forward) {
-            auto lt = tiles_for(p, kLegFwd, fb, 2 * B, 0, 2 * B, true);
+            auto lt = tiles_for(p, kLegFwd, fb, 2 * B, 0, 2 * B, true, 0, 0, true);
             auto rt = tiles_for(p, kRadFwd, fb, 2 * B, 0, B, true, 0, 0, true);
             k = staged(p, 0, st, [&] {
                 return sglk::launch_az_forward_real(g, in + (size_t)f0 * psi, psi, w.G.p, p->d_bcal, p->d_tw, st);

@@ -2396,6 +2396,120 @@ static int radfwd_wp_launch(const RadFwd& p, const TileMap* tiles, int ntiles, c
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
+// ------------------------------------------------------------------ Legendre forward, warp-private pipelines
+// The forward counterpart of leginv_wp_kernel: a CTA takes one 32-row block of a problem
+// (rows = degrees l of one parity) and a sequence of 128-column n-blocks, loads its A
+// panel (32 table rows x K = B polar nodes) once, and each warp streams its own 32 columns
+// (16 shells) of the blocked G through a private cp.async ring -- no CTA barrier per chunk
+// (the general TMA-fed kernel spends 23% of its stall samples at that barrier).  Rows of
+// G are one row stride apart (affine), a lane's column offset is fixed per n-block.
+// 64 <= B <= 128 (the panel is 32 x (B + 4) doubles), full n-blocks.
+// Measured and NOT the default (SGL_LEGFWD_WP=1 turns it on): B = 128 90.7 -> 108.2 us with
+// sequences of 4 (97.2 with 2) -- the 34 KB panel leaves 3 CTAs/SM against the TMA-fed
+// kernel's 5; B = 64 x 64 479.3 -> 476.6 us (HBM-bound either way).
+#ifndef SGL_LEGFWD_WP
+#define SGL_LEGFWD_WP 0
+#endif
+template <int KMAX>
+__global__ void __launch_bounds__(128, (KMAX <= 64 ? 4 : 3))
+legfwd_wp_kernel(const __grid_constant__ LegFwd pr, const __grid_constant__ TileMap tm) {
+    using W = RadFwdWp<KMAX>;  // same shared-memory plan: A panel [row][k], 4 x 4 stages of 8 x 36
+    constexpr int ST = W::ST, BK = W::BK, LDA = W::LDA, LDB = W::LDB;
+    extern __shared__ __align__(128) double gsm[];
+    double* As = gsm;
+    double* Bw = gsm + W::A_PANEL + (threadIdx.x >> 5) * (ST * W::B_STAGE);
+    const Tile t = decode_tile<true>(tm, pr.g.NB, blockIdx.x);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int pid = t.prob, m0 = t.m0, n0 = t.n0;
+    const int M = pr.M(pid), N = pr.nlim(pid, n0), K = pr.K(pid);  // K = B, a multiple of 8, <= KMAX
+    const int nch = K / BK;
+    {
+        const double* a0 = pr.A + pr.rowA(pid, m0);
+        const int ku = K / 2, a_sr = pr.a_sr(pid);
+        for (int e = tid; e < 32 * ku; e += 128) {
+            const int r = e / ku, k2 = 2 * (e - r * ku);
+            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(As + r * LDA + k2));
+            const bool ok = m0 + r < M;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(ok ? a0 + (long long)r * a_sr + k2 : pr.A),
+                         "r"(ok ? 16 : 0));
+        }
+        cp_async_commit();
+    }
+    // lane = (row r0 + 2 i of the chunk, shell u of the warp's 16): one column offset per n-block
+    const int r0 = lane >> 4, u = lane & 15;
+    const unsigned bdst = static_cast<unsigned>(__cvta_generic_to_shared(Bw + r0 * LDB + 2 * u));
+    const int rs = g_rowstride(pr.g);
+    const int nv = t.nseq * nch;
+    int is_chunk = 0, is_tile = 0;
+    const double* bp = pr.Bm;
+    auto issue = [&](int v) {
+        if (is_chunk == 0) bp = pr.Bm + pr.colB(pid, n0 + is_tile * 128 + 32 * warp + 2 * u) + (long long)r0 * rs;
+        const unsigned so = bdst + (unsigned)((v % ST) * W::B_STAGE * (int)sizeof(double));
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(so + (unsigned)(2 * i * LDB * 8)),
+                         "l"(bp + (long long)(2 * i) * rs));
+        cp_async_commit();
+        bp += (long long)BK * rs;
+        if (++is_chunk == nch) {
+            is_chunk = 0;
+            ++is_tile;
+        }
+    };
+#pragma unroll
+    for (int v = 0; v < ST - 1; ++v) {
+        if (v < nv) issue(v);
+        else cp_async_commit();
+    }
+    cp_async_wait_group<ST - 1>();
+    __syncthreads();  // panel visible: the only CTA barrier
+    const int fa = max(0, min(4, (M - m0 + 7) >> 3));
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    int c = 0, tv = 0;
+    for (int v = 0; v < nv; ++v) {
+        cp_async_wait_group<ST - 2>();
+        __syncwarp();
+        if (v + ST - 1 < nv) issue(v + ST - 1);
+        else cp_async_commit();
+        const double* as = As + c * BK;
+        const double* bs = Bw + (v % ST) * W::B_STAGE;
+        switch (fa) {
+            case 4: radfwd_wp_chunk<4>(as, bs, acc, lane, LDA, LDB); break;
+            case 3: radfwd_wp_chunk<3>(as, bs, acc, lane, LDA, LDB); break;
+            case 2: radfwd_wp_chunk<2>(as, bs, acc, lane, LDA, LDB); break;
+            default: radfwd_wp_chunk<1>(as, bs, acc, lane, LDA, LDB); break;
+        }
+        if (++c == nch) {
+            gemm_epilogue<LegFwd, 1>(pr, pid, m0, n0 + tv * 128, M, N, acc, 0, 32 * warp, lane);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            c = 0;
+            ++tv;
+        }
+    }
+    cp_async_wait_group<0>();
+}
+
+bool legfwd_wp_ok(const Geo& g) {
+    const char* e = std::getenv("SGL_LEGFWD_WP");
+    return (e ? std::atoi(e) : SGL_LEGFWD_WP) && g.NB % 128 == 0 && g.B % 32 == 0 && g.B >= 64 && g.B <= 128;
+}
+
+template <int KMAX>
+static int legfwd_wp_launch(const LegFwd& p, const TileMap* tiles, int ntiles, cudaStream_t s) {
+    const size_t smem = RadFwdWp<KMAX>::smem_bytes();
+    static SmemAttrOnce attr;
+    attr.ensure(legfwd_wp_kernel<KMAX>, smem);
+    legfwd_wp_kernel<KMAX><<<ntiles, 128, smem, s>>>(p, *tiles);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
 // ------------------------------------------------------------------ G layout
 long long g_layout(Geo& g) {
     const int N = 2 * g.B;
@@ -2725,6 +2839,8 @@ int launch_spherical_forward_fused(const Geo& g, const double* X, size_t sample_
 int launch_legendre_forward(const Geo& g, const SView& sv, const double* G, double* S, const double* tab,
                             const long long* tab_off, const TileMap* tiles, int ntiles, cudaStream_t s) {
     LegFwd p{g, tab, tab_off, G, S, sv};
+    if (ntiles > 0 && tiles->seq > 1)  // the tile builder emits sequences only where legfwd_wp_ok holds
+        return g.B <= 64 ? legfwd_wp_launch<64>(p, tiles, ntiles, s) : legfwd_wp_launch<128>(p, tiles, ntiles, s);
     if (SGL_LEGFWD_TMA) {
         LegFwdTma q;
         static_cast<LegFwd&>(q) = p;

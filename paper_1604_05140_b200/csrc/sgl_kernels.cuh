@@ -215,6 +215,9 @@ struct RadialBlocks {
     long long blk_stride;
     long long nu0;
 };
+// ... and the Legendre forward (legfwd_wp_kernel; the tile builder then emits n-block
+// sequences, TileMap::seq > 1, which select it in launch_legendre_forward).
+bool legfwd_wp_ok(const Geo& g);
 // Does the radial forward of this geometry run on the warp-private kernel
 // (radfwd_wp_kernel: batched small bandlimits)?  The tile builder then emits n-block
 // sequences of 32 x 128 tiles (TileMap::seq > 1), which select that kernel.
