@@ -2080,17 +2080,27 @@ __global__ void __launch_bounds__(128, P::GEMM_MINB) gemm_dmma_kernel(const __gr
 #ifndef SGL_LEGINV_WP
 #define SGL_LEGINV_WP 1
 #endif
-template <int KMAX>
+#ifndef SGL_LEGINV_WP_SWZ
+#define SGL_LEGINV_WP_SWZ 0
+#endif
+// SWZ: unpadded 32-double rows with an XOR swizzle (element (k, x) of the panel or of a
+// ring stage at k * 32 + (x ^ 4 (k & 3)): a DMMA fragment's 4 k x 4 rows / columns still
+// cover 16 distinct doubles of a 128-byte line, 16-byte units stay intact) and 3 ring
+// stages -- 40 KB per CTA at K <= 64, so 5 CTAs per SM fit instead of 4.
+template <int KMAX, bool SWZ>
 struct LegInvWp {
-    static constexpr int ST = 4, BK = 8, LDA = 36, LDB = 36;
-    static constexpr int A_PANEL = KMAX * LDA;        // doubles: [k][row], rows padded to 36
+    static constexpr int ST = SWZ ? 3 : 4, BK = 8, LDA = SWZ ? 32 : 36, LDB = LDA;
+    static constexpr int A_PANEL = KMAX * LDA;        // doubles: [k][row]
     static constexpr int B_STAGE = BK * LDB;          // doubles per warp and stage
+    static constexpr int MINB = SWZ ? 5 : (KMAX <= 64 ? 4 : 3);
     static constexpr size_t smem_bytes() { return sizeof(double) * (A_PANEL + 4 * ST * B_STAGE); }
+    static __host__ __device__ constexpr int sw(int k) { return SWZ ? 4 * (k & 3) : 0; }
 };
 
-template <int KMAX>
-__global__ void __launch_bounds__(128, 4) leginv_wp_kernel(const __grid_constant__ LegInv pr, const __grid_constant__ TileMap tm) {
-    using W = LegInvWp<KMAX>;
+template <int KMAX, bool SWZ>
+__global__ void __launch_bounds__(128, (LegInvWp<KMAX, SWZ>::MINB))
+leginv_wp_kernel(const __grid_constant__ LegInv pr, const __grid_constant__ TileMap tm) {
+    using W = LegInvWp<KMAX, SWZ>;
     constexpr int ST = W::ST, BK = W::BK, LDA = W::LDA, LDB = W::LDB;
     extern __shared__ __align__(128) double gsm[];
     double* As = gsm;
@@ -2108,7 +2118,7 @@ __global__ void __launch_bounds__(128, 4) leginv_wp_kernel(const __grid_constant
         const int a_sk = pr.a_sk(pid);
         for (int e = tid; e < kr * 16; e += 128) {  // 16-byte units: k = e / 16, rows 2 (e % 16), +1
             const int k = e >> 4, r = (e & 15) * 2;
-            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(As + k * LDA + r));
+            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(As + k * LDA + (r ^ W::sw(k))));
             const bool ok = k < K;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(ok ? a0 + (long long)k * a_sk + r : pr.A),
                          "r"(ok ? 16 : 0));
@@ -2122,7 +2132,9 @@ __global__ void __launch_bounds__(128, 4) leginv_wp_kernel(const __grid_constant
     //   off(l + 16) = off(l) + 16 e + 256 NB,  off(l + 4 i) = off(l) + 4 i e + 16 i^2 NB.
     const int r0 = lane >> 4, u = lane & 15;
     const double* bcol = pr.Bm + pr.colB(pid, n0) + 32 * warp + 2 * u;
-    const unsigned bdst = static_cast<unsigned>(__cvta_generic_to_shared(Bw + r0 * LDB + 2 * u));
+    // ring rows r0, r0 + 4 (copies 0, 2) and r0 + 2, r0 + 6 (copies 1, 3) share a swizzle
+    const unsigned bdst = static_cast<unsigned>(__cvta_generic_to_shared(Bw + r0 * LDB + ((2 * u) ^ W::sw(r0))));
+    const unsigned bdst2 = static_cast<unsigned>(__cvta_generic_to_shared(Bw + (r0 + 2) * LDB + ((2 * u) ^ W::sw(r0 + 2))));
     const int nv = t.nseq * nch;
     const int snb = (int)pr.sv.NB;
     const int la0 = pr.am(pid) + (pid & 1) + 2 * r0;
@@ -2131,21 +2143,22 @@ __global__ void __launch_bounds__(128, 4) leginv_wp_kernel(const __grid_constant
     int is_chunk = 0;
     const double* bcs = bcol;  // + 128 per finished tile
     auto issue = [&](int v) {
-        const unsigned so = bdst + (unsigned)((v % ST) * W::B_STAGE * (int)sizeof(double));
+        const unsigned sto = (unsigned)((v % ST) * W::B_STAGE * (int)sizeof(double));
+        const unsigned so = bdst + sto, so2 = bdst2 + sto;
         const int o1 = off + 4 * e + 16 * snb, o2 = off + 8 * e + 64 * snb, o3 = off + 12 * e + 144 * snb;
         const bool tail = is_chunk == nch - 1;
         if (!tail || K == kr) {  // every row of the chunk inside K (uniform)
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(so), "l"(bcs + off));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(so + 2u * LDB * 8u), "l"(bcs + o1));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(so2), "l"(bcs + o1));
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(so + 4u * LDB * 8u), "l"(bcs + o2));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(so + 6u * LDB * 8u), "l"(bcs + o3));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(so2 + 4u * LDB * 8u), "l"(bcs + o3));
         } else {
             const int kb = is_chunk * BK + r0;
             const int oo[4] = {off, o1, o2, o3};
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const bool ok = kb + 2 * i < K;
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(so + (unsigned)(2 * i * LDB * 8)),
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(((i & 1) ? so2 : so) + (unsigned)((i >> 1) * 4 * LDB * 8)),
                              "l"(ok ? bcs + oo[i] : pr.Bm), "r"(ok ? 16 : 0));
             }
         }
@@ -2188,9 +2201,9 @@ __global__ void __launch_bounds__(128, 4) leginv_wp_kernel(const __grid_constant
             if (kk >= ksteps) break;
             double af[4], bf[4];
 #pragma unroll
-            for (int fm = 0; fm < 4; ++fm) af[fm] = as[(kk + (lane & 3)) * LDA + fm * 8 + (lane >> 2)];
+            for (int fm = 0; fm < 4; ++fm) af[fm] = as[(kk + (lane & 3)) * LDA + ((fm * 8 + (lane >> 2)) ^ W::sw(lane & 3))];
 #pragma unroll
-            for (int fn = 0; fn < 4; ++fn) bf[fn] = bs[(kk + (lane & 3)) * LDB + fn * 8 + (lane >> 2)];
+            for (int fn = 0; fn < 4; ++fn) bf[fn] = bs[(kk + (lane & 3)) * LDB + ((fn * 8 + (lane >> 2)) ^ W::sw(lane & 3))];
 #pragma unroll
             for (int fm = 0; fm < 4; ++fm)
 #pragma unroll
@@ -2241,12 +2254,12 @@ bool leginv_wp_ok(const Geo& g) {
     return g.NB % 128 == 0 && g.B % 32 == 0 && g.B >= 64 && g.B <= bmax;
 }
 
-template <int KMAX>
+template <int KMAX, bool SWZ>
 static int leginv_wp_launch(const LegInv& p, const TileMap* tiles, int ntiles, cudaStream_t s) {
-    const size_t smem = LegInvWp<KMAX>::smem_bytes();
+    const size_t smem = LegInvWp<KMAX, SWZ>::smem_bytes();
     static SmemAttrOnce attr;
-    attr.ensure(leginv_wp_kernel<KMAX>, smem);
-    leginv_wp_kernel<KMAX><<<ntiles, 128, smem, s>>>(p, *tiles);
+    attr.ensure(leginv_wp_kernel<KMAX, SWZ>, smem);
+    leginv_wp_kernel<KMAX, SWZ><<<ntiles, 128, smem, s>>>(p, *tiles);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -2879,9 +2892,14 @@ int launch_legendre_inverse(const Geo& g, const SView& sv, const double* S, doub
         // (B = 32: K <= 16, two chunks per tile -- the panel and its barrier do not pay: 444 -> 488 us
         // for 512 functions; B = 64 x 64: 570 -> 561 us; B = 128: 101.9 -> 97.4 us)
         if (wp && ntiles > 0 && leginv_wp_ok(g))
-            return g.B <= 64    ? leginv_wp_launch<32>(p, tiles, ntiles, s)
-                   : g.B <= 128 ? leginv_wp_launch<64>(p, tiles, ntiles, s)
-                                : leginv_wp_launch<128>(p, tiles, ntiles, s);
+        {
+            const char* z = std::getenv("SGL_LEGINV_WP_SWZ");  // 5-CTA swizzled form (K <= 64)
+            const bool swz = z ? std::atoi(z) != 0 : SGL_LEGINV_WP_SWZ != 0;
+            if (g.B > 128) return leginv_wp_launch<128, false>(p, tiles, ntiles, s);
+            if (g.B <= 64)
+                return swz ? leginv_wp_launch<32, true>(p, tiles, ntiles, s) : leginv_wp_launch<32, false>(p, tiles, ntiles, s);
+            return swz ? leginv_wp_launch<64, true>(p, tiles, ntiles, s) : leginv_wp_launch<64, false>(p, tiles, ntiles, s);
+        }
     }
     if (ntiles > 0 && tiles->seq > 1) {
         LegInvSeq q;
