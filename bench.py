@@ -34,7 +34,7 @@ sys.path.insert(0, REPO)
 sys.path.insert(0, os.path.join(REPO, "tests"))
 
 FP64_PEAK_TFLOPS = 37.1  # measured DMMA m8n8k4 peak on this pool's B200 (profiles/fp64_peak_r01.txt)
-TRAFFIC_FILE = "r02f_traffic.json"  # per-kernel DRAM bytes of the committed ncu capture (B = 128, one function)
+TRAFFIC_FILE = "r02g_traffic.json"  # per-kernel DRAM bytes of the committed ncu capture (B = 128, one function)
 
 
 def KERNEL_NAMES(B):  # noqa: N802 -- ncu names of each stage's kernels
