@@ -530,6 +530,14 @@ int pipe_slices(int B, int nb) {
     return (B / 32) % ns == 0 ? ns : 0;
 }
 
+// 16-shell G groups for large complex batches at B = 64 (sglk::Geo::az2x): -72 us per round
+// trip of 64 functions (Legendre -106, azimuthal +35), even at 8, worse for one.
+bool az2x_on(int B, int fb) {
+    const char* e = std::getenv("SGL_AZ2X");
+    if (e) return std::atoi(e) != 0 && B == 64;
+    return B == 64 && fb >= 32;
+}
+
 // Brackets one stage launch with events when profiling is on.
 template <class F>
 int staged(sglgpu_plan* p, int stage, cudaStream_t st, F&& launch) {
@@ -764,6 +772,7 @@ int forward_device(sglgpu_plan* p, Work& w, const double* X, double* C, int nb, 
     for (int f0 = 0; f0 < nb; f0 += sl.functions) {
         const int fb = std::min(sl.functions, nb - f0);
         sglk::Geo g{B, 2 * B, fb, 2LL * fb * 2 * B};
+        g.az2x = az2x_on(B, fb);
         w.G.ensure(2 * (size_t)sglk::g_layout(g));
         const sglk::SView sv{g.NB, 2 * B, 0};
         auto lt = tiles_for(p, kLegFwd, fb, 2 * B, 0, 2 * B, false, 0, 0, true);
@@ -853,6 +862,7 @@ int inverse_device(sglgpu_plan* p, Work& w, const double* C, double* X, int nb, 
     for (int f0 = 0; f0 < nb; f0 += sl.functions) {
         const int fb = std::min(sl.functions, nb - f0);
         sglk::Geo g{B, 2 * B, fb, 2LL * fb * 2 * B};
+        g.az2x = az2x_on(B, fb);
         w.G.ensure(2 * (size_t)sglk::g_layout(g));
         const sglk::SView sv{g.NB, 2 * B, 0};
         auto rt = tiles_for(p, kRadInv, fb, 2 * B, 0, B);

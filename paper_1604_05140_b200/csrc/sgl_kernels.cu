@@ -124,6 +124,11 @@ __device__ __forceinline__ int phys(int x) { return x + (x >> 4); }
 #ifndef SGL_AZ_BIG512
 #define SGL_AZ_BIG512 1
 #endif
+// Geo::az2x (set by the host for large complex batches at B = 64): azimuthal CTAs of twice
+// the elements -- 16-shell G groups, twice as long runs for the Legendre GEMMs.  Measured
+// (B = 64 x 64, us): az 667 / 680 -> 673 / 708, legendre 479 / 564 -> 435 / 502: -72 per round
+// trip; even at 8 functions, worse for one (and for the real path: not used there).
+constexpr int kAz2xElems = 2 * SGL_AZ_ELEMS;
 
 template <int N, int ELEMS = SGL_AZ_ELEMS>
 struct FFTShape {
@@ -416,11 +421,11 @@ __device__ __forceinline__ long long g_block(const Geo& g, int jp, int s0) {
 // (jp, 2B-1-jp), on `rings` (2 IG padded rings of shared memory).  Called by
 // az_forward_kernel (one item per CTA) and by the fused persistent spherical
 // forward (sph_fwd_fused_kernel).
-template <int N>
+template <int N, int ELEMS = SGL_AZ_ELEMS>
 __device__ __forceinline__ void az_fwd_item(const Geo& g, const double2* __restrict__ X, size_t fstride,
                                             double2* __restrict__ G, const double* __restrict__ bcal,
                                             const double2* __restrict__ twg, int s0, int jp, double2* rings) {
-    using S = FFTShape<N>;
+    using S = FFTShape<N, ELEMS>;
     constexpr int B = N / 2;
     const int tid = threadIdx.x;
     const int nshell = g.batch * g.SC;
@@ -521,14 +526,14 @@ __device__ __forceinline__ void az_fwd_item(const Geo& g, const double2* __restr
     }
 }
 
-template <int N>
-__global__ void __launch_bounds__(FFTShape<N>::THREADS, FFTShape<N>::MINB)
+template <int N, int ELEMS = SGL_AZ_ELEMS>
+__global__ void __launch_bounds__((FFTShape<N, ELEMS>::THREADS), (FFTShape<N, ELEMS>::MINB))
 az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2* __restrict__ G,
                   const double* __restrict__ bcal, const double2* __restrict__ twg) {
     extern __shared__ double2 smem[];
     const int bx = (SGL_AZF_REV ? gridDim.x - 1 - blockIdx.x : blockIdx.x) + g.gx0;
     const int by = (SGL_AZF_REV ? gridDim.y - 1 - blockIdx.y : blockIdx.y) + g.jp0;
-    az_fwd_item<N>(g, X, fstride, G, bcal, twg, bx * FFTShape<N>::IG, by, smem);
+    az_fwd_item<N, ELEMS>(g, X, fstride, G, bcal, twg, bx * FFTShape<N, ELEMS>::IG, by, smem);
 }
 
 // ------------------------------------------------------------------ azimuthal inverse
@@ -536,11 +541,11 @@ az_forward_kernel(Geo g, const double2* __restrict__ X, size_t fstride, double2*
 // into the ring-(2B-1-j') buffer.  The first FFT pass reads E +- O straight
 // from both buffers (Nyquist bin B zero); the last pass writes the psi-order
 // samples straight to HBM (coalesced).
-template <int N>
-__global__ void __launch_bounds__(FFTShape<N, SGL_AZI_ELEMS>::THREADS, (FFTShape<N, SGL_AZI_ELEMS>::MINB))
+template <int N, int ELEMS = SGL_AZI_ELEMS>
+__global__ void __launch_bounds__((FFTShape<N, ELEMS>::THREADS), (FFTShape<N, ELEMS>::MINB))
 az_inverse_kernel(Geo g, const double2* __restrict__ G, double2* __restrict__ X, size_t fstride,
                   const double2* __restrict__ twg) {
-    using S = FFTShape<N, SGL_AZI_ELEMS>;
+    using S = FFTShape<N, ELEMS>;
     constexpr int B = N / 2;
     extern __shared__ double2 smem[];
     // the plain twiddle table staged in shared memory under the prologue barrier
@@ -2534,7 +2539,7 @@ long long g_layout(Geo& g) {
         case 16: gib = FFTShape<16>::IG; break;
         case 32: gib = FFTShape<32>::IG; break;
         case 64: gib = FFTShape<64>::IG; break;
-        case 128: gib = FFTShape<128>::IG; break;
+        case 128: gib = g.az2x && !g.real ? FFTShape<128, kAz2xElems>::IG : FFTShape<128>::IG; break;
         case 256: gib = FFTShape<256>::IG; break;
         case 512: gib = FFTShape<512>::IG; break;
         default: gib = 1; break;  // naive DFT kernels: one shell per CTA
@@ -2550,32 +2555,33 @@ long long g_layout(Geo& g) {
 }
 
 // ------------------------------------------------------------------ launchers
-template <int N>
+template <int N, int ELEMS = SGL_AZ_ELEMS>
 static int az_fwd_launch(const Geo& g, const double* X, size_t fstride, double* G, const double* bcal,
                          const double* tw, cudaStream_t s) {
-    using S = FFTShape<N>;
+    using S = FFTShape<N, ELEMS>;
     const size_t smem = sizeof(double2) * (2 * S::IG * S::STRIDE);
     static SmemAttrOnce attr;
-    attr.ensure(az_forward_kernel<N>, smem);
+    attr.ensure(az_forward_kernel<N, ELEMS>, smem);
     const int nshell = g.batch * g.SC;
     dim3 grid(g.gxn ? g.gxn : (nshell + S::IG - 1) / S::IG, g.jpn ? g.jpn : g.B);
-    az_forward_kernel<N><<<grid, S::THREADS, smem, s>>>(g, reinterpret_cast<const double2*>(X), fstride / 2,
+    az_forward_kernel<N, ELEMS><<<grid, S::THREADS, smem, s>>>(g, reinterpret_cast<const double2*>(X), fstride / 2,
                                                          reinterpret_cast<double2*>(G), bcal,
                                                          reinterpret_cast<const double2*>(tw));
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-template <int N>
+template <int N, int ELEMS = SGL_AZI_ELEMS>
 static int az_inv_launch(const Geo& g, const double* G, double* X, size_t fstride, const double* tw,
                          cudaStream_t s) {
-    using S = FFTShape<N, SGL_AZI_ELEMS>;
-    static_assert(S::IG == FFTShape<N>::IG, "forward and inverse azimuthal tiles must match the G blocking");
+    using S = FFTShape<N, ELEMS>;
+    static_assert(ELEMS != SGL_AZI_ELEMS || S::IG == FFTShape<N>::IG,
+                  "forward and inverse azimuthal tiles must match the G blocking");
     const size_t smem = sizeof(double2) * (2 * S::IG * S::STRIDE);
     static SmemAttrOnce attr;
-    attr.ensure(az_inverse_kernel<N>, smem);
+    attr.ensure(az_inverse_kernel<N, ELEMS>, smem);
     const int nshell = g.batch * g.SC;
     dim3 grid(g.gxn ? g.gxn : (nshell + S::IG - 1) / S::IG, g.jpn ? g.jpn : g.B);
-    az_inverse_kernel<N><<<grid, S::THREADS, smem, s>>>(g, reinterpret_cast<const double2*>(G),
+    az_inverse_kernel<N, ELEMS><<<grid, S::THREADS, smem, s>>>(g, reinterpret_cast<const double2*>(G),
                                                          reinterpret_cast<double2*>(X), fstride / 2,
                                                          reinterpret_cast<const double2*>(tw));
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
@@ -2591,7 +2597,9 @@ int launch_az_forward(const Geo& g, const double* samples, size_t sample_stride,
         case 16: return az_fwd_launch<16>(g, samples, sample_stride, G, bcal, twiddle, s);
         case 32: return az_fwd_launch<32>(g, samples, sample_stride, G, bcal, twiddle, s);
         case 64: return az_fwd_launch<64>(g, samples, sample_stride, G, bcal, twiddle, s);
-        case 128: return az_fwd_launch<128>(g, samples, sample_stride, G, bcal, twiddle, s);
+        case 128:
+            return g.az2x ? az_fwd_launch<128, kAz2xElems>(g, samples, sample_stride, G, bcal, twiddle, s)
+                          : az_fwd_launch<128>(g, samples, sample_stride, G, bcal, twiddle, s);
         case 256: return az_fwd_launch<256>(g, samples, sample_stride, G, bcal, twiddle, s);
         case 512: return az_fwd_launch<512>(g, samples, sample_stride, G, bcal, twiddle, s);
         default: break;
@@ -2613,7 +2621,9 @@ int launch_az_inverse(const Geo& g, const double* G, double* samples, size_t sam
         case 16: return az_inv_launch<16>(g, G, samples, sample_stride, twiddle, s);
         case 32: return az_inv_launch<32>(g, G, samples, sample_stride, twiddle, s);
         case 64: return az_inv_launch<64>(g, G, samples, sample_stride, twiddle, s);
-        case 128: return az_inv_launch<128>(g, G, samples, sample_stride, twiddle, s);
+        case 128:
+            return g.az2x ? az_inv_launch<128, kAz2xElems>(g, G, samples, sample_stride, twiddle, s)
+                          : az_inv_launch<128>(g, G, samples, sample_stride, twiddle, s);
         case 256: return az_inv_launch<256>(g, G, samples, sample_stride, twiddle, s);
         case 512: return az_inv_launch<512>(g, G, samples, sample_stride, twiddle, s);
         default: break;
@@ -2715,7 +2725,9 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 template <int N>
 __global__ void __launch_bounds__(128, 4)
 sph_fwd_fused_kernel(const __grid_constant__ SphFwdFused prm, const __grid_constant__ TileMap tm) {
-    static_assert(FFTShape<N>::THREADS == 128, "fused items share 128-thread CTAs");
+    if constexpr (FFTShape<N>::THREADS != 128) {  // fused items share 128-thread CTAs (the launcher declines)
+        return;
+    } else {
     extern __shared__ __align__(128) double gsm[];
     __shared__ int s_item, s_last;
     const int tid = threadIdx.x;
@@ -2785,11 +2797,13 @@ sph_fwd_fused_kernel(const __grid_constant__ SphFwdFused prm, const __grid_const
             }
         }
     }
+    }
 }
 
 template <int N>
 static int sph_fwd_fused_launch(const SphFwdFused& prm, const TileMap* tiles, int grid, cudaStream_t s) {
     using S = FFTShape<N>;
+    if (S::THREADS != 128) return -2;  // fused items share 128-thread CTAs: the caller takes the staged path
     constexpr size_t az_smem = sizeof(double2) * (2 * S::IG * S::STRIDE);
     constexpr size_t gm_smem = gemm_smem_bytes<LegFwdSlice>();
     constexpr size_t smem = az_smem > gm_smem ? az_smem : gm_smem;

@@ -110,6 +110,9 @@ struct Geo {
     // Sub-range of the azimuthal launch (the pipelined spherical stage, sgl_capi.cpp):
     // polar nodes j' in [jp0, jp0 + jpn) and shell groups [gx0, gx0 + gxn); 0 counts = all.
     int jp0 = 0, jpn = 0, gx0 = 0, gxn = 0;
+    // complex path, 2B = 128: azimuthal CTAs of twice the elements (16-shell G groups); set by the
+    // host for large batches before g_layout()
+    int az2x = 0;
 };
 
 // Complex index of G(p, bin, j', flat shell s).
