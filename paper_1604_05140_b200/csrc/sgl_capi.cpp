@@ -346,11 +346,12 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
         // measured: B = 32, 64: 4; B = 128: 2; B = 256: the one-tile kernel (seq 2: +4%)
         seq = kmax <= 32 ? 4 : kmax <= 64 ? 2 : 1;
         {
-            // the warp-private kernel loads its A panel once per sequence: 4 n-blocks
-            // (B = 128: 97.3 us with 2, 96.5 with 4, 96.4 with 8)
+            // the warp-private kernel loads its A panel once per sequence: 4 n-blocks at B >= 128
+            // (B = 128: 95.2 us with 2, 94.8 with 4), 2 at B = 64, whose panel is small (B = 64 x 64:
+            // 556 us with 1, 482 with 2, 493 with 3, 501 with 4, 526 with 8)
             const char* e = std::getenv("SGL_LEGINV_WP");
             sglk::Geo gq{B, SC, batch, NB};
-            if ((!e || std::atoi(e)) && sglk::leginv_wp_ok(gq)) seq = 4;
+            if ((!e || std::atoi(e)) && sglk::leginv_wp_ok(gq)) seq = kmax <= 32 ? 2 : 4;
         }
         // sequences pay only when the launch is several waves deep: a single B = 64
         // function (~1k tiles) runs 18.7 -> 17.1 us without them
