@@ -351,7 +351,7 @@ std::pair<sglk::TileMap*, int> tiles_for(sglgpu_plan* p, Kind kind, int batch, i
             // 556 us with 1, 482 with 2, 493 with 3, 501 with 4, 526 with 8)
             const char* e = std::getenv("SGL_LEGINV_WP");
             sglk::Geo gq{B, SC, batch, NB};
-            if ((!e || std::atoi(e)) && sglk::leginv_wp_ok(gq)) seq = kmax <= 32 ? 2 : 4;
+            if ((!e || std::atoi(e)) && sglk::leginv_wp_ok(gq)) seq = kmax <= 32 ? 2 : kmax <= 64 ? 4 : 8;  // B = 256: 1190 us with 4, 1182 with 8
         }
         // sequences pay only when the launch is several waves deep: a single B = 64
         // function (~1k tiles) runs 18.7 -> 17.1 us without them
