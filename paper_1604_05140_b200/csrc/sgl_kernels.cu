@@ -2226,9 +2226,15 @@ leginv_wp_kernel(const __grid_constant__ LegInv pr, const __grid_constant__ Tile
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {  // sign-bit flips: no FP64 pipe work
-                            acc[i][j][0] = __longlong_as_double(__double_as_longlong(acc[i][j][0]) ^ (1LL << 63));
-                            acc[i][j][1] = __longlong_as_double(__double_as_longlong(acc[i][j][1]) ^ (1LL << 63));
+                        for (int j = 0; j < 4; ++j) {
+                            // sign-bit flips on the integer pipe (a plain negation, and an XOR with a
+                            // constant mask too, compile to DADD: FP64 pipe work next to the DMMAs)
+#pragma unroll
+                            for (int c2 = 0; c2 < 2; ++c2) {
+                                int hi = __double2hiint(acc[i][j][c2]);
+                                asm volatile("xor.b32 %0, %0, 0x80000000;" : "+r"(hi));
+                                acc[i][j][c2] = __hiloint2double(hi, __double2loint(acc[i][j][c2]));
+                            }
                         }
                 }
                 const int rs = g_rowstride(pr.g);
