@@ -41,8 +41,8 @@ def KERNEL_NAMES(B):  # noqa: N802 -- ncu names of each stage's kernels
     return {0: [f"void az_forward_kernel<{2 * B}>"],
             1: ["void gemm_dmma_kernel<LegFwdTma>", "void gemm_dmma_kernel<LegFwd>"],
             2: ["void gemm_dmma_kernel<RadFwd>"], 3: ["void gemm_dmma_kernel<RadInv>"],
-            4: ["void leginv_wp_kernel<64>", "void leginv_wp_kernel<32>", "void gemm_dmma_kernel<LegInvSeq>",
-                "void gemm_dmma_kernel<LegInv>"],
+            4: ["void leginv_wp_kernel<64, 0>", "void leginv_wp_kernel<32, 0>", "void leginv_wp_kernel<128, 0>",
+                "void leginv_wp_kernel<64>", "void gemm_dmma_kernel<LegInvSeq>", "void gemm_dmma_kernel<LegInv>"],
             5: [f"void az_inverse_kernel<{2 * B}>"],
             6: [f"void sph_fwd_fused_kernel<{2 * B}>"], 7: [f"void sph_inv_fused_kernel<{2 * B}>"]}
 
